@@ -1,0 +1,256 @@
+/*
+ * kamino_b200.h — C-ABI of the B200-native per-step PADMM forward-dynamics solve.
+ *
+ * This is the drop-in boundary for the reference's C++ solver/world/step API
+ * (/root/reference/proj/include/loopdyn/ *.hpp).  Every entry point below names
+ * the reference interface it replaces (file:line).  Signatures carry only plain
+ * pointers, sizes and POD structs — no torch, no Eigen, no C++ types — so the
+ * reference-side C++ wrapper (include/loopdyn_b200/) or a ctypes
+ * binding can call it directly.
+ *
+ * Conventions (reference se3.hpp:14-18): quaternions are Hamilton, serialized
+ * scalar-first [w,x,y,z]; a pose maps body to world; twists are world-frame
+ * [linear; angular].  Batch storage is the reference WorldBatch layout
+ * (batch.hpp:41-42): 7 doubles per body pose [x y z qw qx qy qz], 6 doubles per
+ * body twist, per-world prefix-sum offsets in world order.
+ *
+ * Errors: every function returns an int status (KD_OK = 0).  The reference
+ * throws ModelError{Code} (model.hpp:76-94), SceneError (scene.hpp:74-77) and
+ * std::runtime_error on an LLT failure (delassus.cpp:209-215); here those are
+ * status codes plus a thread-local message from kd_last_error().  Solver
+ * non-convergence and CR breakdown are flags in kd_step_diag, never errors
+ * (padmm.cpp:154-157, delassus.cpp:196).
+ */
+#ifndef KAMINO_B200_H
+#define KAMINO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------------- */
+enum {
+  KD_OK = 0,
+  /* ModelError::Code (model.hpp:78-88), offset by 1 so 0 stays "ok" */
+  KD_ERR_MODEL_INVALID_REFERENCE = 1,
+  KD_ERR_MODEL_NON_UNIT_AXIS = 2,
+  KD_ERR_MODEL_BAD_INERTIA = 3,
+  KD_ERR_MODEL_BAD_LIMITS = 4,
+  KD_ERR_MODEL_UNSUPPORTED_ON_JOINT_TYPE = 5,
+  KD_ERR_MODEL_BAD_GEOMETRY = 6,
+  KD_ERR_MODEL_UNSUPPORTED_COLLISION_PAIR = 7,
+  KD_ERR_MODEL_WRONG_JOINT_TYPE = 8,
+  KD_ERR_MODEL_DUPLICATE_NAME = 9,
+  /* runtime */
+  KD_ERR_INVALID_ARGUMENT = 20,
+  KD_ERR_CUDA = 21,
+  KD_ERR_SPD_FAILURE = 22, /* "Delassus factorization failed on an SPD system" (delassus.cpp:212) */
+  KD_ERR_CAPACITY = 23,
+  KD_ERR_NO_DEVICE = 24
+};
+
+/* ---- scene description (mirrors SceneDescription, scene.hpp:15-72) --------- */
+typedef struct kd_body_desc {
+  const char* name;
+  double mass;
+  double inertia[9];          /* row-major 3x3 body-frame inertia about the COM */
+  double position[3];
+  double orientation[4];      /* [w,x,y,z] */
+  double linear_velocity[3];
+  double angular_velocity[3];
+} kd_body_desc;
+
+typedef struct kd_joint_desc {
+  const char* name;
+  const char* type;           /* "fixed" | "revolute" | "prismatic" | "spherical" */
+  const char* parent;         /* body name or "world" */
+  const char* child;
+  double parent_position[3];
+  double parent_orientation[4];
+  double child_position[3];
+  double child_orientation[4];
+  double axis[3];
+  int32_t has_limits;
+  double lower, upper;
+  double kp, kd;
+  int32_t has_target;         /* std::optional<double> target (scene.hpp:34) */
+  double target;
+  double target_rate;
+  double armature;
+  double damping;
+} kd_joint_desc;
+
+typedef struct kd_geom_desc {
+  const char* body;           /* "world" for planes */
+  const char* shape;          /* "sphere" | "plane" | "box" */
+  double radius;
+  double half_extents[3];
+  double normal[3];
+  double offset;
+  double mu;
+  double restitution;
+} kd_geom_desc;
+
+typedef struct kd_scene_desc {
+  const char* name;
+  double gravity[3];
+  int32_t n_bodies;
+  const kd_body_desc* bodies;
+  int32_t n_joints;
+  const kd_joint_desc* joints;
+  int32_t n_geoms;
+  const kd_geom_desc* geoms;
+} kd_scene_desc;
+
+/* ---- step configuration (StepConfig stepper.hpp:16-34 + PadmmConfig padmm.hpp:8-17) */
+enum { KD_INTEGRATOR_SEMI_IMPLICIT_EULER = 0, KD_INTEGRATOR_MOREAU_JEAN = 1 };
+enum { KD_BACKEND_DENSE = 0, KD_BACKEND_MATRIX_FREE = 1, KD_BACKEND_AUTO = 2 }; /* delassus.hpp:85 */
+#define KD_DENSE_ROW_CROSSOVER 300 /* kDenseRowCrossover, delassus.hpp:89 */
+
+typedef struct kd_step_config {
+  double dt;                      /* 1/240 */
+  int32_t integrator;             /* KD_INTEGRATOR_* (default semi-implicit Euler) */
+  int32_t backend;                /* KD_BACKEND_* (default Auto) */
+  double eta;                     /* 1e-6 */
+  double rho;                     /* 0.1 (padmm.hpp:10) */
+  double eps;                     /* 1e-6 */
+  int32_t max_iters;              /* 200 */
+  int32_t acceleration;           /* 1 */
+  int32_t restart;                /* 1 */
+  int32_t fixed_iteration_mode;   /* 0 */
+  int32_t cr_iters;               /* 9 */
+  double baumgarte_beta;          /* 0.2 */
+  double contact_margin;          /* 0.01 */
+  double impact_velocity_threshold; /* 0.1 */
+  double bias_clamp;              /* 10 */
+  double limit_margin_angular;    /* 0.01 */
+  double limit_margin_linear;     /* 0.001 */
+  int32_t warm_start;             /* 1 */
+} kd_step_config;
+
+/* Fill *cfg with the reference defaults (StepConfig{}, PadmmConfig{}). */
+void kd_step_config_default(kd_step_config* cfg);
+
+/* ---- per-world diagnostics (StepDiagnostics stepper.hpp:63-74 + SolveDiagnostics padmm.hpp:19-28) */
+typedef struct kd_step_diag {
+  int32_t iterations;
+  int32_t restarts;
+  int32_t converged;
+  int32_t cr_breakdown;
+  int64_t cr_iterations;
+  double r_p, r_d, r_c;
+  int32_t n_rows;
+  int32_t contact_count;
+  int32_t first_contact_row;
+  int32_t n_limits;
+  double f_inf;
+  double kkt_momentum_inf;
+  double bilateral_velocity_inf;
+} kd_step_diag;
+
+/* ---- model ------------------------------------------------------------------ */
+typedef struct kd_model kd_model;
+
+typedef struct kd_model_info {
+  int32_t n_bodies;
+  int32_t n_joints;
+  int32_t n_geoms;
+  int32_t n_bilateral_rows;   /* MechanismModel::n_bilateral_rows (model.hpp:105) */
+  int32_t n_dynamics_rows;    /* model.hpp:106 */
+  int32_t n_loops;            /* model.hpp:107 */
+  int32_t n_limited_joints;
+  int32_t max_contacts;       /* capacity: 1 per sphere pair, 4 per box-plane pair */
+  int32_t row_capacity;       /* n_bil + n_dyn + 2 n_limited + 3 max_contacts */
+} kd_model_info;
+
+/* build_model (model.hpp:117, model.cpp:100-307): validates, lays out rows,
+ * counts loops, resolves default PD targets.  On error returns the ModelError
+ * code (KD_ERR_MODEL_*) and kd_last_error() holds the reference message. */
+int kd_model_build(const kd_scene_desc* scene, kd_model** out);
+void kd_model_destroy(kd_model* model);
+int kd_model_get_info(const kd_model* model, kd_model_info* out);
+/* JointLayout (model.hpp:63-74): per joint row_offset,row_count,dyn_offset,dyn_count */
+int kd_model_joint_layout(const kd_model* model, int32_t* row_offset, int32_t* row_count,
+                          int32_t* dyn_offset, int32_t* dyn_count);
+/* Resolved per-joint PD targets (JointSpec::target, model.cpp:293-305). */
+int kd_model_joint_targets(const kd_model* model, double* targets);
+/* joint_coordinate (model.hpp:130, model.cpp:326-340) on host; poses are 7/body. */
+int kd_joint_coordinate(const kd_model* model, int32_t joint, const double* poses7, double* out);
+
+/* ---- batch (WorldBatch batch.hpp:14-54, batch_step batch.hpp:58) ------------- */
+typedef struct kd_batch kd_batch;
+
+/* Creates a device-resident batch on CUDA device `device`; world w uses
+ * models[world_model[w]] and starts from that model's initial state
+ * (WorldBatch::add_world(model), batch.cpp:8-11). */
+int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_models,
+                    const int32_t* world_model, int32_t n_worlds, kd_batch** out);
+void kd_batch_destroy(kd_batch* batch);
+int kd_batch_size(const kd_batch* batch, int32_t* n_worlds, int64_t* pose_len, int64_t* twist_len);
+/* pose_offset / twist_offset (batch.hpp:31-32) for every world. */
+int kd_batch_offsets(const kd_batch* batch, int32_t* pose_offset, int32_t* twist_offset);
+/* Whole-batch host<->device state copies in the reference storage layout
+ * (pose_storage/twist_storage, batch.hpp:33-34; extract/insert_state batch.cpp:27-72).
+ * `time` has one entry per world; any pointer may be NULL to skip that field. */
+int kd_batch_set_state(kd_batch* batch, const double* poses, const double* twists, const double* time);
+int kd_batch_get_state(kd_batch* batch, double* poses, double* twists, double* time);
+/* Clear every warm-start cache (WorldState caches, stepper.hpp:38-56). */
+int kd_batch_reset_caches(kd_batch* batch);
+/* set_active (batch.hpp:25): one byte per world. */
+int kd_batch_set_active(kd_batch* batch, const uint8_t* active);
+/* batch_step (batch.hpp:58, batch.cpp:74-110) applied n_steps times on the
+ * device stream; returns after the work is enqueued AND completed. */
+int kd_batch_step(kd_batch* batch, const kd_step_config* cfg, int32_t n_steps);
+/* diagnostics(w)/converged(w) (batch.hpp:27-29) of the last step, per world. */
+int kd_batch_get_diagnostics(kd_batch* batch, kd_step_diag* per_world);
+/* StepDiagnostics::impulses (stepper.hpp:68) of the last step: world w's rows
+ * are written at out[offsets[w] .. offsets[w]+n_rows(w)), offsets[] being the
+ * per-world row capacity prefix sum returned by kd_batch_row_offsets. */
+int kd_batch_row_offsets(const kd_batch* batch, int64_t* row_offset, int64_t* total_rows);
+int kd_batch_get_impulses(kd_batch* batch, double* out);
+/* Per-iteration combined residual max(r_p,r_d,r_c) of the last step
+ * (padmm_solve combined_history, padmm.hpp:64-67).  Enable with capacity > 0
+ * before stepping; out is [n_worlds][capacity], unused tail = -1. */
+int kd_batch_set_history_capacity(kd_batch* batch, int32_t capacity);
+int kd_batch_get_history(kd_batch* batch, double* out);
+
+/* ---- one-step introspection for parity (ConstraintSet constraints.hpp:39-65) -- */
+typedef struct kd_row_dump {
+  int32_t body_a, body_b;
+  int32_t kind;        /* 0 bilateral/dynamics, 1 limit (nonnegative), 2 contact (SOC) */
+  int32_t pad;
+  double block_a[6], block_b[6];
+  double bias, reg, scale, vf_scaled, lambda, z;
+} kd_row_dump;
+/* Rows assembled by the last step of world w (n_rows entries). */
+int kd_batch_dump_rows(kd_batch* batch, int32_t world, kd_row_dump* out, int32_t capacity,
+                       int32_t* n_rows);
+/* Contacts of the last step of world w: geom_a, geom_b per contact and
+ * position/normal/depth/mu/e (ContactPoint, contacts.hpp:11-19). */
+int kd_batch_dump_contacts(kd_batch* batch, int32_t world, int32_t* geoms, double* data9,
+                           int32_t capacity, int32_t* n_contacts);
+/* Active limit keys (joint, bound) of the last step (ConstraintSet::limit_keys). */
+int kd_batch_dump_limits(kd_batch* batch, int32_t world, int32_t* keys2, int32_t capacity,
+                         int32_t* n_limits);
+
+/* ---- multi-GPU helpers --------------------------------------------------------- */
+/* Deterministic bench jitter (main.cpp:199-211): std::mt19937_64(seed) +
+ * std::normal_distribution<double>(0, sigma), applied world-major, per body,
+ * for k=0..2 linear[k] then angular[k].  twists6 is the batch twist storage. */
+int kd_bench_jitter(uint64_t seed, double sigma, int32_t n_worlds, const int32_t* n_bodies,
+                    double* twists6);
+
+/* Device timing of the last kd_batch_step call, per kernel family:
+ * ms[0]=assemble, ms[1]=dense solve, ms[2]=matrix-free solve, ms[3]=recover. */
+int kd_batch_enable_timing(kd_batch* batch, int32_t enable);
+int kd_batch_get_timing(kd_batch* batch, double* ms4, int64_t* launches);
+
+const char* kd_last_error(void);
+const char* kd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KAMINO_B200_H */
