@@ -249,6 +249,10 @@ int kd_batch_get_timing(kd_batch* batch, double* ms4, int64_t* launches);
 
 const char* kd_last_error(void);
 const char* kd_version(void);
+/* ABI self-check: writes sizeof of kd_body_desc, kd_joint_desc, kd_geom_desc,
+ * kd_scene_desc, kd_step_config, kd_step_diag, kd_model_info, kd_row_dump
+ * (in that order) into out[0..7]; returns the count written. */
+int kd_abi_sizes(int32_t* out, int32_t capacity);
 
 #ifdef __cplusplus
 }

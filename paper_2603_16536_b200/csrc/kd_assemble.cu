@@ -1,0 +1,640 @@
+// kd_assemble.cu — K1: per-world constraint assembly, one warp per world.
+//
+// Restates, on the device and in the reference order:
+//   step() prologue (stepper.cpp:139-176): Moreau-Jean eval poses, world
+//     inertias (delassus.cpp:21-34), free forces at start-of-step poses
+//     (stepper.cpp:108-121), u_free;
+//   collide (contacts.cpp:119-145) with sphere-plane / sphere-sphere /
+//     box-plane narrow phases;
+//   assemble_constraints (constraints.cpp:189-329) incl. build_joint_rows
+//     (20-109), coordinate_rate_row (160-187), limit and contact rows;
+//   jacobi_preconditioner (delassus.cpp:36-57), v_f = J u_free - v* and its
+//     preconditioned form, fold_inverse_mass (JM rows);
+//   gather_warmstart (stepper.cpp:19-46) with match_warmstart
+//     (contacts.cpp:147-182).
+// Lanes own bodies / pairs / joints / rows; ordered outputs (contacts, limit
+// rows, per-body row lists) use warp prefix sums so indexing is bit-exact with
+// the reference.  Work per world is small (~10^4 flops), so 8 worlds share a
+// 256-thread CTA and the grid covers the batch once.
+#include "kd_device.cuh"
+
+namespace kd {
+
+namespace {
+
+struct Frames {
+  V3 ap, ac;  // anchors
+  M3 Rp, Rc;  // joint frames in world
+};
+
+// joint_world_frames (model.cpp:309-324)
+__device__ __forceinline__ Frames joint_frames(const DevJoint& j, const BodyS* bs) {
+  Frames f;
+  if (j.parent < 0) {
+    f.ap = ld3(j.fp_pos);
+    f.Rp = ldm(j.fp_R);
+  } else {
+    const BodyS& p = bs[j.parent];
+    f.ap = add(ld3(p.ep), qapply(ldq(p.eq), ld3(j.fp_pos)));
+    f.Rp = mmul(ldm(p.eR), ldm(j.fp_R));
+  }
+  const BodyS& c = bs[j.child];
+  f.ac = add(ld3(c.ep), qapply(ldq(c.eq), ld3(j.fc_pos)));
+  f.Rc = mmul(ldm(c.eR), ldm(j.fc_R));
+  return f;
+}
+
+// joint_coordinate (model.cpp:326-340)
+__device__ __forceinline__ double joint_coord(const DevJoint& j, const Frames& f) {
+  if (j.type == J_REVOLUTE) {
+    Q4 rel = qfrom(mmul(mtrans(f.Rp), f.Rc));
+    if (rel.w < 0) rel = Q4{-rel.w, -rel.x, -rel.y, -rel.z};
+    return 2.0 * atan2(dot(ld3(j.axis), V3{rel.x, rel.y, rel.z}), rel.w);
+  }
+  return dot(ld3(j.axis), mvec(mtrans(f.Rp), sub(f.ac, f.ap)));
+}
+
+__device__ __forceinline__ void put_row(RowJ* rj, int32_t* rb, int r, int ba, int bb, V3 al, V3 aa, V3 bl, V3 ba3) {
+  double* J = rj[r].J;
+  J[0] = al.x; J[1] = al.y; J[2] = al.z; J[3] = aa.x; J[4] = aa.y; J[5] = aa.z;
+  J[6] = bl.x; J[7] = bl.y; J[8] = bl.z; J[9] = ba3.x; J[10] = ba3.y; J[11] = ba3.z;
+  rb[2 * r] = ba;
+  rb[2 * r + 1] = bb;
+}
+
+// JacobianRow::dot (constraints.hpp:25-30)
+__device__ __forceinline__ double row_dot(const double* J, int ba, int bb, const double* u) {
+  double s = 0.0;
+  if (ba >= 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) t += J[k] * u[6 * ba + k];
+    s += t;
+  }
+  if (bb >= 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) t += J[6 + k] * u[6 * bb + k];
+    s += t;
+  }
+  return s;
+}
+
+// coordinate_rate_row (constraints.cpp:160-187): returns blocks via out params.
+__device__ __forceinline__ void rate_row(const DevJoint& j, const Frames& f, const BodyS* bs, V3& al, V3& aa, V3& bl,
+                                         V3& bang) {
+  const V3 axis_w = mvec(f.Rp, ld3(j.axis));
+  const V3 z{0, 0, 0};
+  if (j.type == J_REVOLUTE) {
+    al = z;
+    aa = axis_w;
+    bl = z;
+    bang = (j.parent >= 0) ? neg(axis_w) : z;
+  } else {
+    const V3 lever = sub(f.ac, ld3(bs[j.child].ep));
+    al = axis_w;
+    aa = vmat(neg(axis_w), skew(lever));
+    if (j.parent >= 0) {
+      bl = neg(axis_w);
+      bang = vmat(axis_w, skew(sub(f.ac, ld3(bs[j.parent].ep))));
+    } else {
+      bl = z;
+      bang = z;
+    }
+  }
+}
+
+// One contact of the narrow phase.
+struct CP {
+  V3 pos, nrm;
+  double depth;
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams sp) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= bv.n_worlds) return;
+  WorldStep& ws = bv.wstep[w];
+  if (!bv.active[w]) {
+    if (lane == 0) ws.backend = BE_NONE, ws.n_rows = -1;
+    return;
+  }
+  const DevWorld W = bv.worlds[w];
+  const DevModel M = bv.models[W.model];
+  const DevBody* mb = bv.bodies + M.body_off;
+  const DevJoint* mj = bv.joints + M.joint_off;
+  const DevGeom* mg = bv.geoms + M.geom_off;
+  const DevPair* mp = bv.pairs + M.pair_off;
+  const double* pose = bv.poses + W.pose_off;
+  const double* tw = bv.twists + W.twist_off;
+  BodyS* bs = bv.bs + W.body_off;
+  const int64_t R0 = W.row_off;
+  RowJ* rj = bv.rowj + R0;
+  int32_t* rb = bv.rbody + 2 * R0;
+  int32_t* rk = bv.rkind + R0;
+  int32_t* lk = bv.lkey + 2 * R0;
+  double* rmu = bv.rmu + R0;
+  double* bias = bv.bias + R0;
+  double* reg = bv.reg + R0;
+  double* scale = bv.scale + R0;
+  double* vf = bv.vf + R0;
+  double* x0 = bv.x0 + R0;
+  double* z0 = bv.z0 + R0;
+  Contact* ct = bv.contacts + W.contact_off;
+  const double dt = sp.dt;
+  const double bgain = sp.beta / dt;
+
+  // ---- 1. bodies: eval pose, inertias, free forces, u_free (stepper.cpp:139-164)
+  for (int b = lane; b < M.nb; b += 32) {
+    const double* p = pose + 7 * b;
+    const double* t = tw + 6 * b;
+    const V3 x{p[0], p[1], p[2]};
+    const Q4 q{p[3], p[4], p[5], p[6]};
+    const V3 vl{t[0], t[1], t[2]}, va{t[3], t[4], t[5]};
+    V3 ex = x;
+    Q4 eq = q;
+    if (sp.moreau) {
+      ex = add(x, scl(0.5 * dt, vl));
+      const V3 wb = mtvec(qrot(q), va);
+      eq = quat_integrate(q, wb, 0.5 * dt);
+    }
+    const M3 eR = qrot(eq);
+    const DevBody db = mb[b];
+    const M3 ib = ldm(db.ib);
+    const M3 Iw = world_inertia(ib, eq);
+    const M3 inv = llt_inverse3(Iw);
+    const M3 Iwinv = mscl(0.5, madd(inv, mtrans(inv)));
+    const M3 Iw0 = world_inertia(ib, q);  // free_forces uses the start-of-step pose
+    const V3 hf = scl(db.mass, ld3(M.gravity));
+    const V3 ht = neg(cross(va, mvec(Iw0, va)));
+    const V3 ufl = add(vl, scl(dt * (1.0 / db.mass), hf));
+    const V3 ufa = add(va, scl(dt, mvec(Iwinv, ht)));
+    BodyS& o = bs[b];
+    st3(o.ep, ex);
+    o.eq[0] = eq.w; o.eq[1] = eq.x; o.eq[2] = eq.y; o.eq[3] = eq.z;
+    stm(o.eR, eR);
+    o.uf[0] = ufl.x; o.uf[1] = ufl.y; o.uf[2] = ufl.z; o.uf[3] = ufa.x; o.uf[4] = ufa.y; o.uf[5] = ufa.z;
+    o.h[0] = hf.x; o.h[1] = hf.y; o.h[2] = hf.z; o.h[3] = ht.x; o.h[4] = ht.y; o.h[5] = ht.z;
+    stm(o.Iw, Iw);
+    stm(o.Iwinv, Iwinv);
+    o.mass = db.mass;
+    o.inv_mass = 1.0 / db.mass;
+  }
+  __syncwarp();
+
+  // ---- 2. narrow phase (contacts.cpp:119-145), pair order then corner index
+  int nc = 0;
+  for (int base = 0; base < M.npairs; base += 32) {
+    const int pi = base + lane;
+    CP cps[4];
+    int cnt = 0;
+    DevPair pr{0, 0, 0, 0};
+    if (pi < M.npairs) {
+      pr = mp[pi];
+      const DevGeom ga = mg[pr.a], gb = mg[pr.b];
+      if (pr.kind == P_SPHERE_PLANE) {  // sphere_plane (contacts.cpp:26-43)
+        const V3 c = ld3(bs[ga.body].ep);
+        const V3 n = ld3(gb.normal);
+        const double depth = ga.radius - (dot(n, c) - gb.offset);
+        if (!(depth <= -sp.contact_margin)) {
+          cps[0] = CP{sub(c, scl(ga.radius, n)), n, depth};
+          cnt = 1;
+        }
+      } else if (pr.kind == P_SPHERE_SPHERE) {  // sphere_sphere (contacts.cpp:45-64)
+        const V3 ca = ld3(bs[ga.body].ep), cb = ld3(bs[gb.body].ep);
+        const V3 d = sub(ca, cb);
+        const double dist = norm(d);
+        const double depth = ga.radius + gb.radius - dist;
+        if (!(depth <= -sp.contact_margin)) {
+          const V3 n = dist > 1e-12 ? V3{d.x / dist, d.y / dist, d.z / dist} : V3{0, 0, 1};
+          cps[0] = CP{scl(0.5, add(sub(ca, scl(ga.radius, n)), add(cb, scl(gb.radius, n)))), n, depth};
+          cnt = 1;
+        }
+      } else {  // box_plane (contacts.cpp:66-106)
+        const V3 c = ld3(bs[ga.body].ep);
+        const M3 R = ldm(bs[ga.body].eR);
+        const V3 n = ld3(gb.normal);
+        double dep[8];
+        V3 pt[8];
+        int hits = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const V3 loc{(k & 1) ? ga.he[0] : -ga.he[0], (k & 2) ? ga.he[1] : -ga.he[1], (k & 4) ? ga.he[2] : -ga.he[2]};
+          pt[k] = add(c, mvec(R, loc));
+          dep[k] = gb.offset - dot(n, pt[k]);
+          if (dep[k] > -sp.contact_margin) hits |= 1 << k;
+        }
+        const int nh = __popc(hits);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (!(hits & (1 << k))) continue;
+          if (nh > 4) {  // stable_sort by depth desc, keep 4 (contacts.cpp:88-92)
+            int rank = 0;
+            for (int j2 = 0; j2 < 8; ++j2)
+              if ((hits & (1 << j2)) && (dep[j2] > dep[k] || (dep[j2] == dep[k] && j2 < k))) ++rank;
+            if (rank >= 4) continue;
+          }
+          cps[cnt++] = CP{pt[k], n, dep[k]};
+        }
+      }
+    }
+    int excl;
+    const int tot = warp_exclusive_sum(cnt, lane, excl);
+    if (nc + excl + cnt > W.contact_cap) cnt = max(0, W.contact_cap - nc - excl);  // overflow: reported below
+    if (cnt) {
+      const DevGeom ga = mg[pr.a], gb = mg[pr.b];
+      const double mu = sqrt(ga.mu * gb.mu);
+      const double e = fmax(ga.restitution, gb.restitution);
+      for (int k = 0; k < cnt; ++k) {
+        Contact& o = ct[nc + excl + k];
+        o.ga = pr.a;
+        o.gb = pr.b;
+        o.pair = pi;
+        st3(o.pos, cps[k].pos);
+        st3(o.nrm, cps[k].nrm);
+        o.depth = cps[k].depth;
+        o.mu = mu;
+        o.e = e;
+      }
+    }
+    nc += tot;
+  }
+  bool overflow = false;
+  if (nc > W.contact_cap) {
+    overflow = true;
+    nc = W.contact_cap;
+  }
+
+  // ---- 3. joint rows, joint-dynamics rows, limit activation (constraints.cpp:20-109, 189-295)
+  const int n_jd = M.n_bil + M.n_dyn;
+  double f_inf = 0.0;
+  int nlim = 0;
+  for (int base = 0; base < M.nj; base += 32) {
+    const int ji = base + lane;
+    int lim_cnt = 0;
+    int lo_act = 0, up_act = 0;
+    double g_lo = 0, g_up = 0;
+    Frames fr;
+    DevJoint j;
+    if (ji < M.nj) {
+      j = mj[ji];
+      fr = joint_frames(j, bs);
+      const M3 wpt = mtrans(fr.Rp);
+      const int child = j.child;
+      const V3 lever_c = sub(fr.ac, ld3(bs[child].ep));
+      const V3 f_pos = mvec(wpt, sub(fr.ac, fr.ap));
+      const M3 c_ang = mmul(mscl(-1.0, wpt), skew(lever_c));
+      M3 p_lin = mzero(), p_ang = mzero();
+      if (j.parent >= 0) {
+        p_lin = mscl(-1.0, wpt);
+        p_ang = mmul(wpt, skew(sub(fr.ac, ld3(bs[j.parent].ep))));
+      }
+      const int pb = j.parent;
+      V3 f_rot{0, 0, 0};
+      M3 r_ang = mzero();
+      if (j.type != J_SPHERICAL) {
+        const M3 rel = mmul(wpt, fr.Rc);
+        f_rot = so3_log(rel);
+        r_ang = mmul(left_jacobian_inverse(f_rot), wpt);
+      }
+      const V3 z3{0, 0, 0};
+      int r = j.row_offset;
+      auto emit = [&](V3 al, V3 aa, V3 bl, V3 bang, double fval) {
+        put_row(rj, rb, r, child, pb, al, aa, pb >= 0 ? bl : z3, pb >= 0 ? bang : z3);
+        rk[r] = ROW_BILATERAL;
+        rmu[r] = 0.0;
+        reg[r] = 0.0;
+        bias[r] = fmin(fmax(-bgain * fval, -sp.bias_clamp), sp.bias_clamp);  // clamp_abs
+        f_inf = fmax(f_inf, fabs(fval));
+        ++r;
+      };
+      auto emit_pos = [&](int k) { emit(mrow(wpt, k), mrow(c_ang, k), mrow(p_lin, k), mrow(p_ang, k), comp(f_pos, k)); };
+      auto emit_rot = [&](int k) { emit(z3, mrow(r_ang, k), z3, neg(mrow(r_ang, k)), comp(f_rot, k)); };
+      // push_combined (constraints.cpp:77-87): weights^T applied to a 3-row block
+      auto emit_comb = [&](bool pos, const double* wv) {
+        V3 al{0, 0, 0}, aa{0, 0, 0}, bl{0, 0, 0}, bang{0, 0, 0};
+        for (int k = 0; k < 3; ++k) {
+          const double wk = wv[k];
+          if (pos) {
+            al = add(al, scl(wk, mrow(wpt, k)));
+            aa = add(aa, scl(wk, mrow(c_ang, k)));
+            bl = add(bl, scl(wk, mrow(p_lin, k)));
+            bang = add(bang, scl(wk, mrow(p_ang, k)));
+          } else {
+            aa = add(aa, scl(wk, mrow(r_ang, k)));
+            bang = add(bang, scl(wk, neg(mrow(r_ang, k))));
+          }
+        }
+        emit(al, aa, bl, bang, dot(ld3(wv), pos ? f_pos : f_rot));
+      };
+      switch (j.type) {
+        case J_FIXED:
+          for (int k = 0; k < 3; ++k) emit_pos(k);
+          for (int k = 0; k < 3; ++k) emit_rot(k);
+          break;
+        case J_REVOLUTE:
+          for (int k = 0; k < 3; ++k) emit_pos(k);
+          emit_comb(false, j.comp0);
+          emit_comb(false, j.comp1);
+          break;
+        case J_PRISMATIC:
+          emit_comb(true, j.comp0);
+          emit_comb(true, j.comp1);
+          for (int k = 0; k < 3; ++k) emit_rot(k);
+          break;
+        default:
+          for (int k = 0; k < 3; ++k) emit_pos(k);
+          break;
+      }
+      // coordinate (limited or actuated scalar joints), dynamics rows
+      const bool scalar = j.type == J_REVOLUTE || j.type == J_PRISMATIC;
+      double coord = 0.0;
+      if (scalar && (j.flags & (JF_LIMITS | JF_PD))) coord = joint_coord(j, fr);
+      if (j.flags & (JF_PD | JF_ARMATURE | JF_DAMPING)) {
+        V3 al, aa, bl, bang;
+        rate_row(j, fr, bs, al, aa, bl, bang);
+        int rr = M.n_bil + j.dyn_offset;
+        if (j.flags & JF_PD) {
+          put_row(rj, rb, rr, child, pb, al, aa, bl, bang);
+          rk[rr] = ROW_BILATERAL;
+          rmu[rr] = 0.0;
+          reg[rr] = 1.0 / (dt * (dt * j.kp + j.kd));
+          bias[rr] = (j.kp * (j.target - coord) + j.kd * j.target_rate) / (dt * j.kp + j.kd);
+          ++rr;
+        }
+        if (j.flags & JF_ARMATURE) {
+          put_row(rj, rb, rr, child, pb, al, aa, bl, bang);
+          rk[rr] = ROW_BILATERAL;
+          rmu[rr] = 0.0;
+          reg[rr] = 1.0 / j.armature;
+          bias[rr] = row_dot(rj[rr].J, child, pb, tw);
+          ++rr;
+        }
+        if (j.flags & JF_DAMPING) {
+          put_row(rj, rb, rr, child, pb, al, aa, bl, bang);
+          rk[rr] = ROW_BILATERAL;
+          rmu[rr] = 0.0;
+          reg[rr] = 1.0 / (dt * j.damping);
+          bias[rr] = 0.0;
+          ++rr;
+        }
+      }
+      if (j.flags & JF_LIMITS) {  // constraints.cpp:222-229
+        const double margin = j.type == J_REVOLUTE ? sp.lim_margin_ang : sp.lim_margin_lin;
+        g_lo = coord - j.lower;
+        g_up = j.upper - coord;
+        lo_act = g_lo < margin;
+        up_act = g_up < margin;
+        lim_cnt = lo_act + up_act;
+      }
+    }
+    int excl;
+    const int tot = warp_exclusive_sum(lim_cnt, lane, excl);
+    if (lim_cnt) {  // limit rows (constraints.cpp:281-295), lower before upper
+      V3 al, aa, bl, bang;
+      rate_row(j, fr, bs, al, aa, bl, bang);
+      int r = n_jd + nlim + excl;
+      for (int bound = 0; bound < 2; ++bound) {
+        if (!(bound == 0 ? lo_act : up_act)) continue;
+        const double sgn = bound == 1 ? -1.0 : 1.0;
+        put_row(rj, rb, r, j.child, j.parent, scl(sgn, al), scl(sgn, aa), scl(sgn, bl), scl(sgn, bang));
+        const double gap = bound == 0 ? g_lo : g_up;
+        rk[r] = ROW_LIMIT;
+        rmu[r] = 0.0;
+        reg[r] = 0.0;
+        bias[r] = fmin(-bgain * fmin(gap, 0.0), sp.bias_clamp);
+        lk[2 * r] = ji;
+        lk[2 * r + 1] = bound;
+        ++r;
+      }
+    }
+    nlim += tot;
+  }
+  f_inf = warp_max(f_inf);
+  const int first_contact = n_jd + nlim;
+  const int n = first_contact + 3 * nc;
+  __syncwarp();
+
+  // ---- 4. contact rows (constraints.cpp:297-326)
+  for (int c = lane; c < nc; c += 32) {
+    const Contact cp = ct[c];
+    const V3 nrm = ld3(cp.nrm);
+    V3 t1, t2;
+    orthonormal_complement(nrm, t1, t2);  // contact_frame (contacts.cpp:110-117)
+    const int ba = mg[cp.ga].body;
+    const int bb = mg[cp.gb].body;
+    const int r = first_contact + 3 * c;
+    const V3 pos = ld3(cp.pos);
+    for (int d = 0; d < 3; ++d) {
+      const V3 dir = d == 0 ? nrm : (d == 1 ? t1 : t2);
+      const V3 aa = vmat(neg(dir), skew(sub(pos, ld3(bs[ba].ep))));
+      V3 bl{0, 0, 0}, bang{0, 0, 0};
+      if (bb >= 0) {
+        bl = neg(dir);
+        bang = vmat(dir, skew(sub(pos, ld3(bs[bb].ep))));
+      }
+      put_row(rj, rb, r + d, ba, bb >= 0 ? bb : -1, dir, aa, bl, bang);
+      rk[r + d] = ROW_CONTACT;
+      rmu[r + d] = cp.mu;
+      reg[r + d] = 0.0;
+      bias[r + d] = 0.0;
+    }
+    const double vn = row_dot(rj[r].J, ba, bb >= 0 ? bb : -1, tw);
+    double bn = fmin(-bgain * fmin(-cp.depth, 0.0), sp.bias_clamp);
+    if (vn < -sp.impact_thr) bn += -cp.e * vn;
+    bias[r] = bn;
+  }
+
+  // ---- 5. contact warm start: match_warmstart per geom-pair group (contacts.cpp:147-182)
+  const int ncache = ws.ccache_count;
+  const CacheEntry* cache = bv.ccache + W.contact_off;
+  for (int c = lane; c < nc; c += 32) {
+    const int r = first_contact + 3 * c;
+    for (int d = 0; d < 3; ++d) x0[r + d] = z0[r + d] = 0.0;
+  }
+  __syncwarp();
+  if (sp.warm_start) {
+    for (int c = lane; c < nc; c += 32) {
+      const Contact cp = ct[c];
+      if (c > 0 && ct[c - 1].ga == cp.ga && ct[c - 1].gb == cp.gb) continue;  // not group head
+      int gsize = 1;
+      while (c + gsize < nc && ct[c + gsize].ga == cp.ga && ct[c + gsize].gb == cp.gb && gsize < 4) ++gsize;
+      // candidates (dist, entry, contact) within tolerance 1e-3
+      double cd[16];
+      int ce[16], cc[16], ncand = 0;
+      for (int e = 0; e < ncache; ++e) {
+        if (cache[e].ga != cp.ga || cache[e].gb != cp.gb) continue;
+        for (int k = 0; k < gsize; ++k) {
+          const double dd = norm(sub(ld3(cache[e].pos), ld3(ct[c + k].pos)));
+          if (dd <= 1e-3 && ncand < 16) {
+            cd[ncand] = dd;
+            ce[ncand] = e;
+            cc[ncand] = k;
+            ++ncand;
+          }
+        }
+      }
+      // greedy nearest-first over the sorted candidate list
+      unsigned used_e = 0, done_c = 0;  // a pair's cache entries are contiguous and <= 4
+      for (int round = 0; round < ncand; ++round) {
+        int best = -1;
+        for (int k = 0; k < ncand; ++k) {
+          if (ce[k] < 0) continue;
+          if (best < 0 || cd[k] < cd[best] || (cd[k] == cd[best] && (ce[k] < ce[best] || (ce[k] == ce[best] && cc[k] < cc[best]))))
+            best = k;
+        }
+        if (best < 0) break;
+        const int e = ce[best], k = cc[best];
+        ce[best] = -1;
+        if ((used_e >> (e & 31)) & 1u) continue;
+        if ((done_c >> k) & 1u) continue;
+        used_e |= 1u << (e & 31);
+        done_c |= 1u << k;
+        const int r = first_contact + 3 * (c + k);
+        for (int d = 0; d < 3; ++d) {
+          x0[r + d] = cache[e].imp[d];
+          z0[r + d] = cache[e].dual[d];
+        }
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- 6. rows: JM, preconditioner, v_f, remaining warm start (delassus.cpp:12-57; stepper.cpp:19-46, 175-176)
+  const bool jvalid = sp.warm_start && ws.jcache_valid;
+  for (int r = lane; r < n; r += 32) {
+    RowJ& R = rj[r];
+    const int ba = rb[2 * r], bb = rb[2 * r + 1];
+    double d = reg[r];
+    if (ba >= 0) {
+      const BodyS& B = bs[ba];
+      const V3 t = vmat(V3{R.J[3], R.J[4], R.J[5]}, ldm(B.Iwinv));
+      R.JM[0] = R.J[0] * B.inv_mass; R.JM[1] = R.J[1] * B.inv_mass; R.JM[2] = R.J[2] * B.inv_mass;
+      R.JM[3] = t.x; R.JM[4] = t.y; R.JM[5] = t.z;
+      double s = 0;
+      for (int k = 0; k < 6; ++k) s += R.JM[k] * R.J[k];
+      d += s;
+    } else {
+      for (int k = 0; k < 6; ++k) R.JM[k] = 0.0;
+    }
+    if (bb >= 0) {
+      const BodyS& B = bs[bb];
+      const V3 t = vmat(V3{R.J[9], R.J[10], R.J[11]}, ldm(B.Iwinv));
+      R.JM[6] = R.J[6] * B.inv_mass; R.JM[7] = R.J[7] * B.inv_mass; R.JM[8] = R.J[8] * B.inv_mass;
+      R.JM[9] = t.x; R.JM[10] = t.y; R.JM[11] = t.z;
+      double s = 0;
+      for (int k = 0; k < 6; ++k) s += R.JM[6 + k] * R.J[6 + k];
+      d += s;
+    } else {
+      for (int k = 0; k < 6; ++k) R.JM[6 + k] = 0.0;
+    }
+    scale[r] = 1.0 / sqrt(fmax(d, 1e-12));
+  }
+  __syncwarp();
+  for (int r = lane; r < n; r += 32) {
+    double p = scale[r];
+    if (r >= first_contact) {  // SOC rows share the normal-row scale (delassus.cpp:50-55)
+      p = scale[first_contact + 3 * ((r - first_contact) / 3)];
+    }
+    // v_f = J u_free - v*; scaled by P
+    double u6a[6], u6b[6];
+    const int ba = rb[2 * r], bb = rb[2 * r + 1];
+    double s = 0.0;
+    if (ba >= 0) {
+      for (int k = 0; k < 6; ++k) u6a[k] = bs[ba].uf[k];
+      double t = 0;
+      for (int k = 0; k < 6; ++k) t += rj[r].J[k] * u6a[k];
+      s += t;
+    }
+    if (bb >= 0) {
+      for (int k = 0; k < 6; ++k) u6b[k] = bs[bb].uf[k];
+      double t = 0;
+      for (int k = 0; k < 6; ++k) t += rj[r].J[6 + k] * u6b[k];
+      s += t;
+    }
+    vf[r] = p * (s - bias[r]);
+    // warm start of joint and limit rows (contacts were filled above)
+    double xl = 0.0, xz = 0.0;
+    if (r < n_jd) {
+      if (jvalid) {
+        xl = bv.jc_lam[W.jcache_off + r];
+        xz = bv.jc_z[W.jcache_off + r];
+      }
+    } else if (r < first_contact) {
+      if (sp.warm_start) {
+        const int ji = lk[2 * r], bound = lk[2 * r + 1];
+        const int slot = W.lslot_off + 2 * mj[ji].limit_slot + bound;
+        if (bv.ls_valid[slot]) {
+          xl = bv.ls_lam[slot];
+          xz = bv.ls_z[slot];
+        }
+      }
+    } else {
+      xl = x0[r];
+      xz = z0[r];
+    }
+    x0[r] = xl / p;
+    z0[r] = xz * p;
+    if (r >= first_contact) scale[r] = p;
+  }
+  __syncwarp();
+
+  // ---- 7. per-body row lists in ascending row order (for J^T lambda and the CR scatter)
+  int32_t* cptr = bv.csr_ptr + W.body_off + w;
+  int32_t* clist = bv.csr + 2 * R0;
+  int run = 0;
+  for (int base = 0; base < M.nb; base += 32) {
+    const int b = base + lane;
+    int cnt = 0;
+    if (b < M.nb)
+      for (int r = 0; r < n; ++r) cnt += (rb[2 * r] == b) + (rb[2 * r + 1] == b);
+    int excl;
+    const int tot = warp_exclusive_sum(cnt, lane, excl);
+    if (b < M.nb) {
+      int pos = run + excl;
+      cptr[b] = pos;
+      for (int r = 0; r < n; ++r) {
+        if (rb[2 * r] == b) clist[pos++] = 2 * r;
+        if (rb[2 * r + 1] == b) clist[pos++] = 2 * r + 1;
+      }
+    }
+    run += tot;
+  }
+  if (lane == 0) {
+    cptr[M.nb] = run;
+    ws.n_rows = n;
+    ws.n_limits = nlim;
+    ws.n_contacts = nc;
+    ws.f_inf = M.n_bil > 0 ? f_inf : 0.0;
+    int be = BE_NONE;
+    ws.fail = 0;
+    if (n > 0) {  // build_backend choice (delassus.cpp:204-206)
+      const bool dense = sp.backend == 0 /*KD_BACKEND_DENSE*/ || (sp.backend == 2 /*AUTO*/ && n <= 300);
+      be = dense ? (n <= W.smem_cap ? BE_DENSE_SMEM : BE_DENSE_GLOBAL) : BE_MATRIX_FREE;
+      if (be == BE_DENSE_GLOBAL && n > W.slab_cap) overflow = true;
+    }
+    if (overflow) {
+      be = BE_NONE;
+      ws.fail = 2;
+      atomicAdd(bv.error_count + 1, 1);
+    }
+    ws.backend = be;
+    // solver diagnostics default (SolveDiagnostics{}, padmm.hpp:19-28) for n == 0
+    ws.iterations = 0;
+    ws.restarts = 0;
+    ws.converged = 1;
+    ws.cr_breakdown = 0;
+    ws.cr_iterations = 0;
+    ws.r_p = ws.r_d = ws.r_c = 0.0;
+  }
+}
+
+void launch_assemble(const BatchView& bv, const StepParams& sp, cudaStream_t s) {
+  const int wpb = 8;
+  const int grid = (bv.n_worlds + wpb - 1) / wpb;
+  if (grid > 0) assemble_kernel<<<grid, 32 * wpb, 0, s>>>(bv, sp);
+}
+
+}  // namespace kd

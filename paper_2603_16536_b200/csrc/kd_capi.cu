@@ -1,0 +1,729 @@
+// kd_capi.cu — the C-ABI (include/kamino_b200.h): models, device-resident
+// world batches, stepping and introspection.
+//
+// kd_batch is the device-side WorldBatch (batch.hpp:14-54).  Creation lays out
+// every per-world slab (state, rows, bodies, contacts, caches) by prefix sums
+// over model capacities, bins worlds by dense-Delassus shared-memory class, and
+// uploads the immutable model tables once.  kd_batch_step runs, per step,
+//   K1 assemble (warp/world) -> K2 dense (CTA/world, per bin)
+//   -> K2g dense-global -> K2b matrix-free CR -> K3 recover (warp/world)
+// on one stream; a K2 CTA exits immediately when its world chose another
+// backend this step (the choice depends on the contact/limit count, known only
+// on the device).
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "kd_host.h"
+
+using namespace kd;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define KD_CK(x)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) return fail(KD_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevMem {
+  std::vector<void*> ptrs;
+  ~DevMem() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  cudaError_t alloc(T*& out, size_t count) {
+    void* p = nullptr;
+    const cudaError_t e = cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T));
+    if (e == cudaSuccess) {
+      cudaMemset(p, 0, std::max<size_t>(1, count) * sizeof(T));
+      ptrs.push_back(p);
+      out = static_cast<T*>(p);
+    }
+    return e;
+  }
+};
+
+struct Bin {
+  int cap = 0;  // rows (dense) / rows (cr)
+  int nbcap = 0;
+  int nt = 0;
+  int count = 0;
+  int32_t* d_worlds = nullptr;
+  std::vector<int32_t> worlds;
+};
+
+// dense shared-memory classes: (row capacity, threads per CTA)
+constexpr int kClasses[4][2] = {{32, 64}, {64, 64}, {128, 128}, {236, 512}};
+constexpr int kSmemMaxRows = 236;
+constexpr int kDenseGlobalMaxRows = KD_DENSE_ROW_CROSSOVER;
+
+}  // namespace
+
+struct kd_batch {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<HostModel> models;
+  std::vector<int32_t> world_model;
+  int n_worlds = 0;
+  std::vector<DevWorld> worlds;
+  std::vector<int32_t> pose_off, twist_off;
+  std::vector<int64_t> row_off;
+  int64_t total_rows = 0, pose_len = 0, twist_len = 0, total_lslab = 0;
+  int total_bodies = 0, total_contacts = 0, total_jcache = 0, total_lslots = 0;
+  DevMem mem;
+  BatchView view{};
+  std::vector<Bin> dense_bins;
+  Bin global_bin, cr_auto_bin, cr_all_bin;
+  int hist_cap = 0;
+  double* d_hist = nullptr;
+  int32_t* d_err = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[6] = {};
+  double ms[4] = {0, 0, 0, 0};
+  int64_t launches = 0;
+  ~kd_batch() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+extern "C" {
+
+const char* kd_last_error(void) { return g_err.c_str(); }
+const char* kd_version(void) { return "kamino_b200 0.1 (sm_100a)"; }
+
+int kd_abi_sizes(int32_t* out, int32_t cap) {
+  const int32_t s[8] = {(int32_t)sizeof(kd_body_desc),   (int32_t)sizeof(kd_joint_desc),
+                        (int32_t)sizeof(kd_geom_desc),   (int32_t)sizeof(kd_scene_desc),
+                        (int32_t)sizeof(kd_step_config), (int32_t)sizeof(kd_step_diag),
+                        (int32_t)sizeof(kd_model_info),  (int32_t)sizeof(kd_row_dump)};
+  const int n = cap < 8 ? cap : 8;
+  for (int i = 0; i < n; ++i) out[i] = s[i];
+  return n;
+}
+
+void kd_step_config_default(kd_step_config* c) {
+  c->dt = 1.0 / 240.0;
+  c->integrator = KD_INTEGRATOR_SEMI_IMPLICIT_EULER;
+  c->backend = KD_BACKEND_AUTO;
+  c->eta = 1e-6;
+  c->rho = 0.1;
+  c->eps = 1e-6;
+  c->max_iters = 200;
+  c->acceleration = 1;
+  c->restart = 1;
+  c->fixed_iteration_mode = 0;
+  c->cr_iters = 9;
+  c->baumgarte_beta = 0.2;
+  c->contact_margin = 0.01;
+  c->impact_velocity_threshold = 0.1;
+  c->bias_clamp = 10.0;
+  c->limit_margin_angular = 0.01;
+  c->limit_margin_linear = 0.001;
+  c->warm_start = 1;
+}
+
+int kd_model_build(const kd_scene_desc* scene, kd_model** out) {
+  if (!scene || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  auto* m = new kd_model;
+  std::string err;
+  const int code = build_host_model(scene, m->m, err);
+  if (code != KD_OK) {
+    delete m;
+    return fail(code, err);
+  }
+  *out = m;
+  return KD_OK;
+}
+
+void kd_model_destroy(kd_model* m) { delete m; }
+
+int kd_model_get_info(const kd_model* m, kd_model_info* out) {
+  if (!m || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  *out = m->m.info;
+  return KD_OK;
+}
+
+int kd_model_joint_layout(const kd_model* mp, int32_t* ro, int32_t* rc, int32_t* dof, int32_t* dc) {
+  if (!mp) return fail(KD_ERR_INVALID_ARGUMENT, "null model");
+  const HostModel& m = mp->m;
+  for (size_t j = 0; j < m.joints.size(); ++j) {
+    const DevJoint& J = m.joints[j];
+    ro[j] = J.row_offset;
+    rc[j] = J.row_count;
+    dof[j] = J.dyn_offset;
+    dc[j] = ((J.flags & JF_PD) ? 1 : 0) + ((J.flags & JF_ARMATURE) ? 1 : 0) + ((J.flags & JF_DAMPING) ? 1 : 0);
+  }
+  return KD_OK;
+}
+
+int kd_model_joint_targets(const kd_model* mp, double* t) {
+  if (!mp) return fail(KD_ERR_INVALID_ARGUMENT, "null model");
+  for (size_t j = 0; j < mp->m.joints.size(); ++j) t[j] = mp->m.joints[j].target;
+  return KD_OK;
+}
+
+int kd_joint_coordinate(const kd_model* mp, int32_t joint, const double* poses7, double* out) {
+  if (!mp || !poses7 || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  const HostModel& m = mp->m;
+  if (joint < 0 || joint >= (int)m.joints.size()) return fail(KD_ERR_INVALID_ARGUMENT, "joint index out of range");
+  const int t = m.joints[joint].type;
+  if (t != J_REVOLUTE && t != J_PRISMATIC)
+    return fail(KD_ERR_MODEL_WRONG_JOINT_TYPE, "joint '" + m.joint_names[joint] + "' has no scalar coordinate");
+  *out = host_joint_coordinate(m, joint, poses7);
+  return KD_OK;
+}
+
+// --------------------------------------------------------------------- batch
+int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_models, const int32_t* world_model,
+                    int32_t n_worlds, kd_batch** out) {
+  if (!models || !out || n_models <= 0 || n_worlds < 0 || (n_worlds > 0 && !world_model))
+    return fail(KD_ERR_INVALID_ARGUMENT, "invalid arguments");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(KD_ERR_NO_DEVICE, "no CUDA device visible: the B200 solver has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(KD_ERR_INVALID_ARGUMENT, "device index out of range");
+  KD_CK(cudaSetDevice(device));
+  auto* b = new kd_batch;
+  std::unique_ptr<kd_batch> guard(b);
+  b->device = device;
+  KD_CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  for (int i = 0; i < n_models; ++i) {
+    if (!models[i]) return fail(KD_ERR_INVALID_ARGUMENT, "null model");
+    b->models.push_back(models[i]->m);
+  }
+  b->n_worlds = n_worlds;
+  // model tables
+  std::vector<DevModel> dm(n_models);
+  std::vector<DevBody> bodies;
+  std::vector<DevJoint> joints;
+  std::vector<DevGeom> geoms;
+  std::vector<DevPair> pairs;
+  std::vector<int> contact_cap(n_models), row_cap(n_models);
+  for (int i = 0; i < n_models; ++i) {
+    const HostModel& m = b->models[i];
+    DevModel& d = dm[i];
+    d.nb = (int)m.bodies.size();
+    d.nj = (int)m.joints.size();
+    d.ng = (int)m.geoms.size();
+    d.npairs = (int)m.pairs.size();
+    d.n_bil = m.n_bil;
+    d.n_dyn = m.n_dyn;
+    d.n_limited = m.info.n_limited_joints;
+    // contact capacity: every supported pair can produce 1 (4 for box-plane)
+    // contact, capped for large piles at 6 per geom (+16); overflow is an error.
+    contact_cap[i] = std::min(m.info.max_contacts, 6 * d.ng + 16);
+    d.max_contacts = contact_cap[i];
+    row_cap[i] = d.n_bil + d.n_dyn + 2 * d.n_limited + 3 * contact_cap[i];
+    d.row_cap = row_cap[i];
+    d.body_off = (int)bodies.size();
+    d.joint_off = (int)joints.size();
+    d.geom_off = (int)geoms.size();
+    d.pair_off = (int)pairs.size();
+    for (int k = 0; k < 3; ++k) d.gravity[k] = m.gravity[k];
+    bodies.insert(bodies.end(), m.bodies.begin(), m.bodies.end());
+    joints.insert(joints.end(), m.joints.begin(), m.joints.end());
+    geoms.insert(geoms.end(), m.geoms.begin(), m.geoms.end());
+    pairs.insert(pairs.end(), m.pairs.begin(), m.pairs.end());
+  }
+  // world layout
+  b->world_model.assign(world_model, world_model + n_worlds);
+  b->worlds.resize(n_worlds);
+  b->pose_off.resize(n_worlds);
+  b->twist_off.resize(n_worlds);
+  b->row_off.resize(n_worlds);
+  std::vector<double> h_pose, h_twist;
+  std::vector<std::vector<int32_t>> class_worlds(4);
+  for (int w = 0; w < n_worlds; ++w) {
+    const int mi = world_model[w];
+    if (mi < 0 || mi >= n_models) return fail(KD_ERR_INVALID_ARGUMENT, "world_model index out of range");
+    const HostModel& m = b->models[mi];
+    DevWorld& W = b->worlds[w];
+    W.model = mi;
+    W.nb = (int)m.bodies.size();
+    W.pose_off = (int)b->pose_len;
+    W.twist_off = (int)b->twist_len;
+    W.row_off = b->total_rows;
+    W.body_off = b->total_bodies;
+    W.contact_off = b->total_contacts;
+    W.jcache_off = b->total_jcache;
+    W.lslot_off = b->total_lslots;
+    W.contact_cap = contact_cap[mi];
+    const int rc = row_cap[mi];
+    int cls = 3;
+    for (int c = 0; c < 4; ++c)
+      if (std::min(rc, kSmemMaxRows) <= kClasses[c][0]) {
+        cls = c;
+        break;
+      }
+    W.bin = cls;
+    W.smem_cap = kClasses[cls][0];
+    class_worlds[cls].push_back(w);
+    W.slab_cap = 0;
+    W.lslab_off = -1;
+    if (rc > kSmemMaxRows) {
+      W.slab_cap = std::min(rc, kDenseGlobalMaxRows);
+      W.lslab_off = b->total_lslab;
+      b->total_lslab += (int64_t)W.slab_cap * (W.slab_cap + 1) / 2;
+      b->global_bin.worlds.push_back(w);
+    }
+    if (rc > kDenseGlobalMaxRows) {
+      b->cr_auto_bin.worlds.push_back(w);
+      b->cr_auto_bin.cap = std::max(b->cr_auto_bin.cap, rc);
+      b->cr_auto_bin.nbcap = std::max(b->cr_auto_bin.nbcap, W.nb);
+    }
+    b->cr_all_bin.worlds.push_back(w);
+    b->cr_all_bin.cap = std::max(b->cr_all_bin.cap, rc);
+    b->cr_all_bin.nbcap = std::max(b->cr_all_bin.nbcap, W.nb);
+    b->pose_off[w] = W.pose_off;
+    b->twist_off[w] = W.twist_off;
+    b->row_off[w] = W.row_off;
+    b->pose_len += 7 * W.nb;
+    b->twist_len += 6 * W.nb;
+    b->total_rows += rc;
+    b->total_bodies += W.nb;
+    b->total_contacts += contact_cap[mi];
+    b->total_jcache += m.n_bil + m.n_dyn;
+    b->total_lslots += 2 * m.info.n_limited_joints;
+    h_pose.insert(h_pose.end(), m.init_pose.begin(), m.init_pose.end());
+    h_twist.insert(h_twist.end(), m.init_twist.begin(), m.init_twist.end());
+  }
+  for (int c = 0; c < 4; ++c) {
+    if (class_worlds[c].empty()) continue;
+    Bin bin;
+    bin.cap = kClasses[c][0];
+    bin.nt = kClasses[c][1];
+    bin.worlds = class_worlds[c];
+    b->dense_bins.push_back(bin);
+  }
+  b->global_bin.cap = kDenseGlobalMaxRows;
+  b->global_bin.nt = 512;
+  for (Bin* bin : {&b->cr_auto_bin, &b->cr_all_bin}) bin->nt = bin->cap > 256 ? 512 : (bin->cap > 128 ? 256 : 128);
+  if (cr_smem_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) > 232448)
+    return fail(KD_ERR_CAPACITY, "matrix-free path: world too large for one CTA's shared memory");
+
+  // device allocations
+  BatchView& v = b->view;
+  DevMem& mem = b->mem;
+  const int64_t R = std::max<int64_t>(1, b->total_rows);
+  DevModel* d_models;
+  DevBody* d_bodies;
+  DevJoint* d_joints;
+  DevGeom* d_geoms;
+  DevPair* d_pairs;
+  DevWorld* d_worlds;
+  uint8_t* d_active;
+  KD_CK(mem.alloc(d_models, n_models));
+  KD_CK(mem.alloc(d_bodies, bodies.size()));
+  KD_CK(mem.alloc(d_joints, joints.size()));
+  KD_CK(mem.alloc(d_geoms, geoms.size()));
+  KD_CK(mem.alloc(d_pairs, pairs.size()));
+  KD_CK(mem.alloc(d_worlds, n_worlds));
+  KD_CK(mem.alloc(d_active, n_worlds));
+  KD_CK(cudaMemcpy(d_models, dm.data(), sizeof(DevModel) * dm.size(), cudaMemcpyHostToDevice));
+  if (!bodies.empty()) KD_CK(cudaMemcpy(d_bodies, bodies.data(), sizeof(DevBody) * bodies.size(), cudaMemcpyHostToDevice));
+  if (!joints.empty()) KD_CK(cudaMemcpy(d_joints, joints.data(), sizeof(DevJoint) * joints.size(), cudaMemcpyHostToDevice));
+  if (!geoms.empty()) KD_CK(cudaMemcpy(d_geoms, geoms.data(), sizeof(DevGeom) * geoms.size(), cudaMemcpyHostToDevice));
+  if (!pairs.empty()) KD_CK(cudaMemcpy(d_pairs, pairs.data(), sizeof(DevPair) * pairs.size(), cudaMemcpyHostToDevice));
+  if (n_worlds) KD_CK(cudaMemcpy(d_worlds, b->worlds.data(), sizeof(DevWorld) * n_worlds, cudaMemcpyHostToDevice));
+  {
+    std::vector<uint8_t> ones(std::max(1, n_worlds), 1);
+    KD_CK(cudaMemcpy(d_active, ones.data(), std::max(1, n_worlds), cudaMemcpyHostToDevice));
+  }
+  v.n_worlds = n_worlds;
+  v.models = d_models;
+  v.bodies = d_bodies;
+  v.joints = d_joints;
+  v.geoms = d_geoms;
+  v.pairs = d_pairs;
+  v.worlds = d_worlds;
+  v.active = d_active;
+  KD_CK(mem.alloc(v.poses, b->pose_len));
+  KD_CK(mem.alloc(v.twists, b->twist_len));
+  KD_CK(mem.alloc(v.time, n_worlds));
+  KD_CK(mem.alloc(v.wstep, n_worlds));
+  KD_CK(mem.alloc(v.rowj, R));
+  KD_CK(mem.alloc(v.rbody, 2 * R));
+  KD_CK(mem.alloc(v.rkind, R));
+  KD_CK(mem.alloc(v.lkey, 2 * R));
+  KD_CK(mem.alloc(v.rmu, R));
+  KD_CK(mem.alloc(v.bias, R));
+  KD_CK(mem.alloc(v.reg, R));
+  KD_CK(mem.alloc(v.scale, R));
+  KD_CK(mem.alloc(v.vf, R));
+  KD_CK(mem.alloc(v.x0, R));
+  KD_CK(mem.alloc(v.z0, R));
+  KD_CK(mem.alloc(v.lam, R));
+  KD_CK(mem.alloc(v.zo, R));
+  KD_CK(mem.alloc(v.imp, R));
+  KD_CK(mem.alloc(v.csr_ptr, b->total_bodies + n_worlds));
+  KD_CK(mem.alloc(v.csr, 2 * R));
+  KD_CK(mem.alloc(v.bs, b->total_bodies));
+  KD_CK(mem.alloc(v.contacts, b->total_contacts));
+  KD_CK(mem.alloc(v.ccache, b->total_contacts));
+  KD_CK(mem.alloc(v.jc_lam, b->total_jcache));
+  KD_CK(mem.alloc(v.jc_z, b->total_jcache));
+  KD_CK(mem.alloc(v.ls_lam, b->total_lslots));
+  KD_CK(mem.alloc(v.ls_z, b->total_lslots));
+  KD_CK(mem.alloc(v.ls_valid, b->total_lslots));
+  KD_CK(mem.alloc(v.lslab, b->total_lslab));
+  KD_CK(mem.alloc(b->d_hist, 1));
+  KD_CK(mem.alloc(b->d_err, 4));
+  v.hist = b->d_hist;
+  v.hist_cap = 0;
+  v.error_count = b->d_err;
+  if (b->pose_len) KD_CK(cudaMemcpy(v.poses, h_pose.data(), 8 * b->pose_len, cudaMemcpyHostToDevice));
+  if (b->twist_len) KD_CK(cudaMemcpy(v.twists, h_twist.data(), 8 * b->twist_len, cudaMemcpyHostToDevice));
+  for (Bin* bin : {&b->global_bin, &b->cr_auto_bin, &b->cr_all_bin}) {
+    bin->count = (int)bin->worlds.size();
+    if (bin->count) {
+      KD_CK(mem.alloc(bin->d_worlds, bin->count));
+      KD_CK(cudaMemcpy(bin->d_worlds, bin->worlds.data(), 4 * bin->count, cudaMemcpyHostToDevice));
+    }
+  }
+  for (Bin& bin : b->dense_bins) {
+    bin.count = (int)bin.worlds.size();
+    KD_CK(mem.alloc(bin.d_worlds, bin.count));
+    KD_CK(cudaMemcpy(bin.d_worlds, bin.worlds.data(), 4 * bin.count, cudaMemcpyHostToDevice));
+  }
+  for (cudaEvent_t& e : b->ev) KD_CK(cudaEventCreate(&e));
+  KD_CK(cudaDeviceSynchronize());
+  *out = guard.release();
+  return KD_OK;
+}
+
+void kd_batch_destroy(kd_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  delete b;
+}
+
+int kd_batch_size(const kd_batch* b, int32_t* nw, int64_t* pl, int64_t* tl) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  if (nw) *nw = b->n_worlds;
+  if (pl) *pl = b->pose_len;
+  if (tl) *tl = b->twist_len;
+  return KD_OK;
+}
+
+int kd_batch_offsets(const kd_batch* b, int32_t* po, int32_t* to) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  for (int w = 0; w < b->n_worlds; ++w) {
+    if (po) po[w] = b->pose_off[w];
+    if (to) to[w] = b->twist_off[w];
+  }
+  return KD_OK;
+}
+
+int kd_batch_set_state(kd_batch* b, const double* poses, const double* twists, const double* time) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
+  if (poses && b->pose_len) KD_CK(cudaMemcpy(b->view.poses, poses, 8 * b->pose_len, cudaMemcpyHostToDevice));
+  if (twists && b->twist_len) KD_CK(cudaMemcpy(b->view.twists, twists, 8 * b->twist_len, cudaMemcpyHostToDevice));
+  if (time && b->n_worlds) KD_CK(cudaMemcpy(b->view.time, time, 8 * b->n_worlds, cudaMemcpyHostToDevice));
+  return KD_OK;
+}
+
+int kd_batch_get_state(kd_batch* b, double* poses, double* twists, double* time) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
+  KD_CK(cudaStreamSynchronize(b->stream));
+  if (poses && b->pose_len) KD_CK(cudaMemcpy(poses, b->view.poses, 8 * b->pose_len, cudaMemcpyDeviceToHost));
+  if (twists && b->twist_len) KD_CK(cudaMemcpy(twists, b->view.twists, 8 * b->twist_len, cudaMemcpyDeviceToHost));
+  if (time && b->n_worlds) KD_CK(cudaMemcpy(time, b->view.time, 8 * b->n_worlds, cudaMemcpyDeviceToHost));
+  return KD_OK;
+}
+
+int kd_batch_reset_caches(kd_batch* b) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
+  std::vector<WorldStep> ws(b->n_worlds);
+  if (b->n_worlds) {
+    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+    for (WorldStep& s : ws) {
+      s.jcache_valid = 0;
+      s.ccache_count = 0;
+    }
+    KD_CK(cudaMemcpy(b->view.wstep, ws.data(), sizeof(WorldStep) * b->n_worlds, cudaMemcpyHostToDevice));
+  }
+  if (b->total_lslots) KD_CK(cudaMemset(b->view.ls_valid, 0, 4 * b->total_lslots));
+  return KD_OK;
+}
+
+int kd_batch_set_active(kd_batch* b, const uint8_t* active) {
+  if (!b || !active) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  KD_CK(cudaSetDevice(b->device));
+  if (b->n_worlds)
+    KD_CK(cudaMemcpy(const_cast<uint8_t*>(b->view.active), active, b->n_worlds, cudaMemcpyHostToDevice));
+  return KD_OK;
+}
+
+int kd_batch_set_history_capacity(kd_batch* b, int32_t cap) {
+  if (!b || cap < 0) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
+  KD_CK(cudaSetDevice(b->device));
+  double* h = nullptr;
+  KD_CK(b->mem.alloc(h, (size_t)std::max(1, cap) * std::max(1, b->n_worlds)));
+  b->d_hist = h;
+  b->hist_cap = cap;
+  b->view.hist = h;
+  b->view.hist_cap = cap;
+  return KD_OK;
+}
+
+int kd_batch_get_history(kd_batch* b, double* out) {
+  if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  KD_CK(cudaSetDevice(b->device));
+  if (b->hist_cap && b->n_worlds)
+    KD_CK(cudaMemcpy(out, b->d_hist, 8 * (size_t)b->hist_cap * b->n_worlds, cudaMemcpyDeviceToHost));
+  return KD_OK;
+}
+
+int kd_batch_enable_timing(kd_batch* b, int32_t on) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  b->timing = on != 0;
+  for (double& m : b->ms) m = 0.0;
+  b->launches = 0;
+  return KD_OK;
+}
+
+int kd_batch_get_timing(kd_batch* b, double* ms4, int64_t* launches) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  if (ms4)
+    for (int i = 0; i < 4; ++i) ms4[i] = b->ms[i];
+  if (launches) *launches = b->launches;
+  return KD_OK;
+}
+
+int kd_batch_step(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
+  if (!b || !c) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (b->n_worlds == 0 || n_steps <= 0) return KD_OK;
+  KD_CK(cudaSetDevice(b->device));
+  StepParams sp{};
+  sp.dt = c->dt;
+  sp.eta = c->eta;
+  sp.rho = c->rho;
+  sp.eps = c->eps;
+  sp.beta = c->baumgarte_beta;
+  sp.contact_margin = c->contact_margin;
+  sp.impact_thr = c->impact_velocity_threshold;
+  sp.bias_clamp = c->bias_clamp;
+  sp.lim_margin_ang = c->limit_margin_angular;
+  sp.lim_margin_lin = c->limit_margin_linear;
+  sp.max_iters = c->max_iters;
+  sp.acceleration = c->acceleration;
+  sp.restart = c->restart;
+  sp.fixed_mode = c->fixed_iteration_mode;
+  sp.cr_iters = c->cr_iters;
+  sp.warm_start = c->warm_start;
+  sp.moreau = c->integrator == KD_INTEGRATOR_MOREAU_JEAN;
+  sp.backend = c->backend;
+  KD_CK(cudaMemsetAsync(b->d_err, 0, 16, b->stream));
+  const BatchView& v = b->view;
+  cudaStream_t s = b->stream;
+  auto mark = [&](int i) {
+    if (b->timing) cudaEventRecord(b->ev[i], s);
+  };
+  for (int k = 0; k < n_steps; ++k) {
+    mark(0);
+    launch_assemble(v, sp, s);
+    KD_CK(cudaGetLastError());
+    ++b->launches;
+    mark(1);
+    if (c->backend != KD_BACKEND_MATRIX_FREE) {
+      for (const Bin& bin : b->dense_bins) {
+        KD_CK(launch_dense(v, sp, bin.d_worlds, bin.count, bin.cap, bin.nt, false, s));
+        ++b->launches;
+      }
+      if (b->global_bin.count) {
+        KD_CK(launch_dense(v, sp, b->global_bin.d_worlds, b->global_bin.count, b->global_bin.cap, 512, true, s));
+        ++b->launches;
+      }
+    }
+    mark(2);
+    const Bin& cr = c->backend == KD_BACKEND_MATRIX_FREE ? b->cr_all_bin
+                    : c->backend == KD_BACKEND_AUTO      ? b->cr_auto_bin
+                                                         : b->global_bin /* unused */;
+    if (c->backend != KD_BACKEND_DENSE && cr.count) {
+      KD_CK(launch_cr(v, sp, cr.d_worlds, cr.count, cr.cap, cr.nbcap, cr.nt, s));
+      ++b->launches;
+    }
+    mark(3);
+    launch_recover(v, sp, s);
+    ++b->launches;
+    mark(4);
+    KD_CK(cudaGetLastError());
+    if (b->timing) {
+      KD_CK(cudaEventSynchronize(b->ev[4]));
+      float t;
+      for (int i = 0; i < 4; ++i) {
+        cudaEventElapsedTime(&t, b->ev[i], b->ev[i + 1]);
+        // ev: 0 assemble 1 dense 2 cr 3 recover 4
+        const int slot = i == 0 ? 0 : (i == 1 ? 1 : (i == 2 ? 2 : 3));
+        b->ms[slot] += t;
+      }
+    }
+  }
+  KD_CK(cudaStreamSynchronize(b->stream));
+  int32_t err[4];
+  KD_CK(cudaMemcpy(err, b->d_err, 16, cudaMemcpyDeviceToHost));
+  if (err[0]) return fail(KD_ERR_SPD_FAILURE, "Delassus factorization failed on an SPD system (" +
+                                                  std::to_string(err[0]) + " worlds)");
+  if (err[1]) return fail(KD_ERR_CAPACITY, "contact or dense-slab capacity exceeded in " + std::to_string(err[1]) +
+                                               " worlds");
+  return KD_OK;
+}
+
+int kd_batch_get_diagnostics(kd_batch* b, kd_step_diag* out) {
+  if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  KD_CK(cudaSetDevice(b->device));
+  std::vector<WorldStep> ws(b->n_worlds);
+  if (b->n_worlds)
+    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+  for (int w = 0; w < b->n_worlds; ++w) {
+    const WorldStep& s = ws[w];
+    const HostModel& m = b->models[b->world_model[w]];
+    kd_step_diag& o = out[w];
+    std::memset(&o, 0, sizeof(o));
+    o.iterations = s.iterations;
+    o.restarts = s.restarts;
+    o.converged = s.converged;
+    o.cr_breakdown = s.cr_breakdown;
+    o.cr_iterations = s.cr_iterations;
+    o.r_p = s.r_p;
+    o.r_d = s.r_d;
+    o.r_c = s.r_c;
+    o.n_rows = std::max(0, s.n_rows);
+    o.contact_count = s.n_contacts;
+    o.first_contact_row = m.n_bil + m.n_dyn + s.n_limits;
+    o.n_limits = s.n_limits;
+    o.f_inf = s.f_inf;
+    o.kkt_momentum_inf = s.kkt;
+    o.bilateral_velocity_inf = s.bil_vel;
+  }
+  return KD_OK;
+}
+
+int kd_batch_row_offsets(const kd_batch* b, int64_t* ro, int64_t* total) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  for (int w = 0; w < b->n_worlds; ++w) ro[w] = b->row_off[w];
+  if (total) *total = b->total_rows;
+  return KD_OK;
+}
+
+int kd_batch_get_impulses(kd_batch* b, double* out) {
+  if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  KD_CK(cudaSetDevice(b->device));
+  KD_CK(cudaMemcpy(out, b->view.imp, 8 * b->total_rows, cudaMemcpyDeviceToHost));
+  return KD_OK;
+}
+
+int kd_batch_dump_rows(kd_batch* b, int32_t w, kd_row_dump* out, int32_t cap, int32_t* n_rows) {
+  if (!b || !out || !n_rows || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
+  KD_CK(cudaSetDevice(b->device));
+  WorldStep s;
+  KD_CK(cudaMemcpy(&s, b->view.wstep + w, sizeof(s), cudaMemcpyDeviceToHost));
+  const int n = std::max(0, s.n_rows);
+  *n_rows = n;
+  if (n > cap) return fail(KD_ERR_CAPACITY, "dump capacity too small");
+  if (n == 0) return KD_OK;
+  const int64_t R0 = b->row_off[w];
+  std::vector<RowJ> rj(n);
+  std::vector<int32_t> rb(2 * n), rk(n);
+  std::vector<double> bias(n), reg(n), scale(n), vf(n), lam(n), zo(n);
+  const BatchView& v = b->view;
+  KD_CK(cudaMemcpy(rj.data(), v.rowj + R0, sizeof(RowJ) * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(rb.data(), v.rbody + 2 * R0, 8 * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(rk.data(), v.rkind + R0, 4 * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(bias.data(), v.bias + R0, 8 * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(reg.data(), v.reg + R0, 8 * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(scale.data(), v.scale + R0, 8 * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(vf.data(), v.vf + R0, 8 * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(lam.data(), v.lam + R0, 8 * n, cudaMemcpyDeviceToHost));
+  KD_CK(cudaMemcpy(zo.data(), v.zo + R0, 8 * n, cudaMemcpyDeviceToHost));
+  for (int r = 0; r < n; ++r) {
+    kd_row_dump& o = out[r];
+    std::memset(&o, 0, sizeof(o));
+    o.body_a = rb[2 * r];
+    o.body_b = rb[2 * r + 1];
+    o.kind = rk[r];
+    for (int k = 0; k < 6; ++k) {
+      o.block_a[k] = rj[r].J[k];
+      o.block_b[k] = rj[r].J[6 + k];
+    }
+    o.bias = bias[r];
+    o.reg = reg[r];
+    o.scale = scale[r];
+    o.vf_scaled = vf[r];
+    o.lambda = lam[r];
+    o.z = zo[r];
+  }
+  return KD_OK;
+}
+
+int kd_batch_dump_contacts(kd_batch* b, int32_t w, int32_t* geoms, double* data9, int32_t cap, int32_t* nc) {
+  if (!b || !nc || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
+  KD_CK(cudaSetDevice(b->device));
+  WorldStep s;
+  KD_CK(cudaMemcpy(&s, b->view.wstep + w, sizeof(s), cudaMemcpyDeviceToHost));
+  *nc = std::max(0, s.n_contacts);
+  if (*nc > cap) return fail(KD_ERR_CAPACITY, "dump capacity too small");
+  std::vector<Contact> ct(*nc);
+  if (*nc)
+    KD_CK(cudaMemcpy(ct.data(), b->view.contacts + b->worlds[w].contact_off, sizeof(Contact) * *nc,
+                     cudaMemcpyDeviceToHost));
+  for (int c = 0; c < *nc; ++c) {
+    geoms[2 * c] = ct[c].ga;
+    geoms[2 * c + 1] = ct[c].gb;
+    double* d = data9 + 9 * c;
+    for (int k = 0; k < 3; ++k) {
+      d[k] = ct[c].pos[k];
+      d[3 + k] = ct[c].nrm[k];
+    }
+    d[6] = ct[c].depth;
+    d[7] = ct[c].mu;
+    d[8] = ct[c].e;
+  }
+  return KD_OK;
+}
+
+int kd_batch_dump_limits(kd_batch* b, int32_t w, int32_t* keys2, int32_t cap, int32_t* nl) {
+  if (!b || !nl || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
+  KD_CK(cudaSetDevice(b->device));
+  WorldStep s;
+  KD_CK(cudaMemcpy(&s, b->view.wstep + w, sizeof(s), cudaMemcpyDeviceToHost));
+  *nl = std::max(0, s.n_limits);
+  if (*nl > cap) return fail(KD_ERR_CAPACITY, "dump capacity too small");
+  const HostModel& m = b->models[b->world_model[w]];
+  const int64_t first = b->row_off[w] + m.n_bil + m.n_dyn;
+  if (*nl) KD_CK(cudaMemcpy(keys2, b->view.lkey + 2 * first, 8 * *nl, cudaMemcpyDeviceToHost));
+  return KD_OK;
+}
+
+int kd_bench_jitter(uint64_t seed, double sigma, int32_t n_worlds, const int32_t* n_bodies, double* twists6) {
+  if (!n_bodies || !twists6) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (seed == 0) return KD_OK;  // main.cpp:204: jitter only for seed != 0
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> jitter(0.0, sigma);
+  int64_t off = 0;
+  for (int w = 0; w < n_worlds; ++w)
+    for (int b = 0; b < n_bodies[w]; ++b, off += 6)
+      for (int k = 0; k < 3; ++k) {
+        twists6[off + k] += jitter(rng);
+        twists6[off + 3 + k] += jitter(rng);
+      }
+  return KD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,379 @@
+// kd_cr.cu — K2b: fused PADMM + warm-started matrix-free Conjugate Residual,
+// one CTA per world (worlds with n > 300 under Auto, or backend = sparse).
+//
+// Restates MatrixFreeDelassus::apply (delassus.cpp:106-122) with the baked rows
+// of bake_jacobian (130-154) recomputed on the fly (ja = p J, jma = fold(ja):
+// the same floating-point operations, half the bytes), cr_solve (156-187) with
+// the fixed budget and breakdown guard, DelassusBackend::solve accounting
+// (189-197), and the PADMM loop of padmm.cpp:87-159.
+// The scatter J^T v runs per body over its ascending row list (the reference's
+// accumulation order); dot products use a fixed-order block reduction, so the
+// result is deterministic run to run.  All n-vectors and the per-body scratch
+// live in shared memory; Jacobian rows stream from L2/HBM (the HBM-bound leg of
+// the roofline).
+#include "kd_device.cuh"
+
+namespace kd {
+
+namespace {
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = red[0];
+#pragma unroll
+  for (int k = 1; k < NW; ++k) s += red[k];
+  return s;
+}
+
+template <int NT>
+__device__ __forceinline__ void block_max3(double& a, double& b, double& c, double* red) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  a = warp_max(a);
+  b = warp_max(b);
+  c = warp_max(c);
+  __syncthreads();
+  if (lane == 0) {
+    red[3 * wid] = a;
+    red[3 * wid + 1] = b;
+    red[3 * wid + 2] = c;
+  }
+  __syncthreads();
+  a = red[0];
+  b = red[1];
+  c = red[2];
+#pragma unroll
+  for (int k = 1; k < NW; ++k) {
+    a = fmax(a, red[3 * k]);
+    b = fmax(b, red[3 * k + 1]);
+    c = fmax(c, red[3 * k + 2]);
+  }
+}
+
+struct CrCtx {
+  int n, nb;
+  const RowJ* rj;
+  const int32_t* rb;
+  const int32_t* cptr;
+  const int32_t* clist;
+  const double* P;      // smem
+  const double* dadd;   // smem: P^2 R + (eta + rho)
+  const double* binv;   // smem: per body [inv_mass, Iwinv(9)]
+  double* scratch;      // smem: 6 nb
+};
+
+// out = D_{eta,rho} v   (MatrixFreeDelassus::apply)
+template <int NT>
+__device__ void apply_op(const CrCtx& c, const double* v, double* out) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  for (int u = tid; u < 6 * c.nb; u += NT) {
+    const int b = u / 6, k = u - 6 * b;
+    double s = 0.0;
+    for (int e = c.cptr[b]; e < c.cptr[b + 1]; ++e) {
+      const int code = c.clist[e];
+      const int r = code >> 1;
+      s += (c.P[r] * c.rj[r].J[6 * (code & 1) + k]) * v[r];
+    }
+    c.scratch[u] = s;
+  }
+  __syncthreads();
+  for (int r = tid; r < c.n; r += NT) {
+    const double p = c.P[r];
+    double s = c.dadd[r] * v[r];
+    for (int side = 0; side < 2; ++side) {
+      const int b = c.rb[2 * r + side];
+      if (b < 0) continue;
+      const double* J = c.rj[r].J + 6 * side;
+      const double* bi = c.binv + 10 * b;
+      double ja[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) ja[k] = p * J[k];
+      // jma = fold_inverse_mass(ja) (delassus.cpp:12-17)
+      double jm[6];
+      jm[0] = ja[0] * bi[0];
+      jm[1] = ja[1] * bi[0];
+      jm[2] = ja[2] * bi[0];
+      const double* I = bi + 1;
+      jm[3] = ja[3] * I[0] + ja[4] * I[3] + ja[5] * I[6];
+      jm[4] = ja[3] * I[1] + ja[4] * I[4] + ja[5] * I[7];
+      jm[5] = ja[3] * I[2] + ja[4] * I[5] + ja[5] * I[8];
+      const double* sc = c.scratch + 6 * b;
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) t += jm[k] * sc[k];
+      s += t;
+    }
+    out[r] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void project_soc(const double w[3], double mu, double y[3]) {
+  const double wn = w[0];
+  const double tn = sqrt(w[1] * w[1] + w[2] * w[2]);
+  y[0] = w[0];
+  y[1] = w[1];
+  y[2] = w[2];
+  if (tn <= mu * wn) return;
+  if (mu * tn <= -wn) {
+    y[0] = y[1] = y[2] = 0.0;
+    return;
+  }
+  const double tau = (wn + mu * tn) / (1.0 + mu * mu);
+  y[0] = tau;
+  if (tn > 0) {
+    y[1] = mu * tau * w[1] / tn;
+    y[2] = mu * tau * w[2] / tn;
+  } else {
+    y[1] = y[2] = 0.0;
+  }
+}
+
+}  // namespace
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) cr_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
+  extern __shared__ __align__(16) double smem[];
+  const int w = bin_worlds[blockIdx.x];
+  WorldStep& ws = bv.wstep[w];
+  if (ws.backend != BE_MATRIX_FREE) return;
+  const int tid = threadIdx.x;
+  const DevWorld W = bv.worlds[w];
+  const int n = ws.n_rows;
+  const int nb = W.nb;
+  const int64_t R0 = W.row_off;
+  // shared layout
+  double* P = smem;
+  double* dadd = P + n;
+  double* xs = dadd + n;   // x
+  double* rr = xs + n;     // r
+  double* ar = rr + n;     // A r
+  double* pp = ar + n;     // p
+  double* ap = pp + n;     // A p
+  double* rhs = ap + n;
+  double* yv = rhs + n;
+  double* zv = yv + n;
+  double* yh = zv + n;
+  double* zh = yh + n;
+  double* vf = zh + n;
+  double* binv = vf + n;       // 10 nb
+  double* scratch = binv + 10 * nb;  // 6 nb
+  double* red = scratch + 6 * nb;    // 3 * NW
+
+  const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
+  for (int r = tid; r < n; r += NT) {
+    const double p = bv.scale[R0 + r];
+    P[r] = p;
+    dadd[r] = p * p * bv.reg[R0 + r] + eta_rho;
+    vf[r] = bv.vf[R0 + r];
+    xs[r] = bv.x0[R0 + r];
+    zv[r] = bv.z0[R0 + r];
+  }
+  for (int b = tid; b < nb; b += NT) {
+    const BodyS& B = bv.bs[W.body_off + b];
+    binv[10 * b] = B.inv_mass;
+    for (int k = 0; k < 9; ++k) binv[10 * b + 1 + k] = B.Iwinv[k];
+  }
+  CrCtx c{n, nb, bv.rowj + R0, bv.rbody + 2 * R0, bv.csr_ptr + W.body_off + w, bv.csr + 2 * R0, P, dadd, binv,
+          scratch};
+  const int n_jd = n - ws.n_limits - 3 * ws.n_contacts;
+  const int first_contact = n_jd + ws.n_limits;
+  const int n_units = first_contact + ws.n_contacts;
+  const double* rmu = bv.rmu + R0;
+  __syncthreads();
+
+  // y = Pi_K(x0); hats
+  for (int u = tid; u < n_units; u += NT) {
+    if (u < n_jd) {
+      yv[u] = xs[u];
+    } else if (u < first_contact) {
+      yv[u] = fmax(0.0, xs[u]);
+    } else {
+      const int r = first_contact + 3 * (u - first_contact);
+      double wv[3] = {xs[r], xs[r + 1], xs[r + 2]}, yn[3];
+      project_soc(wv, rmu[r], yn);
+      for (int d = 0; d < 3; ++d) yv[r + d] = yn[d];
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < n; r += NT) {
+    yh[r] = yv[r];
+    zh[r] = zv[r];
+  }
+  double a = 1.0, prev = __longlong_as_double(0x7ff0000000000000ll);
+  double r_p = 0, r_d = 0, r_c = 0;
+  int restarts = 0, it;
+  bool converged = false;
+  long long cr_total = 0;
+  bool cr_break = false;
+  const int hcap = bv.hist_cap;
+  for (it = 1; it <= sp.max_iters; ++it) {
+    __syncthreads();
+    // rhs = -(v_f + s - eta x - rho y_hat - z_hat)
+    for (int r = tid; r < n; r += NT) {
+      double s = 0.0;
+      if (r >= first_contact && ((r - first_contact) % 3) == 0) s = rmu[r] * hypot(zh[r + 1], zh[r + 2]);
+      rhs[r] = -((((vf[r] + s) - eta * xs[r]) - rho * yh[r]) - zh[r]);
+    }
+    // ---- cr_solve(op, rhs, x, budget)
+    apply_op<NT>(c, xs, ar);
+    double loc = 0.0;
+    for (int r = tid; r < n; r += NT) rr[r] = rhs[r] - ar[r];
+    apply_op<NT>(c, rr, ar);
+    for (int r = tid; r < n; r += NT) {
+      pp[r] = rr[r];
+      ap[r] = ar[r];
+      loc += rr[r] * ar[r];
+    }
+    double rar = block_sum<NT>(loc, red);
+    loc = 0.0;
+    for (int r = tid; r < n; r += NT) loc += rhs[r] * rhs[r];
+    const double rhs2 = block_sum<NT>(loc, red);
+    const double beps = 1e-30 * fmax(1.0, rhs2);
+    int iters = 0;
+    bool brk = false;
+    for (int k = 0; k < sp.cr_iters; ++k) {
+      loc = 0.0;
+      for (int r = tid; r < n; r += NT) loc += ap[r] * ap[r];
+      const double apap = block_sum<NT>(loc, red);
+      if (!(rar > beps) || !(apap > beps)) {
+        brk = true;
+        break;
+      }
+      const double alpha = rar / apap;
+      for (int r = tid; r < n; r += NT) {
+        xs[r] += alpha * pp[r];
+        rr[r] -= alpha * ap[r];
+      }
+      apply_op<NT>(c, rr, ar);
+      loc = 0.0;
+      for (int r = tid; r < n; r += NT) loc += rr[r] * ar[r];
+      const double rar_next = block_sum<NT>(loc, red);
+      const double beta = rar_next / rar;
+      for (int r = tid; r < n; r += NT) {
+        pp[r] = rr[r] + beta * pp[r];
+        ap[r] = ar[r] + beta * ap[r];
+      }
+      rar = rar_next;
+      ++iters;
+    }
+    cr_total += iters;
+    if (brk) {
+      loc = 0.0;
+      for (int r = tid; r < n; r += NT) loc += rr[r] * rr[r];
+      const double rn = sqrt(block_sum<NT>(loc, red));
+      if (rn > 1e-9 * fmax(1.0, sqrt(rhs2))) cr_break = true;
+    }
+    __syncthreads();
+    // ---- projection, dual update, residuals (padmm.cpp:120-123)
+    double rp = 0.0, dmax = 0.0, rc = 0.0;
+    for (int u = tid; u < n_units; u += NT) {
+      const int r = u < first_contact ? u : first_contact + 3 * (u - first_contact);
+      const int nr = u < first_contact ? 1 : 3;
+      double wv[3], yn[3];
+      for (int d = 0; d < nr; ++d) wv[d] = xs[r + d] - zh[r + d] / rho;
+      if (u >= first_contact) project_soc(wv, rmu[r], yn);
+      else if (u >= n_jd) yn[0] = fmax(0.0, wv[0]);
+      else yn[0] = wv[0];
+      double ymax = 0.0, zmax = 0.0;
+      for (int d = 0; d < nr; ++d) {
+        const double zn = zh[r + d] - rho * (xs[r + d] - yn[d]);
+        rp = fmax(rp, fabs(xs[r + d] - yn[d]));
+        dmax = fmax(dmax, fabs(yn[d] - yv[r + d]));
+        ymax = fmax(ymax, fabs(yn[d]));
+        zmax = fmax(zmax, fabs(zn));
+        // y_prev, z_prev are kept in yh/zh until the Nesterov step below
+        yh[r + d] = yv[r + d];
+        zh[r + d] = zv[r + d];
+        yv[r + d] = yn[d];
+        zv[r + d] = zn;
+      }
+      if (u >= n_jd) rc = fmax(rc, fmin(ymax, zmax));
+    }
+    block_max3<NT>(rp, dmax, rc, red);
+    r_p = rp;
+    r_d = rho * dmax;
+    r_c = rc;
+    const double combined = fmax(r_p, fmax(r_d, r_c));
+    if (tid == 0 && it <= hcap) bv.hist[(int64_t)w * hcap + it - 1] = combined;
+    if (!sp.fixed_mode && combined < sp.eps) {
+      converged = true;
+      break;
+    }
+    if (sp.acceleration) {
+      const bool restart = sp.restart && combined > prev;
+      if (restart) {
+        a = 1.0;
+        ++restarts;
+        for (int r = tid; r < n; r += NT) {
+          yh[r] = yv[r];
+          zh[r] = zv[r];
+        }
+      } else {
+        const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));
+        const double beta = (a - 1.0) / an;
+        for (int r = tid; r < n; r += NT) {
+          yh[r] = yv[r] + beta * (yv[r] - yh[r]);
+          zh[r] = zv[r] + beta * (zv[r] - zh[r]);
+        }
+        a = an;
+      }
+    } else {
+      for (int r = tid; r < n; r += NT) {
+        yh[r] = yv[r];
+        zh[r] = zv[r];
+      }
+    }
+    prev = combined;
+  }
+  __syncthreads();
+  for (int r = tid; r < n; r += NT) {
+    bv.lam[R0 + r] = yv[r];
+    bv.zo[R0 + r] = zv[r];
+  }
+  if (tid == 0) {
+    const int done = min(it, sp.max_iters);
+    ws.iterations = done;
+    ws.r_p = r_p;
+    ws.r_d = r_d;
+    ws.r_c = r_c;
+    ws.restarts = restarts;
+    ws.converged = (converged || fmax(r_p, fmax(r_d, r_c)) < sp.eps) ? 1 : 0;
+    ws.cr_iterations = cr_total;
+    ws.cr_breakdown = cr_break ? 1 : 0;
+    for (int i = done; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
+  }
+}
+
+size_t cr_smem_bytes(int n, int nb, int nt) { return 8 * ((size_t)13 * n + 16 * (size_t)nb + 3 * (nt / 32) + 8); }
+
+template <int NT>
+static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap,
+                               int nbcap, cudaStream_t s) {
+  const size_t smem = cr_smem_bytes(ncap, nbcap, NT);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    const cudaError_t e = cudaFuncSetAttribute(cr_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cr_kernel<NT><<<count, NT, smem, s>>>(bv, sp, worlds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
+                      int nt, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  if (nt <= 128) return launch_cr_t<128>(bv, sp, worlds, count, ncap, nbcap, s);
+  if (nt <= 256) return launch_cr_t<256>(bv, sp, worlds, count, ncap, nbcap, s);
+  return launch_cr_t<512>(bv, sp, worlds, count, ncap, nbcap, s);
+}
+
+}  // namespace kd

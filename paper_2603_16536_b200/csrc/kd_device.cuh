@@ -1,0 +1,56 @@
+// kd_device.cuh — device helpers shared by the step kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kd_layout.h"
+#include "kd_math.cuh"
+
+namespace kd {
+
+__device__ __forceinline__ V3 ld3(const double* p) { return V3{p[0], p[1], p[2]}; }
+__device__ __forceinline__ Q4 ldq(const double* p) { return Q4{p[0], p[1], p[2], p[3]}; }
+__device__ __forceinline__ M3 ldm(const double* p) {
+  M3 m;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) m.m[i] = p[i];
+  return m;
+}
+__device__ __forceinline__ void st3(double* p, V3 v) {
+  p[0] = v.x;
+  p[1] = v.y;
+  p[2] = v.z;
+}
+__device__ __forceinline__ void stm(double* p, const M3& m) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) p[i] = m.m[i];
+}
+
+// Warp exclusive prefix sum; returns the warp total.
+__device__ __forceinline__ int warp_exclusive_sum(int v, int lane, int& excl) {
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  excl = incl - v;
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// max is exactly associative/commutative: any reduction order gives the
+// reference's serial lpNorm<Infinity> result bit for bit.
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Fixed-order (deterministic) butterfly sum.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace kd

@@ -1,0 +1,45 @@
+// kd_host.h — host-side structures of the C-ABI implementation.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/kamino_b200.h"
+#include "kd_layout.h"
+#include "kd_math.cuh"
+
+namespace kd {
+
+struct HostModel {
+  std::string name;
+  double gravity[3] = {0, 0, -9.81};
+  std::vector<DevBody> bodies;
+  std::vector<DevJoint> joints;
+  std::vector<DevGeom> geoms;
+  std::vector<DevPair> pairs;
+  std::vector<std::string> body_names, joint_names;
+  std::vector<double> init_pose, init_twist;
+  int n_bil = 0, n_dyn = 0, n_loops = 0;
+  kd_model_info info{};
+};
+
+int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err);
+double host_joint_coordinate(const HostModel& m, int joint, const double* poses7);
+
+// kernel launchers (one per translation unit)
+void launch_assemble(const BatchView& bv, const StepParams& sp, cudaStream_t s);
+cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int cap, int nt,
+                  bool global_l, cudaStream_t s);
+cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
+               int nt, cudaStream_t s);
+void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s);
+size_t dense_smem_bytes(int n, int nt, bool global_l);
+size_t cr_smem_bytes(int n, int nb, int nt);
+
+}  // namespace kd
+
+struct kd_model {
+  kd::HostModel m;
+};

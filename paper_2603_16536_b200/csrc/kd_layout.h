@@ -1,0 +1,181 @@
+// kd_layout.h — HBM data layout of a device-resident world batch.
+//
+// Model data (immutable, shared by all worlds of a model; L2/L1-resident):
+//   DevModel (one per model) indexes arrays of DevBody / DevJoint / DevGeom /
+//   DevPair.  These are the reference MechanismModel (model.hpp:97-113) with
+//   the row layout (JointLayout, model.hpp:63-74), frame rotations and the
+//   ordered collision-pair list (contacts.cpp:119-145) precomputed on the host.
+//
+// World state (the WorldBatch storage, batch.hpp:41-42): poses7 / twists6 in the
+//   reference AoS-per-world layout with prefix-sum offsets, so host<->device
+//   copies are single memcpys and a CTA/warp reads one contiguous slab.
+//
+// Per-step scratch (SoA over rows / bodies / contacts, each world owning a
+//   capacity-sized slab at a prefix-sum offset): rows are addressed
+//   row_off[w] + r with r in the reference row order
+//   [bilateral | dynamics | limits | contacts] (constraints.hpp:33-38).
+#pragma once
+
+#include <stdint.h>
+
+namespace kd {
+
+enum JointKind : int32_t { J_FIXED = 0, J_REVOLUTE = 1, J_PRISMATIC = 2, J_SPHERICAL = 3 };
+enum GeomShape : int32_t { G_SPHERE = 0, G_PLANE = 1, G_BOX = 2 };
+// Collision pair kinds in collide() dispatch order (contacts.cpp:130-140);
+// `a` is always the moving geom (ContactPoint::geom_a), `b` the other one.
+enum PairKind : int32_t { P_SPHERE_SPHERE = 0, P_SPHERE_PLANE = 1, P_BOX_PLANE = 2 };
+enum RowKind : int32_t { ROW_BILATERAL = 0, ROW_LIMIT = 1, ROW_CONTACT = 2 };
+enum Backend : int32_t { BE_NONE = -1, BE_DENSE_SMEM = 0, BE_DENSE_GLOBAL = 1, BE_MATRIX_FREE = 2 };
+
+enum JointFlags : int32_t {
+  JF_PD = 1,
+  JF_ARMATURE = 2,
+  JF_DAMPING = 4,
+  JF_LIMITS = 8,
+};
+
+struct DevBody {
+  double mass, inv_mass;
+  double ib[9];  // body-frame inertia
+};
+
+struct DevJoint {
+  int32_t type, parent, child, flags;
+  int32_t row_offset, row_count, dyn_offset, limit_slot;  // limit_slot: index among limited joints
+  double fp_pos[3], fc_pos[3];
+  double fp_q[4], fc_q[4];     // frame orientations [w,x,y,z]
+  double fp_R[9], fc_R[9];     // Eigen toRotationMatrix of the frame orientations
+  double axis[3], comp0[3], comp1[3];
+  double lower, upper, kp, kd, target, target_rate, armature, damping;
+};
+
+struct DevGeom {
+  int32_t body, shape, pad0, pad1;
+  double radius, he[3], normal[3], offset, mu, restitution;
+};
+
+struct DevPair {
+  int32_t a, b, kind, pad;
+};
+
+struct DevModel {
+  int32_t nb, nj, ng, npairs;
+  int32_t n_bil, n_dyn, n_limited, max_contacts;
+  int32_t row_cap, body_off, joint_off, geom_off;
+  int32_t pair_off, pad0, pad1, pad2;
+  double gravity[3];
+  double pad3;
+};
+
+// Per-world indexing (prefix sums over model capacities).
+struct DevWorld {
+  int32_t model, nb, pose_off, twist_off;
+  int64_t row_off;      // rows (capacity n_bil + n_dyn + 2 n_limited + 3 contact_cap)
+  int32_t body_off;     // bodies
+  int32_t contact_off;  // contacts
+  int32_t jcache_off;   // n_bil + n_dyn
+  int32_t lslot_off;    // 2 * n_limited
+  int32_t bin;          // dense-smem bin
+  int32_t smem_cap;     // rows the bin's dense-smem kernel can hold
+  int32_t contact_cap;  // contacts this world can hold (overflow is reported, never silent)
+  int32_t slab_cap;     // rows the dense-global slab can hold (0 if none)
+  int64_t lslab_off;    // dense-global factor slab (doubles), -1 if none
+};
+
+// Per-row Jacobian blocks: J = [block_a | block_b], JM = J M^-1 folded
+// (fold_inverse_mass, delassus.cpp:12-17).
+struct RowJ {
+  double J[12];
+  double JM[12];
+};
+
+// Per-body step scratch.
+struct BodyS {
+  double ep[3];      // evaluation pose (Moreau-Jean half step)
+  double eq[4];
+  double eR[9];
+  double uf[6];      // u_free
+  double h[6];       // free forces at start-of-step poses
+  double Iw[9];      // world inertia at eval pose
+  double Iwinv[9];
+  double mass, inv_mass;
+  double up[6];      // u+
+};
+
+struct Contact {
+  int32_t ga, gb, pair, pad;
+  double pos[3], nrm[3];
+  double depth, mu, e;
+};
+
+struct CacheEntry {
+  int32_t ga, gb, pad0, pad1;
+  double pos[3], imp[3], dual[3];
+};
+
+// Per-world step results that are not rows.
+struct WorldStep {
+  int32_t n_rows, n_limits, n_contacts, backend;
+  int32_t iterations, restarts, converged, cr_breakdown;
+  int64_t cr_iterations;
+  double r_p, r_d, r_c;
+  double f_inf, kkt, bil_vel;
+  int32_t jcache_valid, ccache_count, fail, pad;
+};
+
+// Everything a kernel needs, passed by value (device pointers).
+struct BatchView {
+  int32_t n_worlds;
+  int32_t hist_cap;
+  const DevModel* models;
+  const DevBody* bodies;
+  const DevJoint* joints;
+  const DevGeom* geoms;
+  const DevPair* pairs;
+  const DevWorld* worlds;
+  const uint8_t* active;
+  double* poses;
+  double* twists;
+  double* time;
+  WorldStep* wstep;
+  // rows
+  RowJ* rowj;
+  int32_t* rbody;   // 2 per row
+  int32_t* rkind;
+  int32_t* lkey;    // 2 per row (joint, bound) for limit rows
+  double* rmu;
+  double* bias;
+  double* reg;
+  double* scale;
+  double* vf;       // P (J u_free - v*)
+  double* x0;
+  double* z0;
+  double* lam;      // solver y (preconditioned)
+  double* zo;       // solver z (preconditioned)
+  double* imp;      // physical impulses P y
+  int32_t* csr_ptr; // per world nb+1 entries at body_off + world
+  int32_t* csr;     // per world 2*row_cap entries at 2*row_off: row*2 + side
+  // bodies
+  BodyS* bs;
+  // contacts + caches
+  Contact* contacts;
+  CacheEntry* ccache;
+  double* jc_lam;
+  double* jc_z;
+  double* ls_lam;
+  double* ls_z;
+  int32_t* ls_valid;
+  double* lslab;    // dense-global factor storage
+  double* hist;     // [n_worlds][hist_cap]
+  int32_t* error_count;
+};
+
+struct StepParams {
+  double dt, eta, rho, eps;
+  double beta, contact_margin, impact_thr, bias_clamp, lim_margin_ang, lim_margin_lin;
+  int32_t max_iters, acceleration, restart, fixed_mode;
+  int32_t cr_iters, warm_start, moreau, backend;  // backend: KD_BACKEND_*
+};
+
+}  // namespace kd

@@ -1,0 +1,341 @@
+"""Python mirror of the reference loopdyn API over the B200 C-ABI.
+
+Names and semantics follow /root/reference/proj/include/loopdyn:
+`build_model` (model.hpp:117), `WorldBatch` (batch.hpp:14-54: add_world,
+extract_state, insert_state, set_active, active, converged, diagnostics,
+pose_offset, twist_offset, pose_storage, twist_storage), `batch_step`
+(batch.hpp:58), `initial_state` (stepper.hpp:58) and `joint_coordinate`
+(model.hpp:130).  Every call goes through libkamino_b200.so (include/kamino_b200.h);
+there is no CPU fallback: if the library or a GPU is missing, calls raise.
+
+Worlds are added on the host and the device batch is materialised on first
+use (the device needs every world's capacity to lay out HBM once).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _capi
+from .scene import ModelError, SceneDescription, StepConfig
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkamino_b200.so")
+_lib = None
+
+
+class KaminoError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def lib():
+    """The sm_100a shared library.  Raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                               f"g.build()'` (no CPU fallback exists)")
+        _lib = _capi.bind(C.CDLL(LIB_PATH), "kd_", _capi.KD_ONLY)
+    return _lib
+
+
+def _check(code):
+    if code != 0:
+        msg = lib().kd_last_error().decode()
+        if code in _capi.MODEL_ERROR_CODES:
+            raise ModelError(_capi.MODEL_ERROR_CODES[code], msg)
+        raise KaminoError(code, msg)
+
+
+# ------------------------------------------------------------------ model
+class Model:
+    """MechanismModel (model.hpp:97-113), built and validated by kd_model_build."""
+
+    def __init__(self, scene: SceneDescription):
+        desc, keep = scene.to_ctypes()
+        h = C.c_void_p()
+        _check(lib().kd_model_build(C.byref(desc), C.byref(h)))
+        self.handle = h
+        self.scene = scene
+        self.name = scene.name
+        info = _capi.kd_model_info()
+        lib().kd_model_get_info(h, C.byref(info))
+        self.info = info
+        self.body_names = [b.name for b in scene.bodies]
+        self.joint_names = [j.name for j in scene.joints]
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _lib is not None:
+            _lib.kd_model_destroy(h)
+            self.handle = None
+
+    n_bodies = property(lambda self: self.info.n_bodies)
+    n_bilateral_rows = property(lambda self: self.info.n_bilateral_rows)
+    n_dynamics_rows = property(lambda self: self.info.n_dynamics_rows)
+    n_loops = property(lambda self: self.info.n_loops)
+
+    def velocity_dim(self):
+        return 6 * self.n_bodies
+
+    def joint_layout(self):
+        nj = self.info.n_joints
+        arrs = [np.zeros(max(1, nj), np.int32) for _ in range(4)]
+        _check(lib().kd_model_joint_layout(self.handle, *[_capi.i32ptr(a) for a in arrs]))
+        return [a[:nj] for a in arrs]
+
+    def joint_targets(self):
+        t = np.zeros(max(1, self.info.n_joints))
+        _check(lib().kd_model_joint_targets(self.handle, _capi.dptr(t)))
+        return t[: self.info.n_joints]
+
+    def joint_coordinate(self, joint: int, poses7) -> float:
+        p = np.ascontiguousarray(poses7, dtype=np.float64).reshape(-1)
+        out = C.c_double()
+        _check(lib().kd_joint_coordinate(self.handle, int(joint), _capi.dptr(p), C.byref(out)))
+        return out.value
+
+    def initial_state(self) -> "WorldState":
+        """initial_state (stepper.cpp:97-106)."""
+        poses = np.array([list(b.position) + list(_normalized(b.orientation)) for b in self.scene.bodies],
+                         dtype=np.float64).reshape(-1, 7)
+        twists = np.array([list(b.linear_velocity) + list(b.angular_velocity) for b in self.scene.bodies],
+                          dtype=np.float64).reshape(-1, 6)
+        return WorldState(poses, twists, 0.0)
+
+
+def _normalized(q):
+    n = float(np.sqrt(q[1] * q[1] + q[2] * q[2] + q[3] * q[3] + q[0] * q[0]))
+    return [q[0] / n, q[1] / n, q[2] / n, q[3] / n]
+
+
+def build_model(scene: SceneDescription) -> Model:
+    return Model(scene)
+
+
+@dataclass
+class WorldState:
+    """Body poses [x y z qw qx qy qz] and twists [v; w] of one world
+    (stepper.hpp:49-56; the warm-start caches stay on the device)."""
+    poses: np.ndarray
+    twists: np.ndarray
+    time: float = 0.0
+
+
+# ------------------------------------------------------------------ batch
+class WorldBatch:
+    """Device-resident heterogeneous world batch (batch.hpp:14-54)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self._models: List[Model] = []
+        self._world_model: List[int] = []
+        self._init: List[Optional[WorldState]] = []
+        self.handle = None
+        self._hist_cap = 0
+
+    # -- building
+    def add_world(self, model: Model, state: Optional[WorldState] = None) -> int:
+        if self.handle is not None:
+            raise RuntimeError("add_world after the batch was materialised on the device")
+        idx = next((i for i, m in enumerate(self._models) if m is model), None)
+        if idx is None:
+            self._models.append(model)
+            idx = len(self._models) - 1
+        self._world_model.append(idx)
+        self._init.append(state)
+        return len(self._world_model) - 1
+
+    def _ensure(self):
+        if self.handle is not None:
+            return
+        wm = np.ascontiguousarray(self._world_model, dtype=np.int32)
+        hs = (C.c_void_p * max(1, len(self._models)))(*[m.handle.value for m in self._models])
+        h = C.c_void_p()
+        _check(lib().kd_batch_create(self.device, hs, len(self._models), _capi.i32ptr(wm), len(wm), C.byref(h)))
+        self.handle = h
+        nw, pl, tl = C.c_int32(), C.c_int64(), C.c_int64()
+        lib().kd_batch_size(h, C.byref(nw), C.byref(pl), C.byref(tl))
+        self.n_worlds, self.pose_len, self.twist_len = nw.value, pl.value, tl.value
+        self._pose_off = np.zeros(max(1, self.n_worlds), np.int32)
+        self._twist_off = np.zeros(max(1, self.n_worlds), np.int32)
+        lib().kd_batch_offsets(h, _capi.i32ptr(self._pose_off), _capi.i32ptr(self._twist_off))
+        self.row_offset = np.zeros(max(1, self.n_worlds), np.int64)
+        tot = C.c_int64()
+        lib().kd_batch_row_offsets(h, _capi.i64ptr(self.row_offset), C.byref(tot))
+        self.total_rows = tot.value
+        if any(s is not None for s in self._init):
+            p, t, tm = self.get_state()
+            for w, s in enumerate(self._init):
+                if s is not None:
+                    nb = self._models[self._world_model[w]].n_bodies
+                    p[self._pose_off[w]: self._pose_off[w] + 7 * nb] = np.asarray(s.poses).reshape(-1)
+                    t[self._twist_off[w]: self._twist_off[w] + 6 * nb] = np.asarray(s.twists).reshape(-1)
+                    tm[w] = s.time
+            self.set_state(p, t, tm)
+        self._active = np.ones(max(1, self.n_worlds), np.uint8)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _lib is not None:
+            _lib.kd_batch_destroy(h)
+            self.handle = None
+
+    # -- reference accessors
+    def size(self):
+        return len(self._world_model)
+
+    def model(self, w) -> Model:
+        return self._models[self._world_model[w]]
+
+    def pose_offset(self, w):
+        self._ensure()
+        return int(self._pose_off[w])
+
+    def twist_offset(self, w):
+        self._ensure()
+        return int(self._twist_off[w])
+
+    def pose_storage(self):
+        return self.get_state()[0]
+
+    def twist_storage(self):
+        return self.get_state()[1]
+
+    def extract_state(self, w) -> WorldState:
+        p, t, tm = self.get_state()
+        nb = self.model(w).n_bodies
+        po, to = self._pose_off[w], self._twist_off[w]
+        return WorldState(p[po: po + 7 * nb].reshape(nb, 7).copy(), t[to: to + 6 * nb].reshape(nb, 6).copy(),
+                          float(tm[w]))
+
+    def insert_state(self, w, s: WorldState):
+        p, t, tm = self.get_state()
+        nb = self.model(w).n_bodies
+        po, to = self._pose_off[w], self._twist_off[w]
+        p[po: po + 7 * nb] = np.asarray(s.poses).reshape(-1)
+        t[to: to + 6 * nb] = np.asarray(s.twists).reshape(-1)
+        tm[w] = s.time
+        self.set_state(p, t, tm)
+
+    def set_active(self, w, active: bool):
+        self._ensure()
+        self._active[w] = 1 if active else 0
+        _check(lib().kd_batch_set_active(self.handle, self._active.ctypes.data_as(_capi.c_uint8_p)))
+
+    def active(self, w):
+        self._ensure()
+        return bool(self._active[w])
+
+    def converged(self, w):
+        return bool(self.diagnostics()[w].converged)
+
+    # -- bulk state
+    def get_state(self):
+        self._ensure()
+        p = np.zeros(max(1, self.pose_len))
+        t = np.zeros(max(1, self.twist_len))
+        tm = np.zeros(max(1, self.n_worlds))
+        _check(lib().kd_batch_get_state(self.handle, _capi.dptr(p), _capi.dptr(t), _capi.dptr(tm)))
+        return p[: self.pose_len], t[: self.twist_len], tm[: self.n_worlds]
+
+    def set_state(self, poses=None, twists=None, time=None):
+        self._ensure()
+        f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+        p, t, tm = f(poses), f(twists), f(time)
+        _check(lib().kd_batch_set_state(self.handle, _capi.dptr(p), _capi.dptr(t), _capi.dptr(tm)))
+
+    def reset_caches(self):
+        self._ensure()
+        _check(lib().kd_batch_reset_caches(self.handle))
+
+    # -- stepping
+    def step(self, cfg: StepConfig, n_steps: int = 1):
+        self._ensure()
+        c = cfg.to_ctypes()
+        _check(lib().kd_batch_step(self.handle, C.byref(c), int(n_steps)))
+
+    def diagnostics(self):
+        self._ensure()
+        d = (_capi.kd_step_diag * max(1, self.n_worlds))()
+        _check(lib().kd_batch_get_diagnostics(self.handle, d))
+        return d
+
+    def impulses(self):
+        self._ensure()
+        out = np.zeros(max(1, self.total_rows))
+        _check(lib().kd_batch_get_impulses(self.handle, _capi.dptr(out)))
+        return out
+
+    def set_history_capacity(self, cap):
+        self._ensure()
+        _check(lib().kd_batch_set_history_capacity(self.handle, int(cap)))
+        self._hist_cap = int(cap)
+
+    def history(self):
+        out = np.zeros(max(1, self.n_worlds * self._hist_cap))
+        _check(lib().kd_batch_get_history(self.handle, _capi.dptr(out)))
+        return out[: self.n_worlds * self._hist_cap].reshape(self.n_worlds, self._hist_cap)
+
+    def enable_timing(self, on=True):
+        self._ensure()
+        _check(lib().kd_batch_enable_timing(self.handle, int(on)))
+
+    def timing(self):
+        ms = np.zeros(4)
+        n = C.c_int64()
+        _check(lib().kd_batch_get_timing(self.handle, _capi.dptr(ms), C.byref(n)))
+        return {"assemble_ms": ms[0], "dense_ms": ms[1], "matrix_free_ms": ms[2], "recover_ms": ms[3],
+                "launches": n.value}
+
+    # -- one-step introspection (parity)
+    def dump_rows(self, w, cap=8192):
+        rows = (_capi.kd_row_dump * cap)()
+        n = C.c_int32()
+        _check(lib().kd_batch_dump_rows(self.handle, int(w), rows, cap, C.byref(n)))
+        return _rows_to_numpy(rows, n.value)
+
+    def dump_contacts(self, w, cap=8192):
+        g = np.zeros(2 * cap, np.int32)
+        d = np.zeros(9 * cap)
+        n = C.c_int32()
+        _check(lib().kd_batch_dump_contacts(self.handle, int(w), _capi.i32ptr(g), _capi.dptr(d), cap, C.byref(n)))
+        return g[: 2 * n.value].reshape(-1, 2), d[: 9 * n.value].reshape(-1, 9)
+
+    def dump_limits(self, w, cap=8192):
+        k = np.zeros(2 * cap, np.int32)
+        n = C.c_int32()
+        _check(lib().kd_batch_dump_limits(self.handle, int(w), _capi.i32ptr(k), cap, C.byref(n)))
+        return k[: 2 * n.value].reshape(-1, 2)
+
+
+def _rows_to_numpy(rows, n):
+    out = {
+        "body": np.array([[rows[i].body_a, rows[i].body_b] for i in range(n)], np.int32).reshape(n, 2),
+        "kind": np.array([rows[i].kind for i in range(n)], np.int32),
+        "J": np.array([list(rows[i].block_a) + list(rows[i].block_b) for i in range(n)]).reshape(n, 12),
+    }
+    for key, attr in (("bias", "bias"), ("reg", "reg"), ("scale", "scale"), ("vf", "vf_scaled"),
+                      ("lambda", "lambda_"), ("z", "z")):
+        out[key] = np.array([getattr(rows[i], attr) for i in range(n)])
+    return out
+
+
+def batch_step(batch: WorldBatch, config: StepConfig, n_threads: int = 0):
+    """batch_step (batch.hpp:58); `n_threads` is accepted for signature parity
+    and ignored (the device runs every active world)."""
+    batch.step(config, 1)
+
+
+def bench_jitter(twists, n_bodies_per_world, seed=1, sigma=1e-3):
+    """main.cpp:199-211 jitter stream (std::mt19937_64 + normal_distribution,
+    libstdc++), applied in place to the batch twist storage."""
+    t = np.ascontiguousarray(twists, dtype=np.float64)
+    nb = np.ascontiguousarray(n_bodies_per_world, dtype=np.int32)
+    _check(lib().kd_bench_jitter(C.c_uint64(seed), sigma, len(nb), _capi.i32ptr(nb), _capi.dptr(t)))
+    return t
