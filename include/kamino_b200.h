@@ -203,6 +203,16 @@ int kd_batch_set_active(kd_batch* batch, const uint8_t* active);
 /* batch_step (batch.hpp:58, batch.cpp:74-110) applied n_steps times on the
  * device stream; returns after the work is enqueued AND completed. */
 int kd_batch_step(kd_batch* batch, const kd_step_config* cfg, int32_t n_steps);
+/* Asynchronous variant: enqueue n_steps on the batch's CUDA stream and return
+ * without synchronising; kd_batch_sync waits and reports device-side errors
+ * (SPD failure / capacity overflow).  kd_batch_stream exposes the stream
+ * (a cudaStream_t) so callers can record CUDA events around the work. */
+int kd_batch_step_async(kd_batch* batch, const kd_step_config* cfg, int32_t n_steps);
+int kd_batch_sync(kd_batch* batch);
+int kd_batch_stream(kd_batch* batch, void** stream);
+/* Async state copies with caller-provided (pinned) host buffers, on the batch stream. */
+int kd_batch_set_state_async(kd_batch* batch, const double* poses, const double* twists);
+int kd_batch_get_state_async(kd_batch* batch, double* poses, double* twists);
 /* diagnostics(w)/converged(w) (batch.hpp:27-29) of the last step, per world. */
 int kd_batch_get_diagnostics(kd_batch* batch, kd_step_diag* per_world);
 /* StepDiagnostics::impulses (stepper.hpp:68) of the last step: world w's rows
@@ -246,6 +256,11 @@ int kd_bench_jitter(uint64_t seed, double sigma, int32_t n_worlds, const int32_t
  * ms[0]=assemble, ms[1]=dense solve, ms[2]=matrix-free solve, ms[3]=recover. */
 int kd_batch_enable_timing(kd_batch* batch, int32_t enable);
 int kd_batch_get_timing(kd_batch* batch, double* ms4, int64_t* launches);
+
+/* Diagnostics: clock64() cycles of the fused dense kernel's phases for the last
+ * step, out[w*8 + k]: 0 Gram assembly, 1 scaling, 2 Cholesky, 3 L^{-1},
+ * 4 PADMM loop (worlds on another backend report zeros). */
+int kd_batch_get_phase_cycles(kd_batch* batch, int64_t* out);
 
 const char* kd_last_error(void);
 const char* kd_version(void);

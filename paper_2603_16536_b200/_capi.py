@@ -210,6 +210,13 @@ KD_ONLY = {
     "batch_enable_timing": (C.c_int, [_H, C.c_int32]),
     "batch_get_timing": (C.c_int, [_H, c_double_p, c_int64_p]),
     "version": (C.c_char_p, []),
+    "batch_get_phase_cycles": (C.c_int, [_H, c_int64_p]),
+    "batch_step_async": (C.c_int, [_H, C.POINTER(kd_step_config), C.c_int32]),
+    "batch_sync": (C.c_int, [_H]),
+    "batch_stream": (C.c_int, [_H, C.POINTER(C.c_void_p)]),
+    "batch_set_state_async": (C.c_int, [_H, c_double_p, c_double_p]),
+    "batch_get_state_async": (C.c_int, [_H, c_double_p, c_double_p]),
+    "abi_sizes": (C.c_int, [c_int32_p, C.c_int32]),
 }
 
 

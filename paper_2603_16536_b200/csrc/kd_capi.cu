@@ -64,8 +64,8 @@ struct Bin {
 };
 
 // dense shared-memory classes: (row capacity, threads per CTA)
-constexpr int kClasses[4][2] = {{32, 64}, {64, 64}, {128, 128}, {236, 512}};
-constexpr int kSmemMaxRows = 236;
+constexpr int kClasses[4][2] = {{32, 64}, {64, 64}, {128, 128}, {232, 384}};
+constexpr int kSmemMaxRows = 232;
 constexpr int kDenseGlobalMaxRows = KD_DENSE_ROW_CROSSOVER;
 
 }  // namespace
@@ -309,7 +309,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     b->dense_bins.push_back(bin);
   }
   b->global_bin.cap = kDenseGlobalMaxRows;
-  b->global_bin.nt = 512;
+  b->global_bin.nt = 384;
   for (Bin* bin : {&b->cr_auto_bin, &b->cr_all_bin}) bin->nt = bin->cap > 256 ? 512 : (bin->cap > 128 ? 256 : 128);
   if (cr_smem_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) > 232448)
     return fail(KD_ERR_CAPACITY, "matrix-free path: world too large for one CTA's shared memory");
@@ -506,10 +506,7 @@ int kd_batch_get_timing(kd_batch* b, double* ms4, int64_t* launches) {
   return KD_OK;
 }
 
-int kd_batch_step(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
-  if (!b || !c) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
-  if (b->n_worlds == 0 || n_steps <= 0) return KD_OK;
-  KD_CK(cudaSetDevice(b->device));
+static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
   StepParams sp{};
   sp.dt = c->dt;
   sp.eta = c->eta;
@@ -529,7 +526,6 @@ int kd_batch_step(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
   sp.warm_start = c->warm_start;
   sp.moreau = c->integrator == KD_INTEGRATOR_MOREAU_JEAN;
   sp.backend = c->backend;
-  KD_CK(cudaMemsetAsync(b->d_err, 0, 16, b->stream));
   const BatchView& v = b->view;
   cudaStream_t s = b->stream;
   auto mark = [&](int i) {
@@ -547,34 +543,36 @@ int kd_batch_step(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
         ++b->launches;
       }
       if (b->global_bin.count) {
-        KD_CK(launch_dense(v, sp, b->global_bin.d_worlds, b->global_bin.count, b->global_bin.cap, 512, true, s));
+        KD_CK(launch_dense(v, sp, b->global_bin.d_worlds, b->global_bin.count, b->global_bin.cap, 384, true, s));
         ++b->launches;
       }
     }
     mark(2);
-    const Bin& cr = c->backend == KD_BACKEND_MATRIX_FREE ? b->cr_all_bin
-                    : c->backend == KD_BACKEND_AUTO      ? b->cr_auto_bin
-                                                         : b->global_bin /* unused */;
+    const Bin& cr = c->backend == KD_BACKEND_MATRIX_FREE ? b->cr_all_bin : b->cr_auto_bin;
     if (c->backend != KD_BACKEND_DENSE && cr.count) {
       KD_CK(launch_cr(v, sp, cr.d_worlds, cr.count, cr.cap, cr.nbcap, cr.nt, s));
       ++b->launches;
     }
     mark(3);
     launch_recover(v, sp, s);
+    KD_CK(cudaGetLastError());
     ++b->launches;
     mark(4);
-    KD_CK(cudaGetLastError());
-    if (b->timing) {
+    if (b->timing) {  // per-family device time, CUDA events on the batch stream
       KD_CK(cudaEventSynchronize(b->ev[4]));
-      float t;
       for (int i = 0; i < 4; ++i) {
+        float t = 0.f;
         cudaEventElapsedTime(&t, b->ev[i], b->ev[i + 1]);
-        // ev: 0 assemble 1 dense 2 cr 3 recover 4
-        const int slot = i == 0 ? 0 : (i == 1 ? 1 : (i == 2 ? 2 : 3));
-        b->ms[slot] += t;
+        b->ms[i] += t;
       }
     }
   }
+  return KD_OK;
+}
+
+int kd_batch_sync(kd_batch* b) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
   KD_CK(cudaStreamSynchronize(b->stream));
   int32_t err[4];
   KD_CK(cudaMemcpy(err, b->d_err, 16, cudaMemcpyDeviceToHost));
@@ -582,6 +580,47 @@ int kd_batch_step(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
                                                   std::to_string(err[0]) + " worlds)");
   if (err[1]) return fail(KD_ERR_CAPACITY, "contact or dense-slab capacity exceeded in " + std::to_string(err[1]) +
                                                " worlds");
+  return KD_OK;
+}
+
+int kd_batch_step_async(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
+  if (!b || !c) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (b->n_worlds == 0 || n_steps <= 0) return KD_OK;
+  KD_CK(cudaSetDevice(b->device));
+  return enqueue_steps(b, c, n_steps);
+}
+
+int kd_batch_step(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
+  if (!b || !c) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (b->n_worlds == 0 || n_steps <= 0) return KD_OK;
+  KD_CK(cudaSetDevice(b->device));
+  KD_CK(cudaMemsetAsync(b->d_err, 0, 16, b->stream));
+  const int rc = enqueue_steps(b, c, n_steps);
+  if (rc != KD_OK) return rc;
+  return kd_batch_sync(b);
+}
+
+int kd_batch_stream(kd_batch* b, void** stream) {
+  if (!b || !stream) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  *stream = (void*)b->stream;
+  return KD_OK;
+}
+
+int kd_batch_set_state_async(kd_batch* b, const double* poses, const double* twists) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  if (poses && b->pose_len)
+    KD_CK(cudaMemcpyAsync(b->view.poses, poses, 8 * b->pose_len, cudaMemcpyHostToDevice, b->stream));
+  if (twists && b->twist_len)
+    KD_CK(cudaMemcpyAsync(b->view.twists, twists, 8 * b->twist_len, cudaMemcpyHostToDevice, b->stream));
+  return KD_OK;
+}
+
+int kd_batch_get_state_async(kd_batch* b, double* poses, double* twists) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  if (poses && b->pose_len)
+    KD_CK(cudaMemcpyAsync(poses, b->view.poses, 8 * b->pose_len, cudaMemcpyDeviceToHost, b->stream));
+  if (twists && b->twist_len)
+    KD_CK(cudaMemcpyAsync(twists, b->view.twists, 8 * b->twist_len, cudaMemcpyDeviceToHost, b->stream));
   return KD_OK;
 }
 
@@ -612,6 +651,17 @@ int kd_batch_get_diagnostics(kd_batch* b, kd_step_diag* out) {
     o.kkt_momentum_inf = s.kkt;
     o.bilateral_velocity_inf = s.bil_vel;
   }
+  return KD_OK;
+}
+
+int kd_batch_get_phase_cycles(kd_batch* b, int64_t* out) {
+  if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  KD_CK(cudaSetDevice(b->device));
+  std::vector<WorldStep> ws(b->n_worlds);
+  if (b->n_worlds)
+    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+  for (int w = 0; w < b->n_worlds; ++w)
+    for (int k = 0; k < 8; ++k) out[8 * w + k] = ws[w].backend == BE_DENSE_SMEM ? ws[w].phase_cycles[k] : 0;
   return KD_OK;
 }
 

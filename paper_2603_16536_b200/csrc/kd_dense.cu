@@ -65,41 +65,56 @@ __device__ __forceinline__ void block_max3(double& a, double& b, double& c, doub
 
 // ---------------------------------------------------------------- Cholesky pieces
 // Factor the packed diagonal tile in place and overwrite it with L_kk^{-1}.
-// One warp; lane r owns row r of the tile.
+// One warp; lane r owns row r of the tile.  Pivots use one rsqrt each
+// (L_cc = d * rsqrt(d), L_rc = a_rc * rsqrt(d)), and the reciprocal of every
+// pivot is kept so the inverse needs no divisions.
 __device__ void diag_factor_invert(double* T, int rk, int lane, int* fail) {
   double a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = (lane < rk && c <= lane) ? T[tri(lane) + c] : (c == lane ? 1.0 : 0.0);
   bool bad = false;
+  double my_rinv = 1.0;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const double dcc = __shfl_sync(FULL, a[c], c);
     if (!(dcc > 0.0)) bad = true;
-    const double piv = sqrt(dcc);
-    if (lane > c) a[c] = a[c] / piv;
-    if (lane == c) a[c] = piv;
+    const double rinv = rsqrt(dcc);
+    const double lc = lane > c ? a[c] * rinv : (lane == c ? dcc * rinv : a[c]);
+    if (lane == c) my_rinv = rinv;
+    a[c] = lc;
 #pragma unroll
-    for (int j = c + 1; j < 32; ++j) {
-      const double ljc = __shfl_sync(FULL, a[c], j);
-      if (j <= lane) a[j] -= a[c] * ljc;
+    for (int j = 1; j < 32; ++j) {
+      if (j > c) {
+        const double ljc = __shfl_sync(FULL, lc, j);
+        if (j <= lane) a[j] -= lc * ljc;
+      }
     }
   }
   if (bad && lane == 0) *fail = 1;
-  // stash L_kk (rows < rk) to shared/global, then invert column-wise
+  // stash L_kk (rows < rk), then invert column-wise: lane c owns column c of
+  // X = L^{-1}: X_rc = (d_rc - sum_{k<r} L_rk X_kc) / L_rr
 #pragma unroll
   for (int c = 0; c < 32; ++c)
     if (lane < rk && c <= lane) T[tri(lane) + c] = a[c];
   __syncwarp();
-  // lane c computes column c of X = L^{-1}: X_rc = (d_rc - sum_{k<r} L_rk X_kc) / L_rr
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = 0.0;
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
+    const double rr = __shfl_sync(FULL, my_rinv, r);
     if (r < rk) {
-      double s = (lane == r) ? 1.0 : 0.0;
+      double s0 = (lane == r) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      const double* row = T + tri(r);
 #pragma unroll
-      for (int k = 0; k < r; ++k) s -= T[tri(r) + k] * a[k];
-      a[r] = (lane <= r) ? s / T[tri(r) + r] : 0.0;
+      for (int k = 0; k + 3 < r; k += 4) {
+        s0 -= row[k] * a[k];
+        s1 -= row[k + 1] * a[k + 1];
+        s2 -= row[k + 2] * a[k + 2];
+        s3 -= row[k + 3] * a[k + 3];
+      }
+#pragma unroll
+      for (int k = r & ~3; k < r; ++k) s0 -= row[k] * a[k];
+      a[r] = (lane <= r) ? ((s0 + s1) + (s2 + s3)) * rr : 0.0;
     }
   }
   __syncwarp();
@@ -182,56 +197,220 @@ __device__ __forceinline__ void syrk_tile(double* L, int i, int j, int k, int n,
   }
 }
 
-// Solve L L^T x = b in place on b (shared memory), diag tiles hold L_kk^{-1}.
+// ---------------------------------------------------------------- L^{-1}
+// 4x8 register blocks over a 32x32 tile: lane owns rows 4*(lane>>2)+t, cols 8*(lane&3)+v.
+// X_kj = Linv_kk * B_kj (in place; B_kj rows rk, full 32 columns)
+__device__ __forceinline__ void trmm_left(double* L, int k, int j, int n, int lane) {
+  const int rk = tile_rows(k, n);
+  const double* Li = L + diag_tile(k, n);
+  double* C = L + off_tile(k, j, n);
+  const int rg = lane >> 2, cg = lane & 3;
+  double acc[4][8];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[t][v] = 0.0;
+#pragma unroll 4
+  for (int q = 0; q < 32; ++q) {
+    if (q >= rk) break;
+    double li[4], cq[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int r = 4 * rg + t;
+      li[t] = (q <= r && r < rk) ? Li[tri(r) + q] : 0.0;
+    }
+    const int f = swz(q);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) cq[v] = C[q * 32 + ((8 * cg + v) ^ f)];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[t][v] += li[t] * cq[v];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int r = 4 * rg + t;
+    if (r >= rk) continue;
+    const int f = swz(r);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) C[r * 32 + ((8 * cg + v) ^ f)] = acc[t][v];
+  }
+  __syncwarp();
+}
+
+// B_ik = -L_ik * Linv_kk (in place; tile (i, k), k < i, Linv_kk full 32x32)
+__device__ __forceinline__ void trmm_right_neg(double* L, int i, int k, int n, int lane) {
+  const int ri = tile_rows(i, n);
+  const double* Li = L + diag_tile(k, n);
+  double* C = L + off_tile(i, k, n);
+  const int rg = lane >> 2, cg = lane & 3;
+  double acc[4][8];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[t][v] = 0.0;
+  int rowi[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) rowi[t] = min(4 * rg + t, ri - 1);
+#pragma unroll 4
+  for (int q = 0; q < 32; ++q) {
+    double cr[4], lq[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cr[t] = C[rowi[t] * 32 + (q ^ swz(rowi[t]))];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int c = 8 * cg + v;
+      lq[v] = c <= q ? Li[tri(q) + c] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[t][v] += cr[t] * lq[v];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int r = 4 * rg + t;
+    if (r >= ri) continue;
+    const int f = swz(r);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) C[r * 32 + ((8 * cg + v) ^ f)] = -acc[t][v];
+  }
+  __syncwarp();
+}
+
+// C_ij -= A_ik * X_kj  (all off-diagonal; k < T-1 so A and X have 32 columns)
+__device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, int lane) {
+  const int ri = tile_rows(i, n);
+  const double* A = L + off_tile(i, k, n);
+  const double* X = L + off_tile(k, j, n);
+  double* C = L + off_tile(i, j, n);
+  const int rg = lane >> 2, cg = lane & 3;
+  double acc[4][8];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[t][v] = 0.0;
+  int rowi[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) rowi[t] = min(4 * rg + t, ri - 1);
+#pragma unroll 4
+  for (int q = 0; q < 32; ++q) {
+    double a[4], x[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) a[t] = A[rowi[t] * 32 + (q ^ swz(rowi[t]))];
+    const int f = swz(q);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) x[v] = X[q * 32 + ((8 * cg + v) ^ f)];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[t][v] += a[t] * x[v];
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int r = 4 * rg + t;
+    if (r >= ri) continue;
+    const int f = swz(r);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) C[r * 32 + ((8 * cg + v) ^ f)] -= acc[t][v];
+  }
+}
+
+// Overwrite the Cholesky factor (diag tiles already inverted) with X = L^{-1}
+// by right-looking block forward substitution on L X = I.
 template <int NT>
-__device__ void chol_solve(const double* L, double* b, int n, int T) {
+__device__ void tri_inverse(double* L, int n, int T) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = 1; k < T; ++k) {
+    // the column-(k-1) contributions B_i,k-1 = -L_i,k-1 Linv_k-1 (phase 3 of step k-1)
+    // and B_ij -= L_i,k-1 X_k-1,j (phase 2) are applied below, in order.
+    const int kk = k - 1;
+    // phase 1 (step kk): X_kk,j = Linv_kk B_kk,j for j < kk
+    for (int u = wid; u < kk; u += NW) trmm_left(L, kk, u, n, lane);
+    __syncthreads();
+    // phase 2 (step kk): B_ij -= L_i,kk X_kk,j for i > kk, j < kk
+    const int below = T - kk - 1;
+    for (int u = wid; u < below * kk; u += NW) gemm_sub(L, kk + 1 + u / kk, u % kk, kk, n, lane);
+    __syncthreads();
+    // phase 3 (step kk): B_i,kk = -L_i,kk Linv_kk for i > kk
+    for (int u = wid; u < below; u += NW) trmm_right_neg(L, kk + 1 + u, kk, n, lane);
+    __syncthreads();
+  }
+  // final step T-1: X_T-1,j = Linv B for j < T-1
+  for (int u = wid; u < T - 1; u += NW) trmm_left(L, T - 1, u, n, lane);
+  __syncthreads();
+}
+
+// x = X^T X b with X = L^{-1} (so x = D^{-1} b).  Warp i owns tile row i for
+// w = X b (lane = row, a dot product over the whole tile row) and tile column
+// i for x = X^T w (lane = column): no cross-warp reduction, two barriers.
+template <int NT>
+__device__ void inv_solve(const double* X, double* b, double* w, int n, int T) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __syncthreads();
-  // forward: L y = b
-  for (int k = 0; k < T; ++k) {
-    const int rk = tile_rows(k, n);
-    if (wid == 0) {
-      const double* Li = L + diag_tile(k, n);
-      double s = 0.0;
-      if (lane < rk) {
-        const double* row = Li + tri(lane);
-        for (int c = 0; c <= lane; ++c) s += row[c] * b[32 * k + c];
+  for (int i = wid; i < T; i += NT / 32) {
+    const int ri = tile_rows(i, n);
+    const int r = lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (r < ri) {
+      const int f = swz(r);
+      for (int j = 0; j < i; ++j) {
+        const double* row = X + off_tile(i, j, n) + r * 32;
+        const double* bj = b + 32 * j;
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          a0 += row[c ^ f] * bj[c];
+          a1 += row[(c + 1) ^ f] * bj[c + 1];
+          a2 += row[(c + 2) ^ f] * bj[c + 2];
+          a3 += row[(c + 3) ^ f] * bj[c + 3];
+        }
       }
-      __syncwarp();
-      if (lane < rk) b[32 * k + lane] = s;
+      const double* drow = X + diag_tile(i, n) + tri(r);
+      const double* bi = b + 32 * i;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        if (c <= r) a0 += drow[c] * bi[c];
+        if (c + 1 <= r) a1 += drow[c + 1] * bi[c + 1];
+      }
+      w[32 * i + r] = (a0 + a1) + (a2 + a3);
     }
-    __syncthreads();
-    for (int i = 32 * (k + 1) + tid; i < n; i += NT) {
-      const int ti = i >> 5, r = i & 31, f = swz(r);
-      const double* row = L + off_tile(ti, k, n) + r * 32;
-      double s = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < 32; ++c) s += row[c ^ f] * b[32 * k + c];
-      b[i] -= s;
-    }
-    __syncthreads();
   }
-  // backward: L^T x = y
-  for (int k = T - 1; k >= 0; --k) {
-    const int rk = tile_rows(k, n);
-    if (wid == 0) {
-      const double* Li = L + diag_tile(k, n);
-      double s = 0.0;
-      if (lane < rk)
-        for (int r = lane; r < rk; ++r) s += Li[tri(r) + lane] * b[32 * k + r];
-      __syncwarp();
-      if (lane < rk) b[32 * k + lane] = s;
+  __syncthreads();
+  for (int j = wid; j < T; j += NT / 32) {
+    const int c = lane;
+    const int rj = tile_rows(j, n);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (c < rj) {
+      const double* D = X + diag_tile(j, n);
+      const double* wj = w + 32 * j;
+#pragma unroll
+      for (int r = 0; r < 32; r += 2) {
+        if (r >= c && r < rj) a0 += D[tri(r) + c] * wj[r];
+        if (r + 1 >= c && r + 1 < rj) a1 += D[tri(r + 1) + c] * wj[r + 1];
+      }
+      for (int i = j + 1; i < T; ++i) {
+        const int ri = tile_rows(i, n);
+        const double* A = X + off_tile(i, j, n);
+        const double* wi = w + 32 * i;
+        if (ri == 32) {
+#pragma unroll
+          for (int r = 0; r < 32; r += 4) {
+            a0 += A[r * 32 + (c ^ swz(r))] * wi[r];
+            a1 += A[(r + 1) * 32 + (c ^ swz(r + 1))] * wi[r + 1];
+            a2 += A[(r + 2) * 32 + (c ^ swz(r + 2))] * wi[r + 2];
+            a3 += A[(r + 3) * 32 + (c ^ swz(r + 3))] * wi[r + 3];
+          }
+        } else {
+          for (int r = 0; r < ri; ++r) a0 += A[r * 32 + (c ^ swz(r))] * wi[r];
+        }
+      }
+      b[32 * j + c] = (a0 + a1) + (a2 + a3);
     }
-    __syncthreads();
-    for (int j = tid; j < 32 * k; j += NT) {
-      const int tj = j >> 5, c = j & 31;
-      const double* A = L + off_tile(k, tj, n);
-      double s = 0.0;
-      for (int r = 0; r < rk; ++r) s += A[r * 32 + (c ^ swz(r))] * b[32 * k + r];
-      b[j] -= s;
-    }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 // SOC projection of one contact triple (padmm.cpp:19-37)
@@ -274,7 +453,8 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   double* L = GLOBAL_L ? bv.lslab + W.lslab_off : smem;
   double* xv = smem + (GLOBAL_L ? 0 : ((nlen + 1) & ~1));
   double* P = xv + npad;
-  double* red = P + npad;          // 3 * NW
+  double* wv_s = P + npad;         // intermediate w = L^{-1} b
+  double* red = wv_s + npad;       // 3 * NW
   int* rbs = reinterpret_cast<int*>(red + 3 * NW + 1);  // 2n body ids
   __shared__ int fail;
   const int64_t R0 = W.row_off;
@@ -283,6 +463,14 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   const double* regg = bv.reg + R0;
   const double eta_rho = sp.eta + sp.rho;
 
+  long long t_prev = clock64();
+  auto stamp = [&](int k) {
+    if (tid == 0) {
+      const long long t = clock64();
+      ws.phase_cycles[k] = t - t_prev;
+      t_prev = t;
+    }
+  };
   if (tid == 0) fail = 0;
   for (int r = tid; r < n; r += NT) {
     P[r] = bv.scale[R0 + r];
@@ -356,56 +544,69 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
       __syncthreads();
     }
   }
+  stamp(0);
   // diagonal += R; P D P; += (eta + rho) I   (delassus.cpp:96-100)
-  for (int e = tid; e < nlen; e += NT) {
-    // decode (i, j) of storage slot e
-    int ti = 0;
-    while (ti + 1 < T && tile_row_base(ti + 1) <= e) ++ti;
-    const int base = tile_row_base(ti), rows = tile_rows(ti, n);
-    const int off = e - base;
-    int i, j;
-    if (off < ti * 32 * rows) {
-      const int tj = off / (32 * rows);
-      const int o2 = off - tj * 32 * rows;
-      const int r = o2 >> 5, cs = o2 & 31;
-      i = 32 * ti + r;
-      j = 32 * tj + (cs ^ swz(r));
-    } else {
-      const int o2 = off - ti * 32 * rows;
-      int r = (int)((sqrt(8.0 * o2 + 1.0) - 1.0) * 0.5);
-      while (tri(r + 1) <= o2) ++r;
-      while (tri(r) > o2) --r;
-      i = 32 * ti + r;
-      j = 32 * ti + (o2 - tri(r));
+  {
+    const int ntiles = T * (T + 1) / 2;
+    for (int u = wid; u < ntiles; u += NW) {
+      int ti = 0;
+      while ((ti + 1) * (ti + 2) / 2 <= u) ++ti;
+      const int tj = u - ti * (ti + 1) / 2;
+      const int rows = tile_rows(ti, n);
+      if (ti == tj) {
+        double* D = L + diag_tile(ti, n);
+        for (int e = lane; e < tri(rows); e += 32) {
+          int r = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+          while (tri(r + 1) <= e) ++r;
+          while (tri(r) > e) --r;
+          const int i = 32 * ti + r, j = 32 * ti + (e - tri(r));
+          double d = D[e];
+          if (i == j) d += regg[i];
+          d = (P[i] * d) * P[j];
+          if (i == j) d += eta_rho;
+          D[e] = d;
+        }
+      } else {
+        double* A = L + off_tile(ti, tj, n);
+        const double pj = P[32 * tj + lane];
+        for (int r = 0; r < rows; ++r) {
+          const int o = r * 32 + (lane ^ swz(r));
+          A[o] = (P[32 * ti + r] * A[o]) * pj;
+        }
+      }
     }
-    double d = L[e];
-    if (i == j) d += regg[i];
-    d = (P[i] * d) * P[j];
-    if (i == j) d += eta_rho;
-    L[e] = d;
   }
   __syncthreads();
-
-  // ---- 2. blocked right-looking Cholesky; diagonal tiles become L_kk^{-1}
+  stamp(1);
+  // ---- 2. blocked right-looking Cholesky with look-ahead; diagonal tiles
+  // become L_kk^{-1}.  While warps 1.. run the trailing update of step k,
+  // warp 0 updates and factors diagonal tile k+1 (the critical path).
+  if (wid == 0) diag_factor_invert(L + diag_tile(0, n), tile_rows(0, n), lane, &fail);
+  __syncthreads();
   for (int k = 0; k < T; ++k) {
-    if (wid == 0) diag_factor_invert(L + diag_tile(k, n), tile_rows(k, n), lane, &fail);
-    __syncthreads();
     const double* Linv = L + diag_tile(k, n);
     for (int i = 32 * (k + 1) + tid; i < n; i += NT) {
       const int ti = i >> 5, r = i & 31;
       panel_row(L + off_tile(ti, k, n) + r * 32, r, Linv);
     }
     __syncthreads();
-    const int m = T - k - 1;
-    const int units = m * (m + 1) / 2;
-    for (int u = wid; u < units; u += NW) {
-      // decode u -> (i, j) with k < j <= i
-      int ii = 0;
-      while ((ii + 1) * (ii + 2) / 2 <= u) ++ii;
-      const int jj = u - ii * (ii + 1) / 2;
-      syrk_tile(L, k + 1 + ii, k + 1 + jj, k, n, lane);
+    if (k + 1 < T) {
+      const int m = T - k - 1;
+      const int units = m * (m + 1) / 2;
+      if (wid == 0) {
+        syrk_tile(L, k + 1, k + 1, k, n, lane);
+        __syncwarp();
+        diag_factor_invert(L + diag_tile(k + 1, n), tile_rows(k + 1, n), lane, &fail);
+      } else {
+        for (int u = wid; u < units; u += NW - 1) {  // unit 0, tile (k+1, k+1), is warp 0's
+          int ii = 0;
+          while ((ii + 1) * (ii + 2) / 2 <= u) ++ii;
+          const int jj = u - ii * (ii + 1) / 2;
+          syrk_tile(L, k + 1 + ii, k + 1 + jj, k, n, lane);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (fail) {
     if (tid == 0) {
@@ -413,6 +614,10 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
       atomicAdd(bv.error_count, 1);
     }
   }
+  stamp(2);
+  // ---- 2b. X = L^{-1}: every PADMM solve becomes two parallel mat-vecs
+  tri_inverse<NT>(L, n, T);
+  stamp(3);
 
   // ---- 3. PADMM (padmm.cpp:87-159), one cone unit per thread
   const int n_jd = ws.n_rows - ws.n_limits - 3 * ws.n_contacts;
@@ -421,12 +626,13 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   const bool has_unit = tid < n_units;
   const int row0 = tid < first_contact ? tid : first_contact + 3 * (tid - first_contact);
   const int kind = !has_unit ? ROW_BILATERAL : (tid < n_jd ? ROW_BILATERAL : (tid < first_contact ? ROW_LIMIT : ROW_CONTACT));
-  const int nr = kind == ROW_CONTACT ? 3 : 1;
+  const int nr = !has_unit ? 0 : (kind == ROW_CONTACT ? 3 : 1);
   const double mu = has_unit ? bv.rmu[R0 + row0] : 0.0;
   const double eta = sp.eta, rho = sp.rho;
   double v[3] = {0, 0, 0}, x[3] = {0, 0, 0}, y[3] = {0, 0, 0}, z[3] = {0, 0, 0}, yh[3], zh[3];
-  if (has_unit) {
-    for (int d = 0; d < nr; ++d) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (d < nr) {
       v[d] = bv.vf[R0 + row0 + d];
       x[d] = bv.x0[R0 + row0 + d];
       z[d] = bv.z0[R0 + row0 + d];
@@ -436,6 +642,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   if (kind == ROW_CONTACT) project_soc(x, mu, y);
   else if (kind == ROW_LIMIT) y[0] = fmax(0.0, x[0]);
   else y[0] = x[0];
+#pragma unroll
   for (int d = 0; d < 3; ++d) {
     yh[d] = y[d];
     zh[d] = z[d];
@@ -447,42 +654,42 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   const int hcap = bv.hist_cap;
   // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
   auto write_rhs = [&]() {
-    if (!has_unit) return;
-    double s0 = 0.0;
-    if (kind == ROW_CONTACT) s0 = mu * hypot(zh[1], zh[2]);  // desaxce_shift (padmm.cpp:44-52)
-    for (int d = 0; d < nr; ++d) {
-      const double s = d == 0 ? s0 : 0.0;
-      xv[row0 + d] = -((((v[d] + s) - eta * x[d]) - rho * yh[d]) - zh[d]);
-    }
+    const double s0 = kind == ROW_CONTACT ? mu * hypot(zh[1], zh[2]) : 0.0;  // desaxce_shift (padmm.cpp:44-52)
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (d < nr) xv[row0 + d] = -((((v[d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * yh[d]) - zh[d]);
   };
   write_rhs();
   for (it = 1; it <= sp.max_iters; ++it) {
-    chol_solve<NT>(L, xv, n, T);
+    inv_solve<NT>(L, xv, wv_s, n, T);
     double rp = 0.0, dmax = 0.0, rc = 0.0;
-    double yp[3], zp[3];
-    if (has_unit) {
-      double wv[3], yn[3], zn[3];
-      for (int d = 0; d < nr; ++d) {
-        x[d] = xv[row0 + d];
-        wv[d] = x[d] - zh[d] / rho;
-      }
-      if (kind == ROW_CONTACT) project_soc(wv, mu, yn);
-      else if (kind == ROW_LIMIT) yn[0] = fmax(0.0, wv[0]);
-      else yn[0] = wv[0];
-      double ymax = 0.0, zmax = 0.0;
-      for (int d = 0; d < nr; ++d) {
-        zn[d] = zh[d] - rho * (x[d] - yn[d]);
+    double yp[3], zp[3], wv[3], yn[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (d < nr) x[d] = xv[row0 + d];
+      wv[d] = x[d] - zh[d] / rho;
+      yp[d] = y[d];
+      zp[d] = z[d];
+    }
+    if (kind == ROW_CONTACT) project_soc(wv, mu, yn);
+    else {
+      yn[0] = kind == ROW_LIMIT ? fmax(0.0, wv[0]) : wv[0];
+      yn[1] = yn[2] = 0.0;
+    }
+    double ymax = 0.0, zmax = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (d < nr) {
+        const double zn = zh[d] - rho * (x[d] - yn[d]);
         rp = fmax(rp, fabs(x[d] - yn[d]));
         dmax = fmax(dmax, fabs(yn[d] - y[d]));
         ymax = fmax(ymax, fabs(yn[d]));
-        zmax = fmax(zmax, fabs(zn[d]));
-        yp[d] = y[d];
-        zp[d] = z[d];
+        zmax = fmax(zmax, fabs(zn));
         y[d] = yn[d];
-        z[d] = zn[d];
+        z[d] = zn;
       }
-      if (kind != ROW_BILATERAL) rc = fmin(ymax, zmax);
     }
+    if (kind != ROW_BILATERAL) rc = fmin(ymax, zmax);
     block_max3<NT>(rp, dmax, rc, red);
     r_p = rp;
     r_d = rho * dmax;
@@ -497,6 +704,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
       const bool restart = sp.restart && combined > prev;
       if (restart) {
         a = 1.0;
+#pragma unroll
         for (int d = 0; d < 3; ++d) {
           yh[d] = y[d];
           zh[d] = z[d];
@@ -505,13 +713,15 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
       } else {
         const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));
         const double beta = (a - 1.0) / an;
-        for (int d = 0; d < nr; ++d) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
           yh[d] = y[d] + beta * (y[d] - yp[d]);
           zh[d] = z[d] + beta * (z[d] - zp[d]);
         }
         a = an;
       }
     } else {
+#pragma unroll
       for (int d = 0; d < 3; ++d) {
         yh[d] = y[d];
         zh[d] = z[d];
@@ -520,15 +730,18 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     prev = combined;
     write_rhs();
   }
+  stamp(4);
   // outputs (padmm.cpp:147-157)
-  if (has_unit) {
-    for (int d = 0; d < nr; ++d) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (d < nr) {
       bv.lam[R0 + row0 + d] = y[d];
       bv.zo[R0 + row0 + d] = z[d];
     }
   }
   if (tid == 0) {
-    ws.iterations = min(it, sp.max_iters);
+    const int done = min(it, sp.max_iters);
+    ws.iterations = done;
     ws.r_p = r_p;
     ws.r_d = r_d;
     ws.r_c = r_c;
@@ -536,7 +749,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     ws.converged = (converged || fmax(r_p, fmax(r_d, r_c)) < sp.eps) ? 1 : 0;
     ws.cr_iterations = 0;
     ws.cr_breakdown = 0;
-    for (int i = it; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
+    for (int i = done; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
   }
 }
 
@@ -544,7 +757,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
 size_t dense_smem_bytes(int n, int nt, bool global_l) {
   const int T = (n + 31) / 32;
   const size_t nlen = global_l ? 0 : (size_t)((n * (n + 1) / 2 + 1) & ~1);
-  return 8 * (nlen + 2 * (size_t)(32 * T) + 3 * (nt / 32) + 1) + 4 * 2 * (size_t)(32 * T) + 64;
+  return 8 * (nlen + 3 * (size_t)(32 * T) + 3 * (nt / 32) + 1) + 4 * 2 * (size_t)(32 * T) + 64;
 }
 
 template <int NT, bool G>
@@ -564,12 +777,12 @@ static cudaError_t launch_t(const BatchView& bv, const StepParams& sp, const int
 cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int cap, int nt,
                          bool global_l, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  if (global_l) return launch_t<512, true>(bv, sp, worlds, count, cap, s);
+  if (global_l) return launch_t<384, true>(bv, sp, worlds, count, cap, s);
   switch (nt) {
     case 64: return launch_t<64, false>(bv, sp, worlds, count, cap, s);
     case 128: return launch_t<128, false>(bv, sp, worlds, count, cap, s);
     case 256: return launch_t<256, false>(bv, sp, worlds, count, cap, s);
-    default: return launch_t<512, false>(bv, sp, worlds, count, cap, s);
+    default: return launch_t<384, false>(bv, sp, worlds, count, cap, s);
   }
 }
 

@@ -122,6 +122,7 @@ struct WorldStep {
   double r_p, r_d, r_c;
   double f_inf, kkt, bil_vel;
   int32_t jcache_valid, ccache_count, fail, pad;
+  int64_t phase_cycles[8];  // fused-kernel phase stamps (clock64 deltas), diagnostics only
 };
 
 // Everything a kernel needs, passed by value (device pointers).

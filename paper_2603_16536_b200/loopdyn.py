@@ -260,6 +260,29 @@ class WorldBatch:
         c = cfg.to_ctypes()
         _check(lib().kd_batch_step(self.handle, C.byref(c), int(n_steps)))
 
+    def step_async(self, cfg: StepConfig, n_steps: int = 1):
+        """Enqueue n_steps on the batch stream without waiting (see sync())."""
+        self._ensure()
+        c = cfg.to_ctypes()
+        _check(lib().kd_batch_step_async(self.handle, C.byref(c), int(n_steps)))
+
+    def sync(self):
+        _check(lib().kd_batch_sync(self.handle))
+
+    def stream(self) -> int:
+        """The batch's cudaStream_t as an integer (for torch.cuda.ExternalStream)."""
+        self._ensure()
+        s = C.c_void_p()
+        _check(lib().kd_batch_stream(self.handle, C.byref(s)))
+        return s.value or 0
+
+    def set_state_async(self, poses, twists):
+        """Host->device state copy on the batch stream (pass pinned buffers)."""
+        _check(lib().kd_batch_set_state_async(self.handle, _capi.dptr(poses), _capi.dptr(twists)))
+
+    def get_state_async(self, poses, twists):
+        _check(lib().kd_batch_get_state_async(self.handle, _capi.dptr(poses), _capi.dptr(twists)))
+
     def diagnostics(self):
         self._ensure()
         d = (_capi.kd_step_diag * max(1, self.n_worlds))()
@@ -292,6 +315,13 @@ class WorldBatch:
         _check(lib().kd_batch_get_timing(self.handle, _capi.dptr(ms), C.byref(n)))
         return {"assemble_ms": ms[0], "dense_ms": ms[1], "matrix_free_ms": ms[2], "recover_ms": ms[3],
                 "launches": n.value}
+
+    def phase_cycles(self):
+        """clock64 cycles per fused-kernel phase of the last step, [n_worlds, 8]."""
+        self._ensure()
+        out = np.zeros(8 * max(1, self.n_worlds), np.int64)
+        _check(lib().kd_batch_get_phase_cycles(self.handle, _capi.i64ptr(out)))
+        return out[: 8 * self.n_worlds].reshape(self.n_worlds, 8)
 
     # -- one-step introspection (parity)
     def dump_rows(self, w, cap=8192):
