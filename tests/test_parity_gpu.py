@@ -1,0 +1,221 @@
+"""Device path vs CPU oracle (GPU box only).
+
+Parity protocol: (i) the oracle passes the reference KATs
+(test_oracle.py); (ii) one-step parity: same input state -> row count, row
+kinds, body ids, limit keys and contact (geom_a, geom_b) order bit-exact; J,
+bias, R, P, v_f within 1e-12 relative, solver lambda/z within 1e-9 relative;
+(iii) N-step trajectories and PADMM iteration counts; (iv) residual histories
+in fixed-iteration mode.  Tolerances: the device uses FMA contraction and a
+blocked factorization, the oracle neither, so agreement is ulp-level per step
+and grows only as the dynamics amplify it.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib
+import paper_2603_16536_b200 as K
+from paper_2603_16536_b200.scenes import closed_chain, dr_legs, sphere_pile
+
+pytestmark = pytest.mark.gpu
+
+BUNDLED = ["fourbar", "double_fourbar", "serial_chain_10", "pendulum", "sphere_on_plane", "inclined_box", "freefall"]
+
+
+def scene(name):
+    if name == "dr_legs":
+        return dr_legs()
+    if name == "closed_chain":
+        return closed_chain(16)
+    if name == "sphere_pile":
+        return sphere_pile(40)
+    return oracle_lib.bundled_scene(name)
+
+
+def pair(sc, n_worlds=1, jitter=False, threads=8):
+    m, om = K.build_model(sc), oracle_lib.OracleModel(sc)
+    gb = K.WorldBatch()
+    for _ in range(n_worlds):
+        gb.add_world(m)
+    ob = oracle_lib.OracleBatch([om], [0] * n_worlds, n_threads=threads)
+    if jitter:
+        p, t, tm = ob.get_state()
+        t = K.bench_jitter(t, [m.n_bodies] * n_worlds, seed=1)
+        ob.set_state(p, t, tm)
+        gb.set_state(p, t, tm)
+    return gb, ob
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(1.0, float(np.abs(b).max()))) if len(b) else 0.0
+
+
+@pytest.mark.parametrize("name", BUNDLED + ["dr_legs", "closed_chain", "sphere_pile"])
+def test_one_step_rows_match_oracle(name):
+    sc = scene(name)
+    cfg = K.config_for(sc)
+    gb, ob = pair(sc, jitter=name == "dr_legs")
+    ob.set_trace(True)
+    for _ in range(3):  # a few steps so warm-start caches are exercised too
+        gb.step(cfg)
+        ob.step(cfg)
+        rg, ro = gb.dump_rows(0), ob.dump_rows(0)
+        assert len(rg["kind"]) == len(ro["kind"])
+        assert (rg["body"] == ro["body"]).all()
+        assert (rg["kind"] == ro["kind"]).all()
+        for key in ("J", "bias", "reg", "scale", "vf"):
+            assert rel(rg[key], ro[key]) < 1e-12, key
+        for key in ("lambda", "z"):
+            assert rel(rg[key], ro[key]) < 1e-9, key
+        cg, cdg = gb.dump_contacts(0)
+        co, cdo = ob.dump_contacts(0)
+        assert (cg == co).all()
+        if len(cdo):
+            assert np.abs(cdg - cdo).max() < 1e-12
+        assert (gb.dump_limits(0) == ob.dump_limits(0)).all()
+        dg, do = gb.diagnostics()[0], ob.diagnostics()[0]
+        assert (dg.n_rows, dg.contact_count, dg.n_limits, dg.first_contact_row) == \
+               (do.n_rows, do.contact_count, do.n_limits, do.first_contact_row)
+        assert dg.iterations == do.iterations
+        assert dg.converged == do.converged
+
+
+@pytest.mark.parametrize("name,steps", [("fourbar", 2400), ("double_fourbar", 480), ("serial_chain_10", 480),
+                                        ("pendulum", 480), ("sphere_on_plane", 480), ("inclined_box", 480),
+                                        ("freefall", 240)])
+def test_trajectory_parity(name, steps):
+    sc = scene(name)
+    cfg = K.config_for(sc)
+    gb, ob = pair(sc)
+    iters_g = iters_o = 0
+    for k in range(steps):
+        gb.step(cfg)
+        ob.step(cfg)
+        dg, do = gb.diagnostics()[0], ob.diagnostics()[0]
+        assert dg.n_rows == do.n_rows and dg.contact_count == do.contact_count
+        iters_g += dg.iterations
+        iters_o += do.iterations
+    pg, tg, tmg = gb.get_state()
+    po, to, tmo = ob.get_state()
+    assert np.abs(pg - po).max() < 1e-9
+    assert np.abs(tg - to).max() < 1e-8
+    assert np.abs(tmg - tmo).max() < 1e-12
+    assert iters_g == iters_o
+
+
+def test_dr_legs_trajectory_parity():
+    sc = dr_legs()
+    cfg = K.config_for(sc)
+    gb, ob = pair(sc, n_worlds=8, jitter=True)
+    same_iters = total = 0
+    for k in range(100):
+        gb.step(cfg)
+        ob.step(cfg)
+        dg, do = gb.diagnostics(), ob.diagnostics()
+        for w in range(8):
+            assert dg[w].n_rows == do[w].n_rows
+            assert dg[w].contact_count == do[w].contact_count
+            assert dg[w].n_limits == do[w].n_limits
+            same_iters += dg[w].iterations == do[w].iterations
+            total += 1
+    assert same_iters >= 0.99 * total
+    pg, tg, _ = gb.get_state()
+    po, to, _ = ob.get_state()
+    assert np.abs(pg - po).max() < 1e-8
+    assert np.abs(tg - to).max() < 1e-6
+
+
+@pytest.mark.parametrize("name", ["serial_chain_10", "dr_legs", "sphere_on_plane"])
+def test_residual_history_parity_fixed_mode(name):
+    sc = scene(name)
+    cfg = K.config_for(sc)
+    cfg.fixed_iteration_mode = True
+    cfg.max_iters = 17
+    gb, ob = pair(sc, jitter=name == "dr_legs")
+    gb.set_history_capacity(32)
+    ob.set_trace(True)
+    for _ in range(3):
+        gb.step(cfg)
+        ob.step(cfg)
+        hg, ho = gb.history()[0], ob.history(32)[0]
+        assert gb.diagnostics()[0].iterations == 17 == ob.diagnostics()[0].iterations
+        assert (hg[17:] == -1).all() and (ho[17:] == -1).all()
+        assert np.all(np.abs(hg[:17] - ho[:17]) <= 1e-9 * np.maximum(1e-3, np.abs(ho[:17])) + 1e-13)
+
+
+@pytest.mark.parametrize("cr_iters", [9, 50])
+def test_matrix_free_fourbar_parity(cr_iters):
+    sc = scene("fourbar")
+    cfg = K.config_for(sc)
+    cfg.backend = "sparse"
+    cfg.cr_iters = cr_iters
+    gb, ob = pair(sc)
+    same = 0
+    for _ in range(240):
+        gb.step(cfg)
+        ob.step(cfg)
+        dg, do = gb.diagnostics()[0], ob.diagnostics()[0]
+        assert dg.iterations == do.iterations
+        # the CR breakdown guard (r.Ar <= 1e-30 |rhs|^2, delassus.cpp:166-172) can
+        # fire one inner iteration apart once the residual is at rounding level
+        assert abs(dg.cr_iterations - do.cr_iterations) <= 2
+        same += dg.cr_iterations == do.cr_iterations
+    assert same >= 0.95 * 240
+    pg, tg, _ = gb.get_state()
+    po, to, _ = ob.get_state()
+    assert np.abs(pg - po).max() < 1e-9 and np.abs(tg - to).max() < 1e-8
+
+
+def test_closed_chain_cr_path_parity():
+    sc = closed_chain(16)
+    cfg = K.config_for(sc)
+    gb, ob = pair(sc)
+    for _ in range(20):
+        gb.step(cfg)
+        ob.step(cfg)
+        dg, do = gb.diagnostics()[0], ob.diagnostics()[0]
+        assert dg.n_rows == do.n_rows > 300  # Auto -> matrix-free
+        assert dg.cr_iterations > 0
+    pg, tg, _ = gb.get_state()
+    po, to, _ = ob.get_state()
+    assert np.abs(pg - po).max() < 1e-7 and np.abs(tg - to).max() < 1e-5
+
+
+def test_sphere_pile_contact_indexing():
+    sc = sphere_pile(40)
+    cfg = K.config_for(sc)
+    gb, ob = pair(sc)
+    ob.set_trace(True)
+    for _ in range(10):
+        gb.step(cfg)
+        ob.step(cfg)
+        cg, _ = gb.dump_contacts(0)
+        co, _ = ob.dump_contacts(0)
+        assert cg.shape == co.shape and (cg == co).all()
+    pg, _, _ = gb.get_state()
+    po, _, _ = ob.get_state()
+    assert np.abs(pg - po).max() < 1e-9
+
+
+def test_dense_vs_matrix_free_on_device():
+    """Acceptance #2 (acceptance.cpp:114-135) on the device: same state and
+    caches solved both ways, impulses within 1e-6 relative."""
+    sc = scene("fourbar")
+    cfg = K.config_for(sc)
+    m = K.build_model(sc)
+    dense, sparse = K.WorldBatch(), K.WorldBatch()
+    dense.add_world(m)
+    sparse.add_world(m)
+    cd = K.StepConfig(**{**cfg.__dict__, "backend": "dense"})
+    cs = K.StepConfig(**{**cfg.__dict__, "backend": "sparse", "cr_iters": 50})
+    worst = 0.0
+    for _ in range(100):
+        p, t, tm = dense.get_state()
+        sparse.set_state(p, t, tm)
+        sparse.reset_caches()
+        dense.reset_caches()
+        dense.step(cd)
+        sparse.step(cs)
+        a = dense.impulses()[:21]
+        b = sparse.impulses()[:21]
+        worst = max(worst, float(np.abs(a - b).max() / max(1e-9, np.abs(a).max())))
+    assert worst <= 1e-6
