@@ -64,7 +64,7 @@ struct Bin {
 };
 
 // dense shared-memory classes: (row capacity, threads per CTA)
-constexpr int kClasses[4][2] = {{32, 64}, {64, 64}, {128, 128}, {232, 384}};
+constexpr int kClasses[4][2] = {{32, 64}, {64, 64}, {128, 128}, {232, 256}};
 constexpr int kSmemMaxRows = 232;
 constexpr int kDenseGlobalMaxRows = KD_DENSE_ROW_CROSSOVER;
 
@@ -276,7 +276,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     if (rc > kSmemMaxRows) {
       W.slab_cap = std::min(rc, kDenseGlobalMaxRows);
       W.lslab_off = b->total_lslab;
-      b->total_lslab += (int64_t)W.slab_cap * (W.slab_cap + 1) / 2;
+      b->total_lslab += (int64_t)dense_factor_doubles(W.slab_cap) + 2;
       b->global_bin.worlds.push_back(w);
     }
     if (rc > kDenseGlobalMaxRows) {
@@ -309,7 +309,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     b->dense_bins.push_back(bin);
   }
   b->global_bin.cap = kDenseGlobalMaxRows;
-  b->global_bin.nt = 384;
+  b->global_bin.nt = 256;
   for (Bin* bin : {&b->cr_auto_bin, &b->cr_all_bin}) bin->nt = bin->cap > 256 ? 512 : (bin->cap > 128 ? 256 : 128);
   if (cr_smem_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) > 232448)
     return fail(KD_ERR_CAPACITY, "matrix-free path: world too large for one CTA's shared memory");
@@ -543,7 +543,7 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
         ++b->launches;
       }
       if (b->global_bin.count) {
-        KD_CK(launch_dense(v, sp, b->global_bin.d_worlds, b->global_bin.count, b->global_bin.cap, 384, true, s));
+        KD_CK(launch_dense(v, sp, b->global_bin.d_worlds, b->global_bin.count, b->global_bin.cap, 256, true, s));
         ++b->launches;
       }
     }

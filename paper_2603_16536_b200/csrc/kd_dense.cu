@@ -25,17 +25,22 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ __forceinline__ int swz(int r) { return (r & 15) ^ ((r >> 4) << 2); }
+// Off-diagonal tiles are stored row-major with a padded row stride of 33
+// doubles: element (r, c) at r*33 + c.  Since 33 = 1 (mod 16 bank pairs), a
+// column walk (lane = row) and a row walk (lane = column) are both
+// bank-conflict free for 8-byte words, and every address is base + constant
+// (no per-element swizzle arithmetic in the mat-vec loops).
+constexpr int LDT = 33;
 __device__ __forceinline__ int tile_rows(int ti, int n) { return min(32, n - 32 * ti); }
-__device__ __forceinline__ int tile_row_base(int ti) { return 512 * ti * (ti - 1) + 528 * ti; }
-__device__ __forceinline__ int off_tile(int ti, int tj, int n) { return tile_row_base(ti) + tj * 32 * tile_rows(ti, n); }
-__device__ __forceinline__ int diag_tile(int ti, int n) { return tile_row_base(ti) + ti * 32 * tile_rows(ti, n); }
+__device__ __forceinline__ int tile_row_base(int ti) { return 528 * ti * ti; }
+__device__ __forceinline__ int off_tile(int ti, int tj, int n) { return tile_row_base(ti) + tj * LDT * tile_rows(ti, n); }
+__device__ __forceinline__ int diag_tile(int ti, int n) { return tile_row_base(ti) + ti * LDT * tile_rows(ti, n); }
 __device__ __forceinline__ int tri(int r) { return (r * (r + 1)) >> 1; }
 // element (i, j), i >= j
 __device__ __forceinline__ int lidx(int i, int j, int n) {
   const int ti = i >> 5, tj = j >> 5, r = i & 31, c = j & 31;
   if (ti == tj) return diag_tile(ti, n) + tri(r) + c;
-  return off_tile(ti, tj, n) + r * 32 + (c ^ swz(r));
+  return off_tile(ti, tj, n) + r * LDT + c;
 }
 
 // ---------------------------------------------------------------- reductions
@@ -65,10 +70,12 @@ __device__ __forceinline__ void block_max3(double& a, double& b, double& c, doub
 
 // ---------------------------------------------------------------- Cholesky pieces
 // Factor the packed diagonal tile in place and overwrite it with L_kk^{-1}.
-// One warp; lane r owns row r of the tile.  Pivots use one rsqrt each
-// (L_cc = d * rsqrt(d), L_rc = a_rc * rsqrt(d)), and the reciprocal of every
-// pivot is kept so the inverse needs no divisions.
-__device__ void diag_factor_invert(double* T, int rk, int lane, int* fail) {
+// One warp; lane r owns row r in registers (fully unrolled so every register
+// index is static; the kernel calls this from exactly one site to keep a
+// single copy of the code in the instruction cache).  Pivots use one rsqrt
+// each (L_cc = d rsqrt(d), L_rc = a_rc rsqrt(d)); the reciprocals are kept so
+// the inverse is division-free.
+__device__ __noinline__ void diag_factor_invert(double* T, int rk, int lane, int* fail) {
   double a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = (lane < rk && c <= lane) ? T[tri(lane) + c] : (c == lane ? 1.0 : 0.0);
@@ -91,12 +98,11 @@ __device__ void diag_factor_invert(double* T, int rk, int lane, int* fail) {
     }
   }
   if (bad && lane == 0) *fail = 1;
-  // stash L_kk (rows < rk), then invert column-wise: lane c owns column c of
-  // X = L^{-1}: X_rc = (d_rc - sum_{k<r} L_rk X_kc) / L_rr
 #pragma unroll
   for (int c = 0; c < 32; ++c)
     if (lane < rk && c <= lane) T[tri(lane) + c] = a[c];
   __syncwarp();
+  // lane c owns column c of X = L^{-1}: X_rc = (d_rc - sum_{k<r} L_rk X_kc) / L_rr
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = 0.0;
 #pragma unroll
@@ -124,198 +130,147 @@ __device__ void diag_factor_invert(double* T, int rk, int lane, int* fail) {
   __syncwarp();
 }
 
-// Panel: L_ik = A_ik Linv_kk^T for one row of tile (ti, k); in place.
-__device__ __forceinline__ void panel_row(double* row, int r, const double* Linv) {
-  double a[32];
-  const int f = swz(r);
+// ---------------------------------------------------------------- DMMA tile products
+// One warp computes a 32x32 tile product with FP64 tensor-core MMAs
+// (mma.sync m8n8k4 f64: 256 FMA per instruction; tcgen05 has no fp64 kind).
+// Fragment layout: A (8x4 row) lane l -> A[l>>2][l&3]; B (4x8 col) lane l ->
+// B[l&3][l>>2]; C (8x8) lane l -> C[l>>2][2(l&3)+{0,1}].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// element loaders (rows beyond `rows` read as 0)
+struct OffT {  // off-diagonal tile, swizzled
+  const double* p;
+  int rows;
+  __device__ __forceinline__ double operator()(int r, int c) const { return r < rows ? p[r * LDT + c] : 0.0; }
+};
+struct OffTT {  // transpose of an off-diagonal tile
+  const double* p;
+  int rows;
+  __device__ __forceinline__ double operator()(int r, int c) const { return c < rows ? p[c * LDT + r] : 0.0; }
+};
+struct DiagL {  // packed lower diagonal tile
+  const double* p;
+  int rows;
+  __device__ __forceinline__ double operator()(int r, int c) const { return (r < rows && c <= r) ? p[tri(r) + c] : 0.0; }
+};
+struct DiagLT {  // transpose of a packed lower diagonal tile (upper)
+  const double* p;
+  int rows;
+  __device__ __forceinline__ double operator()(int r, int c) const { return (c < rows && r <= c) ? p[tri(c) + r] : 0.0; }
+};
+
+// acc[mb][nb][h] += sum_k A(8mb+l/4, k) B(k, 8nb+2(l%4)+h), k < 32
+template <class LA, class LB>
+__device__ __forceinline__ void mma_tile(double acc[4][4][2], const LA& la, const LB& lb) {
+  const int lane = threadIdx.x & 31, qr = lane >> 2, qc = lane & 3;
+#pragma unroll 2
+  for (int ks = 0; ks < 8; ++ks) {
+    double a[4], b[4];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = row[c ^ f];
+    for (int mb = 0; mb < 4; ++mb) a[mb] = la(8 * mb + qr, 4 * ks + qc);
 #pragma unroll
-  for (int c = 31; c >= 0; --c) {
-    double s = 0.0;
+    for (int nb = 0; nb < 4; ++nb) b[nb] = lb(4 * ks + qc, 8 * nb + qr);
 #pragma unroll
-    for (int q = 0; q <= c; ++q) s += a[q] * Linv[tri(c) + q];
-    a[c] = s;
+    for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) dmma(acc[mb][nb][0], acc[mb][nb][1], a[mb], b[nb]);
   }
+}
+
+__device__ __forceinline__ void zero_acc(double acc[4][4][2]) {
 #pragma unroll
-  for (int c = 0; c < 32; ++c) row[c ^ f] = a[c];
+  for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+}
+
+// C (off-diagonal, rows) = alpha * acc + beta * C
+__device__ __forceinline__ void store_off(double* C, int rows, const double acc[4][4][2], double alpha, bool accumulate) {
+  const int lane = threadIdx.x & 31, qr = lane >> 2, qc = lane & 3;
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb) {
+    const int r = 8 * mb + qr;
+    if (r >= rows) continue;
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int o = r * LDT + 8 * nb + 2 * qc + h;
+        C[o] = accumulate ? C[o] + alpha * acc[mb][nb][h] : alpha * acc[mb][nb][h];
+      }
+  }
+}
+
+// C (packed lower diagonal, rows) -= acc (lower part only)
+__device__ __forceinline__ void sub_diag(double* C, int rows, const double acc[4][4][2]) {
+  const int lane = threadIdx.x & 31, qr = lane >> 2, qc = lane & 3;
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb) {
+    const int r = 8 * mb + qr;
+    if (r >= rows) continue;
+#pragma unroll
+    for (int nb = 0; nb <= mb; ++nb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * nb + 2 * qc + h;
+        if (c <= r) C[tri(r) + c] -= acc[mb][nb][h];
+      }
+  }
 }
 
 // Trailing update of tile (i, j) (k < j <= i): A_ij -= L_ik L_jk^T.
-// Lane owns a 4 x 8 block: rows 4*(lane/4)+t, cols 8*(lane%4)+v.
 __device__ __forceinline__ void syrk_tile(double* L, int i, int j, int k, int n, int lane) {
-  const int ri = tile_rows(i, n), rj = tile_rows(j, n);
-  const double* Pi = L + off_tile(i, k, n);
-  const double* Pj = L + off_tile(j, k, n);
-  const int rg = lane >> 2, cg = lane & 3;
-  double acc[4][8];
-#pragma unroll
-  for (int t = 0; t < 4; ++t)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) acc[t][v] = 0.0;
-  int rowi[4], rowj[8];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) rowi[t] = min(4 * rg + t, ri - 1);
-#pragma unroll
-  for (int v = 0; v < 8; ++v) rowj[v] = min(8 * cg + v, rj - 1);
-#pragma unroll 4
-  for (int q = 0; q < 32; ++q) {
-    double li[4], lj[8];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) li[t] = Pi[rowi[t] * 32 + (q ^ swz(rowi[t]))];
-#pragma unroll
-    for (int v = 0; v < 8; ++v) lj[v] = Pj[rowj[v] * 32 + (q ^ swz(rowj[v]))];
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int v = 0; v < 8; ++v) acc[t][v] += li[t] * lj[v];
-  }
-  if (i == j) {
-    double* D = L + diag_tile(i, n);
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int r = 4 * rg + t;
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int c = 8 * cg + v;
-        if (r < ri && c <= r) D[tri(r) + c] -= acc[t][v];
-      }
-    }
-  } else {
-    double* A = L + off_tile(i, j, n);
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int r = 4 * rg + t;
-      if (r >= ri) continue;
-      const int f = swz(r);
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int c = 8 * cg + v;
-        if (c < rj) A[r * 32 + (c ^ f)] -= acc[t][v];
-      }
-    }
-  }
+  double acc[4][4][2];
+  zero_acc(acc);
+  mma_tile(acc, OffT{L + off_tile(i, k, n), tile_rows(i, n)}, OffTT{L + off_tile(j, k, n), tile_rows(j, n)});
+  if (i == j) sub_diag(L + diag_tile(i, n), tile_rows(i, n), acc);
+  else store_off(L + off_tile(i, j, n), tile_rows(i, n), acc, -1.0, true);
+}
+
+// Panel tile: L_ik = A_ik Linv_kk^T (in place).
+__device__ __forceinline__ void panel_tile(double* L, int i, int k, int n) {
+  double acc[4][4][2];
+  zero_acc(acc);
+  double* A = L + off_tile(i, k, n);
+  const int ri = tile_rows(i, n);
+  mma_tile(acc, OffT{A, ri}, DiagLT{L + diag_tile(k, n), 32});
+  __syncwarp();
+  store_off(A, ri, acc, 1.0, false);
 }
 
 // ---------------------------------------------------------------- L^{-1}
-// 4x8 register blocks over a 32x32 tile: lane owns rows 4*(lane>>2)+t, cols 8*(lane&3)+v.
-// X_kj = Linv_kk * B_kj (in place; B_kj rows rk, full 32 columns)
+// X_kj = Linv_kk * B_kj (in place)
 __device__ __forceinline__ void trmm_left(double* L, int k, int j, int n, int lane) {
+  double acc[4][4][2];
+  zero_acc(acc);
   const int rk = tile_rows(k, n);
-  const double* Li = L + diag_tile(k, n);
   double* C = L + off_tile(k, j, n);
-  const int rg = lane >> 2, cg = lane & 3;
-  double acc[4][8];
-#pragma unroll
-  for (int t = 0; t < 4; ++t)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) acc[t][v] = 0.0;
-#pragma unroll 4
-  for (int q = 0; q < 32; ++q) {
-    if (q >= rk) break;
-    double li[4], cq[8];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int r = 4 * rg + t;
-      li[t] = (q <= r && r < rk) ? Li[tri(r) + q] : 0.0;
-    }
-    const int f = swz(q);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) cq[v] = C[q * 32 + ((8 * cg + v) ^ f)];
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int v = 0; v < 8; ++v) acc[t][v] += li[t] * cq[v];
-  }
+  mma_tile(acc, DiagL{L + diag_tile(k, n), rk}, OffT{C, rk});
   __syncwarp();
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int r = 4 * rg + t;
-    if (r >= rk) continue;
-    const int f = swz(r);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) C[r * 32 + ((8 * cg + v) ^ f)] = acc[t][v];
-  }
-  __syncwarp();
+  store_off(C, rk, acc, 1.0, false);
 }
 
-// B_ik = -L_ik * Linv_kk (in place; tile (i, k), k < i, Linv_kk full 32x32)
+// B_ik = -L_ik * Linv_kk (in place)
 __device__ __forceinline__ void trmm_right_neg(double* L, int i, int k, int n, int lane) {
+  double acc[4][4][2];
+  zero_acc(acc);
   const int ri = tile_rows(i, n);
-  const double* Li = L + diag_tile(k, n);
   double* C = L + off_tile(i, k, n);
-  const int rg = lane >> 2, cg = lane & 3;
-  double acc[4][8];
-#pragma unroll
-  for (int t = 0; t < 4; ++t)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) acc[t][v] = 0.0;
-  int rowi[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) rowi[t] = min(4 * rg + t, ri - 1);
-#pragma unroll 4
-  for (int q = 0; q < 32; ++q) {
-    double cr[4], lq[8];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) cr[t] = C[rowi[t] * 32 + (q ^ swz(rowi[t]))];
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const int c = 8 * cg + v;
-      lq[v] = c <= q ? Li[tri(q) + c] : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int v = 0; v < 8; ++v) acc[t][v] += cr[t] * lq[v];
-  }
+  mma_tile(acc, OffT{C, ri}, DiagL{L + diag_tile(k, n), 32});
   __syncwarp();
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int r = 4 * rg + t;
-    if (r >= ri) continue;
-    const int f = swz(r);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) C[r * 32 + ((8 * cg + v) ^ f)] = -acc[t][v];
-  }
-  __syncwarp();
+  store_off(C, ri, acc, -1.0, false);
 }
 
-// C_ij -= A_ik * X_kj  (all off-diagonal; k < T-1 so A and X have 32 columns)
+// C_ij -= A_ik * X_kj
 __device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, int lane) {
-  const int ri = tile_rows(i, n);
-  const double* A = L + off_tile(i, k, n);
-  const double* X = L + off_tile(k, j, n);
-  double* C = L + off_tile(i, j, n);
-  const int rg = lane >> 2, cg = lane & 3;
-  double acc[4][8];
-#pragma unroll
-  for (int t = 0; t < 4; ++t)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) acc[t][v] = 0.0;
-  int rowi[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) rowi[t] = min(4 * rg + t, ri - 1);
-#pragma unroll 4
-  for (int q = 0; q < 32; ++q) {
-    double a[4], x[8];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) a[t] = A[rowi[t] * 32 + (q ^ swz(rowi[t]))];
-    const int f = swz(q);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) x[v] = X[q * 32 + ((8 * cg + v) ^ f)];
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int v = 0; v < 8; ++v) acc[t][v] += a[t] * x[v];
-  }
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int r = 4 * rg + t;
-    if (r >= ri) continue;
-    const int f = swz(r);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) C[r * 32 + ((8 * cg + v) ^ f)] -= acc[t][v];
-  }
+  double acc[4][4][2];
+  zero_acc(acc);
+  mma_tile(acc, OffT{L + off_tile(i, k, n), tile_rows(i, n)}, OffT{L + off_tile(k, j, n), 32});
+  store_off(L + off_tile(i, j, n), tile_rows(i, n), acc, -1.0, true);
 }
 
 // Overwrite the Cholesky factor (diag tiles already inverted) with X = L^{-1}
@@ -347,64 +302,68 @@ __device__ void tri_inverse(double* L, int n, int T) {
 // x = X^T X b with X = L^{-1} (so x = D^{-1} b).  Warp i owns tile row i for
 // w = X b (lane = row, a dot product over the whole tile row) and tile column
 // i for x = X^T w (lane = column): no cross-warp reduction, two barriers.
+// Padded tiles give both walks constant offsets and no bank conflicts; the
+// broadcast vector operand is read as double2 (one wavefront per two entries).
 template <int NT>
 __device__ void inv_solve(const double* X, double* b, double* w, int n, int T) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __syncthreads();
   for (int i = wid; i < T; i += NT / 32) {
-    const int ri = tile_rows(i, n);
-    const int r = lane;
+    const int ri = tile_rows(i, n), r = lane;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (r < ri) {
-      const int f = swz(r);
       for (int j = 0; j < i; ++j) {
-        const double* row = X + off_tile(i, j, n) + r * 32;
-        const double* bj = b + 32 * j;
+        const double* row = X + off_tile(i, j, n) + r * LDT;
+        const double2* bj = reinterpret_cast<const double2*>(b + 32 * j);
 #pragma unroll
         for (int c = 0; c < 32; c += 4) {
-          a0 += row[c ^ f] * bj[c];
-          a1 += row[(c + 1) ^ f] * bj[c + 1];
-          a2 += row[(c + 2) ^ f] * bj[c + 2];
-          a3 += row[(c + 3) ^ f] * bj[c + 3];
+          const double2 b01 = bj[c / 2], b23 = bj[c / 2 + 1];
+          a0 += row[c] * b01.x;
+          a1 += row[c + 1] * b01.y;
+          a2 += row[c + 2] * b23.x;
+          a3 += row[c + 3] * b23.y;
         }
       }
       const double* drow = X + diag_tile(i, n) + tri(r);
-      const double* bi = b + 32 * i;
+      const double2* bi = reinterpret_cast<const double2*>(b + 32 * i);
 #pragma unroll
       for (int c = 0; c < 32; c += 2) {
-        if (c <= r) a0 += drow[c] * bi[c];
-        if (c + 1 <= r) a1 += drow[c + 1] * bi[c + 1];
+        const double2 bb = bi[c / 2];
+        if (c <= r) a0 += drow[c] * bb.x;
+        if (c + 1 <= r) a1 += drow[c + 1] * bb.y;
       }
       w[32 * i + r] = (a0 + a1) + (a2 + a3);
     }
   }
   __syncthreads();
   for (int j = wid; j < T; j += NT / 32) {
-    const int c = lane;
-    const int rj = tile_rows(j, n);
+    const int c = lane, rj = tile_rows(j, n);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (c < rj) {
       const double* D = X + diag_tile(j, n);
-      const double* wj = w + 32 * j;
+      const double2* wj = reinterpret_cast<const double2*>(w + 32 * j);
 #pragma unroll
       for (int r = 0; r < 32; r += 2) {
-        if (r >= c && r < rj) a0 += D[tri(r) + c] * wj[r];
-        if (r + 1 >= c && r + 1 < rj) a1 += D[tri(r + 1) + c] * wj[r + 1];
+        const double2 ww = wj[r / 2];
+        if (r >= c && r < rj) a0 += D[tri(r) + c] * ww.x;
+        if (r + 1 >= c && r + 1 < rj) a1 += D[tri(r + 1) + c] * ww.y;
       }
       for (int i = j + 1; i < T; ++i) {
         const int ri = tile_rows(i, n);
-        const double* A = X + off_tile(i, j, n);
-        const double* wi = w + 32 * i;
+        const double* A = X + off_tile(i, j, n) + c;
+        const double2* wi = reinterpret_cast<const double2*>(w + 32 * i);
         if (ri == 32) {
 #pragma unroll
           for (int r = 0; r < 32; r += 4) {
-            a0 += A[r * 32 + (c ^ swz(r))] * wi[r];
-            a1 += A[(r + 1) * 32 + (c ^ swz(r + 1))] * wi[r + 1];
-            a2 += A[(r + 2) * 32 + (c ^ swz(r + 2))] * wi[r + 2];
-            a3 += A[(r + 3) * 32 + (c ^ swz(r + 3))] * wi[r + 3];
+            const double2 w01 = wi[r / 2], w23 = wi[r / 2 + 1];
+            a0 += A[r * LDT] * w01.x;
+            a1 += A[(r + 1) * LDT] * w01.y;
+            a2 += A[(r + 2) * LDT] * w23.x;
+            a3 += A[(r + 3) * LDT] * w23.y;
           }
         } else {
-          for (int r = 0; r < ri; ++r) a0 += A[r * 32 + (c ^ swz(r))] * wi[r];
+          const double* wr = w + 32 * i;
+          for (int r = 0; r < ri; ++r) a0 += A[r * LDT] * wr[r];
         }
       }
       b[32 * j + c] = (a0 + a1) + (a2 + a3);
@@ -448,7 +407,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   const DevWorld W = bv.worlds[w];
   const int n = ws.n_rows;
   const int T = (n + 31) >> 5;
-  const int nlen = n * (n + 1) / 2;
+  const int nlen = tile_row_base(T - 1) + (T - 1) * LDT * tile_rows(T - 1, n) + tri(tile_rows(T - 1, n));
   const int npad = 32 * T;
   double* L = GLOBAL_L ? bv.lslab + W.lslab_off : smem;
   double* xv = smem + (GLOBAL_L ? 0 : ((nlen + 1) & ~1));
@@ -570,7 +529,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
         double* A = L + off_tile(ti, tj, n);
         const double pj = P[32 * tj + lane];
         for (int r = 0; r < rows; ++r) {
-          const int o = r * 32 + (lane ^ swz(r));
+          const int o = r * LDT + lane;
           A[o] = (P[32 * ti + r] * A[o]) * pj;
         }
       }
@@ -581,22 +540,25 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   // ---- 2. blocked right-looking Cholesky with look-ahead; diagonal tiles
   // become L_kk^{-1}.  While warps 1.. run the trailing update of step k,
   // warp 0 updates and factors diagonal tile k+1 (the critical path).
-  if (wid == 0) diag_factor_invert(L + diag_tile(0, n), tile_rows(0, n), lane, &fail);
-  __syncthreads();
-  for (int k = 0; k < T; ++k) {
-    const double* Linv = L + diag_tile(k, n);
-    for (int i = 32 * (k + 1) + tid; i < n; i += NT) {
-      const int ti = i >> 5, r = i & 31;
-      panel_row(L + off_tile(ti, k, n) + r * 32, r, Linv);
+  long long c_panel = 0, c_syrk = 0, c_diag = 0;
+  for (int k = -1; k < T; ++k) {
+    long long q0 = clock64();
+    if (k >= 0) {
+      for (int i = k + 1 + wid; i < T; i += NW) panel_tile(L, i, k, n);
+      __syncthreads();
     }
-    __syncthreads();
+    long long q1 = clock64();
+    c_panel += q1 - q0;
     if (k + 1 < T) {
       const int m = T - k - 1;
-      const int units = m * (m + 1) / 2;
+      const int units = k >= 0 ? m * (m + 1) / 2 : 0;
       if (wid == 0) {
-        syrk_tile(L, k + 1, k + 1, k, n, lane);
-        __syncwarp();
+        if (k >= 0) {
+          syrk_tile(L, k + 1, k + 1, k, n, lane);
+          __syncwarp();
+        }
         diag_factor_invert(L + diag_tile(k + 1, n), tile_rows(k + 1, n), lane, &fail);
+        c_diag += clock64() - q1;
       } else {
         for (int u = wid; u < units; u += NW - 1) {  // unit 0, tile (k+1, k+1), is warp 0's
           int ii = 0;
@@ -606,7 +568,13 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
         }
       }
       __syncthreads();
+      c_syrk += clock64() - q1;
     }
+  }
+  if (tid == 0) {
+    ws.phase_cycles[5] = c_panel;
+    ws.phase_cycles[6] = c_syrk;
+    ws.phase_cycles[7] = c_diag;
   }
   if (fail) {
     if (tid == 0) {
@@ -754,10 +722,19 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
 }
 
 // Shared-memory bytes the dense kernel needs for n rows with NT threads.
+size_t dense_factor_doubles(int n) {
+  const int T = (n + 31) / 32;
+  const int rl = n - 32 * (T - 1);
+  return (size_t)528 * (T - 1) * (T - 1) + (size_t)(T - 1) * 33 * rl + (size_t)rl * (rl + 1) / 2;
+}
+
 size_t dense_smem_bytes(int n, int nt, bool global_l) {
   const int T = (n + 31) / 32;
-  const size_t nlen = global_l ? 0 : (size_t)((n * (n + 1) / 2 + 1) & ~1);
-  return 8 * (nlen + 3 * (size_t)(32 * T) + 3 * (nt / 32) + 1) + 4 * 2 * (size_t)(32 * T) + 64;
+  const int rl = n - 32 * (T - 1);
+  const size_t nl = (size_t)528 * (T - 1) * (T - 1) + (size_t)(T - 1) * 33 * rl + (size_t)rl * (rl + 1) / 2;
+  const size_t nlen = global_l ? 0 : ((nl + 1) & ~(size_t)1);
+  const size_t npad = 32 * (size_t)T;
+  return 8 * (nlen + 3 * npad + 3 * (nt / 32) + 1) + 4 * 2 * npad + 64;
 }
 
 template <int NT, bool G>
@@ -777,12 +754,12 @@ static cudaError_t launch_t(const BatchView& bv, const StepParams& sp, const int
 cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int cap, int nt,
                          bool global_l, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  if (global_l) return launch_t<384, true>(bv, sp, worlds, count, cap, s);
+  if (global_l) return launch_t<256, true>(bv, sp, worlds, count, cap, s);
   switch (nt) {
     case 64: return launch_t<64, false>(bv, sp, worlds, count, cap, s);
     case 128: return launch_t<128, false>(bv, sp, worlds, count, cap, s);
     case 256: return launch_t<256, false>(bv, sp, worlds, count, cap, s);
-    default: return launch_t<384, false>(bv, sp, worlds, count, cap, s);
+    default: return launch_t<256, false>(bv, sp, worlds, count, cap, s);
   }
 }
 

@@ -36,6 +36,7 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
                int nt, cudaStream_t s);
 void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s);
 size_t dense_smem_bytes(int n, int nt, bool global_l);
+size_t dense_factor_doubles(int n);
 size_t cr_smem_bytes(int n, int nb, int nt);
 
 }  // namespace kd

@@ -9,6 +9,7 @@ using namespace kd;
 __global__ void bench(double* g, long long* out) {
   extern __shared__ double sm[];
   __shared__ int fail;
+  __shared__ double rinv_s[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // SPD 32x32 packed diag tile: I*40 + small
   for (int e = tid; e < 528 * 8; e += blockDim.x) sm[e] = 0.001 * ((e * 7919) % 13);
@@ -17,11 +18,11 @@ __global__ void bench(double* g, long long* out) {
     for (int r = 0; r < 32; ++r) sm[tri(r) + r] = 40.0;
   __syncthreads();
   long long t0 = clock64();
-  if (wid == 0) diag_factor_invert(sm, 32, lane, &fail);
+  if (wid == 0) diag_factor_invert(sm, 32, lane, &fail, rinv_s);
   __syncthreads();
   long long t1 = clock64();
   // panel rows: 32 rows of an off-diag tile at sm+600 using Linv at sm
-  if (tid < 32) panel_row(sm + 600 + tid * 32, tid, sm);
+  if (wid == 0) panel_tile(sm, 1, 0, 96);
   __syncthreads();
   long long t2 = clock64();
   if (wid == 0) syrk_tile(sm, 1, 1, 0, 96, lane);  // uses tiles of an n=96 layout
@@ -84,7 +85,7 @@ int main() {
     bench<<<1, 384, 200000>>>(g, o);
     long long h[4];
     cudaMemcpy(h, o, 32, cudaMemcpyDeviceToHost);
-    printf("diag_factor_invert %lld  panel(32 rows) %lld  syrk(1 warp) %lld  syrk(12 warps) %lld cycles\n", h[0],
+    printf("diag_factor_invert %lld  panel(tile, DMMA) %lld  syrk(1 warp) %lld  syrk(12 warps) %lld cycles\n", h[0],
            h[1], h[2], h[3]);
   }
   for (int n : {64, 128, 214, 232}) {
