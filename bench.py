@@ -146,18 +146,16 @@ def algorithmic_flops(n, iters):
     return n ** 3 / 3 + np.asarray(iters) * (2 * n * n + 20 * n)
 
 
-def build_world_batch(K, scene, n_local, first_global, seed, device):
+def build_world_batch(K, scene, n_local, rank, seed, device):
+    from paper_2603_16536_b200 import sharding
     m = K.build_model(scene)
     b = K.WorldBatch(device=device)
     for _ in range(n_local):
         b.add_world(m)
-    p, t, tm = b.get_state()
-    # The jitter stream is global and world-major (main.cpp:199-211): draw it
-    # for worlds [0, first_global + n_local) and keep this rank's slice.
-    nbody = m.n_bodies
-    full = np.tile(np.asarray(m.initial_state().twists).reshape(-1), first_global + n_local)
-    full = K.bench_jitter(full, [nbody] * (first_global + n_local), seed=seed)
-    t = full[6 * nbody * first_global:].copy()
+    p, _, tm = b.get_state()
+    # The jitter stream is global and world-major (main.cpp:199-211): rank r
+    # keeps the slice of global worlds [r*W, (r+1)*W).
+    t = sharding.jitter_slice(m.initial_state().twists, m.n_bodies, sharding.world_range(n_local, rank), seed)
     b.set_state(p, t, tm)
     return b, m
 
@@ -224,7 +222,7 @@ def main():
     scene = dr_legs()
     cfg = K.config_for(scene)
     W = args.worlds_per_gpu
-    b, model = build_world_batch(K, scene, W, rank * W, args.seed, local)
+    b, model = build_world_batch(K, scene, W, rank, args.seed, local)
     # settle + warm-up (untimed)
     b.step(cfg, args.settle)
     b.step(cfg, max(3, args.warmup))
@@ -276,8 +274,10 @@ def main():
     peak, peak_kind = measured_peaks()
     achieved = (bytes_k2 / rsteps) / (k2_ms / 1e3) / 1e9
     d = b.diagnostics()
-    iters_mean = float(np.mean([d[w].iterations for w in range(W)]))
     rows_mean = float(np.mean([d[w].n_rows for w in range(W)]))
+    from paper_2603_16536_b200 import sharding
+    run_stats = sharding.reduce_stats(dist, sharding.local_stats(d, W), device=f"cuda:{local}")
+    iters_mean = run_stats["mean_iterations"]
     b.enable_timing(False)
 
     # ---- end-to-end through the C-ABI with host (pinned) state buffers
@@ -339,6 +339,7 @@ def main():
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "run_stats": run_stats,
         }
         print(json.dumps(out), flush=True)
     if dist is not None:

@@ -1,0 +1,58 @@
+"""World sharding across GPUs (one process per GPU) — SURVEY.md §8e.
+
+Worlds are independent, so the data path has no collective: rank r owns a
+contiguous block of global world ids and steps it on its own device.  The
+global world order, and therefore every world's initial state (including the
+reference bench jitter stream, main.cpp:199-211, which is drawn world-major
+over the whole batch), is independent of the GPU count.  The only collective
+is the end-of-run reduction of a few statistics (`reduce_stats`).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def world_range(n_per_rank: int, rank: int) -> range:
+    """Weak scaling: every rank owns `n_per_rank` consecutive global worlds."""
+    return range(rank * n_per_rank, (rank + 1) * n_per_rank)
+
+
+def split_range(n_global: int, rank: int, world_size: int) -> range:
+    """Strong scaling: `n_global` worlds split into near-equal contiguous blocks."""
+    base, extra = divmod(n_global, world_size)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def jitter_slice(initial_twists: np.ndarray, n_bodies: int, worlds: range, seed: int = 1, sigma: float = 1e-3):
+    """Twist storage of global worlds `worlds` after the reference bench jitter:
+    the stream is drawn for worlds [0, worlds.stop) and this block is kept."""
+    from .loopdyn import bench_jitter
+    per = np.asarray(initial_twists, dtype=np.float64).reshape(-1)
+    assert per.size == 6 * n_bodies
+    full = np.tile(per, worlds.stop)
+    full = bench_jitter(full, [n_bodies] * worlds.stop, seed=seed, sigma=sigma)
+    return full[6 * n_bodies * worlds.start:].copy()
+
+
+def local_stats(diags, n_worlds: int) -> dict:
+    """Per-step statistics of one rank's worlds (kd_step_diag array)."""
+    its = [diags[w].iterations for w in range(n_worlds)]
+    return {"worlds": float(n_worlds), "iterations": float(sum(its)),
+            "converged": float(sum(diags[w].converged for w in range(n_worlds))),
+            "max_kkt": max((diags[w].kkt_momentum_inf for w in range(n_worlds)), default=0.0),
+            "max_r": max((max(diags[w].r_p, diags[w].r_d, diags[w].r_c) for w in range(n_worlds)), default=0.0)}
+
+
+def reduce_stats(dist, stats: dict, device="cpu") -> dict:
+    """One all-reduce of the run statistics (sums for counts, max for residuals)."""
+    import torch
+    sums = torch.tensor([stats["worlds"], stats["iterations"], stats["converged"]], dtype=torch.float64,
+                        device=device)
+    maxs = torch.tensor([stats["max_kkt"], stats["max_r"]], dtype=torch.float64, device=device)
+    if dist is not None and dist.is_initialized():
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
+    s, m = sums.tolist(), maxs.tolist()
+    return {"worlds": s[0], "iterations": s[1], "converged": s[2], "max_kkt": m[0], "max_r": m[1],
+            "mean_iterations": s[1] / max(1.0, s[0])}
