@@ -258,8 +258,9 @@ int kd_batch_enable_timing(kd_batch* batch, int32_t enable);
 int kd_batch_get_timing(kd_batch* batch, double* ms4, int64_t* launches);
 
 /* Diagnostics: clock64() cycles of the fused dense kernel's phases for the last
- * step, out[w*8 + k]: 0 Gram assembly, 1 scaling, 2 Cholesky, 3 L^{-1},
- * 4 PADMM loop (worlds on another backend report zeros). */
+ * step, out[w*8 + k]: 0 scaled Gram assembly, 1 unused, 2 Cholesky, 3 L^{-1},
+ * 4 PADMM loop, 5/6/7 Cholesky panel/trailing/diagonal-chain sub-totals
+ * (worlds on another backend report zeros). */
 int kd_batch_get_phase_cycles(kd_batch* batch, int64_t* out);
 
 const char* kd_last_error(void);

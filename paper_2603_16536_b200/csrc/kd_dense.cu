@@ -439,104 +439,83 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   for (int e = tid; e < nlen; e += NT) L[e] = 0.0;
   __syncthreads();
 
-  // ---- 1. D = sum_b Gram_b, ascending body order: phase 0 stores the term of
-  // the smallest shared body, phase 1 adds the term of the larger one.
+  // ---- 1. D = P (J M^-1 J^T + R) P + (eta+rho) I  (assemble_dense, delassus.cpp:67-104)
+  // One warp per body b walks the Gram block of the rows touching b
+  // (ascending row order).  Element (i, j) is produced once, by the warp of
+  // its smallest shared body: g_b1 (registers/shuffles) + g_b2 (the other
+  // shared body's blocks, from L1) in ascending body order, then + R on the
+  // diagonal, P-scaled and + (eta+rho) on the diagonal.  No atomics, no second
+  // pass; elements without a shared body keep the zero fill.
   {
     const int nb = W.nb;
     const int32_t* cptr = bv.csr_ptr + W.body_off + w;
     const int32_t* clist = bv.csr + 2 * R0;
-    for (int phase = 0; phase < 2; ++phase) {
-      for (int b = wid; b < nb; b += NW) {
-        const int beg = cptr[b], end = cptr[b + 1];
-        for (int pc = beg; pc < end; pc += 32) {
-          const int p = pc + lane;
-          double gm[6];
-          int ip = -1;
-          if (p < end) {
-            const int e = clist[p];
-            ip = e >> 1;
-            const double* jm = rj[ip].JM + 6 * (e & 1);
+    for (int b = wid; b < nb; b += NW) {
+      const int beg = cptr[b], end = cptr[b + 1];
+      for (int pc = beg; pc < end; pc += 32) {
+        const int p = pc + lane;
+        double gm[6];
+        int ip = -1, sp_ = 0, a0 = -1, a1 = -1;
+        if (p < end) {
+          const int e = clist[p];
+          ip = e >> 1;
+          sp_ = e & 1;
+          const double* jm = rj[ip].JM + 6 * sp_;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) gm[k] = jm[k];
+          for (int k = 0; k < 6; ++k) gm[k] = jm[k];
+          a0 = rbs[2 * ip];
+          a1 = rbs[2 * ip + 1];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 6; ++k) gm[k] = 0.0;
+        }
+        for (int qc = beg; qc <= pc; qc += 32) {
+          const int q = qc + lane;
+          double g[6];
+          int iq = -1;
+          if (q < end) {
+            const int e = clist[q];
+            iq = e >> 1;
+            const double* jj = rj[iq].J + 6 * (e & 1);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) g[k] = jj[k];
           } else {
 #pragma unroll
-            for (int k = 0; k < 6; ++k) gm[k] = 0.0;
+            for (int k = 0; k < 6; ++k) g[k] = 0.0;
           }
-          for (int qc = beg; qc <= pc; qc += 32) {
-            const int q = qc + lane;
-            double g[6];
-            int iq = -1;
-            if (q < end) {
-              const int e = clist[q];
-              iq = e >> 1;
-              const double* jj = rj[iq].J + 6 * (e & 1);
+          const int qn = min(32, end - qc);
+          for (int qq = 0; qq < qn; ++qq) {
+            const int jrow = __shfl_sync(FULL, iq, qq);
+            double gq[6];
 #pragma unroll
-              for (int k = 0; k < 6; ++k) g[k] = jj[k];
-            } else {
+            for (int k = 0; k < 6; ++k) gq[k] = __shfl_sync(FULL, g[k], qq);
+            if (ip < 0 || jrow > ip) continue;  // lower triangle, rows ascending
+            const int c0 = rbs[2 * jrow], c1 = rbs[2 * jrow + 1];
+            const int other = sp_ == 0 ? a1 : a0;  // row ip's other body (b is this side)
+            const bool two = other >= 0 && (other == c0 || other == c1);
+            if (two && other < b) continue;  // the smaller shared body's warp owns (i, j)
+            double s = 0.0;
 #pragma unroll
-              for (int k = 0; k < 6; ++k) g[k] = 0.0;
+            for (int k = 0; k < 6; ++k) s += gm[k] * gq[k];
+            if (two) {
+              const double* jm2 = rj[ip].JM + 6 * (1 - sp_);
+              const double* jj2 = rj[jrow].J + 6 * (c0 == other ? 0 : 1);
+              double s2 = 0.0;
+#pragma unroll
+              for (int k = 0; k < 6; ++k) s2 += jm2[k] * jj2[k];
+              s += s2;
             }
-            for (int qq = 0; qq < 32; ++qq) {
-              const int jrow = __shfl_sync(FULL, iq, qq);
-              double gq[6];
-#pragma unroll
-              for (int k = 0; k < 6; ++k) gq[k] = __shfl_sync(FULL, g[k], qq);
-              if (ip < 0 || jrow < 0 || jrow > ip) continue;  // lower triangle, rows ascending
-              // shared bodies of rows ip and jrow
-              const int a0 = rbs[2 * ip], a1 = rbs[2 * ip + 1], c0 = rbs[2 * jrow], c1 = rbs[2 * jrow + 1];
-              const bool s0 = a0 >= 0 && (a0 == c0 || a0 == c1);
-              const bool s1 = a1 >= 0 && (a1 == c0 || a1 == c1);
-              const int smin = (s0 && s1) ? min(a0, a1) : (s0 ? a0 : a1);
-              const bool two = s0 && s1;
-              const bool mine = phase == 0 ? (b == smin) : (two && b == max(a0, a1));
-              if (!mine) continue;
-              double s = 0.0;
-#pragma unroll
-              for (int k = 0; k < 6; ++k) s += gm[k] * gq[k];
-              const int o = lidx(ip, jrow, n);
-              if (phase == 0) L[o] = s;
-              else L[o] += s;
-            }
+            if (ip == jrow) s += regg[ip];
+            double d = (P[ip] * s) * P[jrow];
+            if (ip == jrow) d += eta_rho;
+            L[lidx(ip, jrow, n)] = d;
           }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  stamp(0);
-  // diagonal += R; P D P; += (eta + rho) I   (delassus.cpp:96-100)
-  {
-    const int ntiles = T * (T + 1) / 2;
-    for (int u = wid; u < ntiles; u += NW) {
-      int ti = 0;
-      while ((ti + 1) * (ti + 2) / 2 <= u) ++ti;
-      const int tj = u - ti * (ti + 1) / 2;
-      const int rows = tile_rows(ti, n);
-      if (ti == tj) {
-        double* D = L + diag_tile(ti, n);
-        for (int e = lane; e < tri(rows); e += 32) {
-          int r = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-          while (tri(r + 1) <= e) ++r;
-          while (tri(r) > e) --r;
-          const int i = 32 * ti + r, j = 32 * ti + (e - tri(r));
-          double d = D[e];
-          if (i == j) d += regg[i];
-          d = (P[i] * d) * P[j];
-          if (i == j) d += eta_rho;
-          D[e] = d;
-        }
-      } else {
-        double* A = L + off_tile(ti, tj, n);
-        const double pj = P[32 * tj + lane];
-        for (int r = 0; r < rows; ++r) {
-          const int o = r * LDT + lane;
-          A[o] = (P[32 * ti + r] * A[o]) * pj;
         }
       }
     }
   }
   __syncthreads();
-  stamp(1);
+  stamp(0);
   // ---- 2. blocked right-looking Cholesky with look-ahead; diagonal tiles
   // become L_kk^{-1}.  While warps 1.. run the trailing update of step k,
   // warp 0 updates and factors diagonal tile k+1 (the critical path).

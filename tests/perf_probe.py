@@ -62,7 +62,7 @@ b, cfg = make(148, settle=50)
 b.step(cfg, 1)
 pc = b.phase_cycles()
 its = np.array([x.iterations for x in b.diagnostics()[:148]])
-names = ["gram", "scale", "cholesky", "inverse", "padmm", "chol_panel", "chol_syrk_phase", "chol_warp0_diag_path"]
+names = ["gram_scaled", "unused", "cholesky", "inverse", "padmm", "chol_panel", "chol_syrk", "chol_diag"]
 print(json.dumps({"phase_cycles_mean": {names[k]: float(pc[:, k].mean()) for k in range(8)},
                   "iters_mean": float(its.mean()),
                   "padmm_cycles_per_iter": float((pc[:, 4] / np.maximum(its, 1)).mean())}), flush=True)
