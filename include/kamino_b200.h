@@ -262,6 +262,28 @@ int kd_batch_get_timing(kd_batch* batch, double* ms4, int64_t* launches);
  * 4 PADMM loop, 5/6/7 Cholesky panel/trailing/diagonal-chain sub-totals
  * (worlds on another backend report zeros). */
 int kd_batch_get_phase_cycles(kd_batch* batch, int64_t* out);
+/* Diagnostics: which device kernel solved each world's last step:
+ * KD_KERNEL_NONE (inactive / no rows), KD_KERNEL_DENSE (fused dense LLT, shared
+ * or global factor), KD_KERNEL_SUPERNODAL (sparse LLT with the model's plan),
+ * KD_KERNEL_CR (matrix-free Conjugate Residual). */
+#define KD_KERNEL_NONE 0
+#define KD_KERNEL_DENSE 1
+#define KD_KERNEL_SUPERNODAL 2
+#define KD_KERNEL_CR 3
+int kd_batch_get_kernels(kd_batch* batch, int32_t* out);
+
+/* Supernodal sparse-LLT plan of a model (the factorization the device uses for
+ * the reference's Dense backend, DenseDelassus delassus.cpp:59-65, on models
+ * whose static row-capacity pattern admits one).  stats[0..11] = slots S,
+ * nnz(L), per-world fp64 array length, supernodes, solve levels, factor
+ * levels, factor FMA terms, solve FMA terms per PADMM iteration, dense-LLT
+ * terms S^3/6, factor critical path, solve critical path, solve phases.
+ * Returns KD_ERR_INVALID_ARGUMENT with the reason if the model has no plan. */
+int kd_model_sparse_plan_info(const kd_model* model, int64_t* stats12);
+/* Host self-test of the plan (no device): a random SPD system with the plan's
+ * pattern and a random active-slot mask, solved by the plan's factor and solve
+ * programs and by a dense Cholesky; writes the max relative difference. */
+int kd_model_sparse_plan_selftest(const kd_model* model, uint64_t seed, double* max_rel_err);
 
 const char* kd_last_error(void);
 const char* kd_version(void);

@@ -35,6 +35,8 @@ KD_INTEGRATOR_MOREAU_JEAN = 1
 KD_BACKEND_DENSE = 0
 KD_BACKEND_MATRIX_FREE = 1
 KD_BACKEND_AUTO = 2
+KD_KERNEL_NONE, KD_KERNEL_DENSE, KD_KERNEL_SUPERNODAL, KD_KERNEL_CR = 0, 1, 2, 3
+KERNEL_NAMES = {0: 'none', 1: 'dense', 2: 'supernodal', 3: 'cr'}
 
 
 class kd_body_desc(C.Structure):
@@ -217,6 +219,9 @@ KD_ONLY = {
     "batch_set_state_async": (C.c_int, [_H, c_double_p, c_double_p]),
     "batch_get_state_async": (C.c_int, [_H, c_double_p, c_double_p]),
     "abi_sizes": (C.c_int, [c_int32_p, C.c_int32]),
+    "batch_get_kernels": (C.c_int, [_H, c_int32_p]),
+    "model_sparse_plan_info": (C.c_int, [_H, c_int64_p]),
+    "model_sparse_plan_selftest": (C.c_int, [_H, C.c_uint64, c_double_p]),
 }
 
 

@@ -602,6 +602,13 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
     }
     run += tot;
   }
+  bool sn_ok = sp.sparse && M.sn;
+  if (sn_ok) {
+    const int32_t* pslot = bv.sn_pair_slot + bv.snplan[W.model].pair_off;
+    bool planned = true;
+    for (int c = lane; c < nc; c += 32) planned = planned && pslot[ct[c].pair] >= 0;
+    sn_ok = __all_sync(0xffffffffu, planned);
+  }
   if (lane == 0) {
     cptr[M.nb] = run;
     ws.n_rows = n;
@@ -613,6 +620,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
     if (n > 0) {  // build_backend choice (delassus.cpp:204-206)
       const bool dense = sp.backend == 0 /*KD_BACKEND_DENSE*/ || (sp.backend == 2 /*AUTO*/ && n <= 300);
       be = dense ? (n <= W.smem_cap ? BE_DENSE_SMEM : BE_DENSE_GLOBAL) : BE_MATRIX_FREE;
+      // the dense LLT is factored by the supernodal kernel when the model has a
+      // plan and every active contact lies in a planned slot (kd_snplan.h)
+      if (dense && sn_ok && !overflow) be = BE_SPARSE;
       if (be == BE_DENSE_GLOBAL && n > W.slab_cap) overflow = true;
     }
     if (overflow) {

@@ -11,10 +11,12 @@
 // backend this step (the choice depends on the contact/limit count, known only
 // on the device).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <random>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "kd_host.h"
@@ -67,6 +69,7 @@ struct Bin {
 constexpr int kClasses[4][2] = {{32, 64}, {64, 64}, {128, 128}, {232, 256}};
 constexpr int kSmemMaxRows = 232;
 constexpr int kDenseGlobalMaxRows = KD_DENSE_ROW_CROSSOVER;
+constexpr size_t kSnMaxSmem = 232448;  // per-CTA shared memory opt-in limit (227 KB)
 
 }  // namespace
 
@@ -85,6 +88,13 @@ struct kd_batch {
   BatchView view{};
   std::vector<Bin> dense_bins;
   Bin global_bin, cr_auto_bin, cr_all_bin;
+  // supernodal sparse-LLT bins: one per planned model (worlds of one model per CTA)
+  struct SnBin {
+    int model = 0, per_warp = 0, wpc = 1;
+    Bin bin;
+  };
+  std::vector<SnBin> sn_bins;
+  bool sparse = true;
   int hist_cap = 0;
   double* d_hist = nullptr;
   int32_t* d_err = nullptr;
@@ -144,7 +154,85 @@ int kd_model_build(const kd_scene_desc* scene, kd_model** out) {
     delete m;
     return fail(code, err);
   }
+  auto plan = std::make_shared<SnPlanHost>();
+  if (build_sn_plan(m->m, *plan, m->m.sn_why)) m->m.sn = plan;
   *out = m;
+  return KD_OK;
+}
+
+int kd_model_sparse_plan_info(const kd_model* mp, int64_t* st) {
+  if (!mp || !st) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (!mp->m.sn) return fail(KD_ERR_INVALID_ARGUMENT, "model has no sparse plan: " + mp->m.sn_why);
+  const SnPlanHost& p = *mp->m.sn;
+  const int64_t v[12] = {p.S, p.nnzL, p.nLv, p.n_super, p.s_levels, (int64_t)p.fphase.size(), p.factor_terms,
+                         p.solve_terms, p.dense_factor_terms, p.factor_crit, p.solve_crit, (int64_t)p.sphase.size()};
+  for (int k = 0; k < 12; ++k) st[k] = v[k];
+  return KD_OK;
+}
+
+int kd_model_sparse_plan_selftest(const kd_model* mp, uint64_t seed, double* max_rel_err) {
+  if (!mp || !max_rel_err) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (!mp->m.sn) return fail(KD_ERR_INVALID_ARGUMENT, "model has no sparse plan: " + mp->m.sn_why);
+  const SnPlanHost& p = *mp->m.sn;
+  const int S = p.S;
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> U(-1.0, 1.0);
+  // rows with random 6-blocks on their slot bodies: D = J J^T + 0.1 I has the plan's pattern
+  std::vector<double> J((size_t)S * 12);
+  for (double& x : J) x = U(rng);
+  std::vector<uint8_t> act(S);
+  for (int s = 0; s < S; ++s) act[s] = s < p.n_jd ? 1 : (rng() & 1);
+  std::vector<double> D((size_t)S * S, 0.0), b(S), x(S);
+  for (int s = 0; s < S; ++s) {
+    b[s] = U(rng);
+    for (int t = 0; t < S; ++t) {
+      double v = s == t ? 0.1 : 0.0;
+      for (int u = 0; u < 2; ++u)
+        for (int w = 0; w < 2; ++w) {
+          const int bs = p.slot_body[2 * s + u];
+          if (bs >= 0 && bs == p.slot_body[2 * t + w])
+            for (int k = 0; k < 6; ++k) v += J[(size_t)s * 12 + 6 * u + k] * J[(size_t)t * 12 + 6 * w + k];
+        }
+      D[(size_t)s * S + t] = v;
+    }
+  }
+  if (!sn_plan_cpu_solve(p, D.data(), act.data(), b.data(), x.data()))
+    return fail(KD_ERR_SPD_FAILURE, "plan factorization hit a non-positive pivot");
+  // dense reference on the active subsystem
+  std::vector<int> idx;
+  for (int s = 0; s < S; ++s)
+    if (act[s]) idx.push_back(s);
+  const int n = (int)idx.size();
+  std::vector<double> A((size_t)n * n), y(n);
+  for (int i = 0; i < n; ++i) {
+    y[i] = b[idx[i]];
+    for (int j = 0; j < n; ++j) A[(size_t)i * n + j] = D[(size_t)idx[i] * S + idx[j]];
+  }
+  for (int j = 0; j < n; ++j) {
+    double d = A[(size_t)j * n + j];
+    for (int k = 0; k < j; ++k) d -= A[(size_t)j * n + k] * A[(size_t)j * n + k];
+    d = std::sqrt(d);
+    A[(size_t)j * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double v = A[(size_t)i * n + j];
+      for (int k = 0; k < j; ++k) v -= A[(size_t)i * n + k] * A[(size_t)j * n + k];
+      A[(size_t)i * n + j] = v / d;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    for (int k = 0; k < i; ++k) y[i] -= A[(size_t)i * n + k] * y[k];
+    y[i] /= A[(size_t)i * n + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    for (int k = i + 1; k < n; ++k) y[i] -= A[(size_t)k * n + i] * y[k];
+    y[i] /= A[(size_t)i * n + i];
+  }
+  double err = 0.0, scale = 0.0;
+  for (int i = 0; i < n; ++i) scale = std::max(scale, std::fabs(y[i]));
+  for (int i = 0; i < n; ++i) err = std::max(err, std::fabs(x[idx[i]] - y[i]));
+  for (int s = 0; s < S; ++s)
+    if (!act[s]) err = std::max(err, std::fabs(x[s]));
+  *max_rel_err = err / std::max(scale, 1e-300);
   return KD_OK;
 }
 
@@ -204,6 +292,10 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     if (!models[i]) return fail(KD_ERR_INVALID_ARGUMENT, "null model");
     b->models.push_back(models[i]->m);
   }
+  {  // KD_SPARSE=0 disables the supernodal path (A/B comparisons against the dense kernel)
+    const char* e = getenv("KD_SPARSE");
+    b->sparse = !(e && e[0] == '0');
+  }
   b->n_worlds = n_worlds;
   // model tables
   std::vector<DevModel> dm(n_models);
@@ -232,6 +324,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     d.joint_off = (int)joints.size();
     d.geom_off = (int)geoms.size();
     d.pair_off = (int)pairs.size();
+    d.sn = (b->sparse && m.sn && (size_t)m.sn->smem_doubles * 8 <= kSnMaxSmem) ? 1 : 0;
     for (int k = 0; k < 3; ++k) d.gravity[k] = m.gravity[k];
     bodies.insert(bodies.end(), m.bodies.begin(), m.bodies.end());
     joints.insert(joints.end(), m.joints.begin(), m.joints.end());
@@ -307,6 +400,16 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     bin.nt = kClasses[c][1];
     bin.worlds = class_worlds[c];
     b->dense_bins.push_back(bin);
+  }
+  for (int i = 0; i < n_models; ++i) {
+    if (!dm[i].sn) continue;
+    kd_batch::SnBin sbn;
+    sbn.model = i;
+    sbn.per_warp = b->models[i].sn->smem_doubles;
+    sbn.wpc = (int)std::max<size_t>(1, std::min<size_t>(8, kSnMaxSmem / (8 * (size_t)sbn.per_warp)));
+    for (int w = 0; w < n_worlds; ++w)
+      if (world_model[w] == i) sbn.bin.worlds.push_back(w);
+    if (!sbn.bin.worlds.empty()) b->sn_bins.push_back(sbn);
   }
   b->global_bin.cap = kDenseGlobalMaxRows;
   b->global_bin.nt = 256;
@@ -397,6 +500,80 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     bin.count = (int)bin.worlds.size();
     KD_CK(mem.alloc(bin.d_worlds, bin.count));
     KD_CK(cudaMemcpy(bin.d_worlds, bin.worlds.data(), 4 * bin.count, cudaMemcpyHostToDevice));
+  }
+  for (auto& sbn : b->sn_bins) {
+    sbn.bin.count = (int)sbn.bin.worlds.size();
+    KD_CK(mem.alloc(sbn.bin.d_worlds, sbn.bin.count));
+    KD_CK(cudaMemcpy(sbn.bin.d_worlds, sbn.bin.worlds.data(), 4 * sbn.bin.count, cudaMemcpyHostToDevice));
+  }
+  {  // supernodal plans, concatenated over models with relocated offsets
+    std::vector<DevSnPlan> dp(n_models);
+    std::vector<SnGram> gram;
+    std::vector<SnOp> fops;
+    std::vector<uint32_t> fterms, sterms;
+    std::vector<SnSOp> sops;
+    std::vector<SnPhase> phases;
+    std::vector<int32_t> pslot;
+    std::vector<uint16_t> spos;
+    for (int i = 0; i < n_models; ++i) {
+      DevSnPlan& d = dp[i];
+      d = DevSnPlan{};
+      if (!dm[i].sn) continue;
+      const SnPlanHost& p = *b->models[i].sn;
+      d.S = p.S;
+      d.nLv = p.nLv;
+      d.n_jd = p.n_jd;
+      d.lim_base = p.lim_base;
+      d.smem_doubles = p.smem_doubles;
+      d.gram_off = (int)gram.size();
+      d.n_gram = (int)p.gram.size();
+      gram.insert(gram.end(), p.gram.begin(), p.gram.end());
+      d.pair_off = (int)pslot.size();
+      pslot.insert(pslot.end(), p.pair_slot.begin(), p.pair_slot.end());
+      d.slotpos_off = (int)spos.size();
+      spos.insert(spos.end(), p.slot_pos.begin(), p.slot_pos.end());
+      const uint32_t fto = (uint32_t)fterms.size(), sto = (uint32_t)sterms.size();
+      const int fo = (int)fops.size(), so = (int)sops.size();
+      for (SnOp o : p.fops) {
+        o.toff += fto;
+        fops.push_back(o);
+      }
+      for (SnSOp o : p.sops) {
+        o.toff += sto;
+        sops.push_back(o);
+      }
+      fterms.insert(fterms.end(), p.fterms.begin(), p.fterms.end());
+      sterms.insert(sterms.end(), p.sterms.begin(), p.sterms.end());
+      d.fph_off = (int)phases.size();
+      d.n_fph = (int)p.fphase.size();
+      for (SnPhase q : p.fphase) {
+        q.off += fo;
+        phases.push_back(q);
+      }
+      d.sph_off = (int)phases.size();
+      d.n_sph = (int)p.sphase.size();
+      for (SnPhase q : p.sphase) {
+        q.off += so;
+        phases.push_back(q);
+      }
+    }
+    auto up = [&](auto*& dst, const auto& vec) -> cudaError_t {
+      using T = typename std::remove_reference<decltype(vec)>::type::value_type;
+      T* ptr = nullptr;
+      cudaError_t e = mem.alloc(ptr, vec.size());
+      if (e == cudaSuccess && !vec.empty()) e = cudaMemcpy(ptr, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice);
+      dst = ptr;
+      return e;
+    };
+    KD_CK(up(v.snplan, dp));
+    KD_CK(up(v.sn_gram, gram));
+    KD_CK(up(v.sn_fops, fops));
+    KD_CK(up(v.sn_fterms, fterms));
+    KD_CK(up(v.sn_sops, sops));
+    KD_CK(up(v.sn_sterms, sterms));
+    KD_CK(up(v.sn_phases, phases));
+    KD_CK(up(v.sn_pair_slot, pslot));
+    KD_CK(up(v.sn_slot_pos, spos));
   }
   for (cudaEvent_t& e : b->ev) KD_CK(cudaEventCreate(&e));
   KD_CK(cudaDeviceSynchronize());
@@ -526,6 +703,7 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
   sp.warm_start = c->warm_start;
   sp.moreau = c->integrator == KD_INTEGRATOR_MOREAU_JEAN;
   sp.backend = c->backend;
+  sp.sparse = b->sparse ? 1 : 0;
   const BatchView& v = b->view;
   cudaStream_t s = b->stream;
   auto mark = [&](int i) {
@@ -538,6 +716,10 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
     ++b->launches;
     mark(1);
     if (c->backend != KD_BACKEND_MATRIX_FREE) {
+      for (const auto& sbn : b->sn_bins) {
+        KD_CK(launch_sparse(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.per_warp, sbn.wpc, s));
+        ++b->launches;
+      }
       for (const Bin& bin : b->dense_bins) {
         KD_CK(launch_dense(v, sp, bin.d_worlds, bin.count, bin.cap, bin.nt, false, s));
         ++b->launches;
@@ -661,7 +843,22 @@ int kd_batch_get_phase_cycles(kd_batch* b, int64_t* out) {
   if (b->n_worlds)
     KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
   for (int w = 0; w < b->n_worlds; ++w)
-    for (int k = 0; k < 8; ++k) out[8 * w + k] = ws[w].backend == BE_DENSE_SMEM ? ws[w].phase_cycles[k] : 0;
+    for (int k = 0; k < 8; ++k) out[8 * w + k] = (ws[w].backend == BE_DENSE_SMEM || ws[w].backend == BE_SPARSE) ? ws[w].phase_cycles[k] : 0;
+  return KD_OK;
+}
+
+int kd_batch_get_kernels(kd_batch* b, int32_t* out) {
+  if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  KD_CK(cudaSetDevice(b->device));
+  std::vector<WorldStep> ws(b->n_worlds);
+  if (b->n_worlds)
+    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+  for (int w = 0; w < b->n_worlds; ++w) {
+    const int be = ws[w].backend;
+    out[w] = be == BE_SPARSE ? KD_KERNEL_SUPERNODAL
+             : (be == BE_DENSE_SMEM || be == BE_DENSE_GLOBAL) ? KD_KERNEL_DENSE
+             : be == BE_MATRIX_FREE ? KD_KERNEL_CR : KD_KERNEL_NONE;
+  }
   return KD_OK;
 }
 

@@ -3,12 +3,14 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/kamino_b200.h"
 #include "kd_layout.h"
 #include "kd_math.cuh"
+#include "kd_snplan.h"
 
 namespace kd {
 
@@ -23,6 +25,9 @@ struct HostModel {
   std::vector<double> init_pose, init_twist;
   int n_bil = 0, n_dyn = 0, n_loops = 0;
   kd_model_info info{};
+  // supernodal sparse-LLT plan (kd_snplan.h); null if the model is unsuited
+  std::shared_ptr<SnPlanHost> sn;
+  std::string sn_why;
 };
 
 int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err);
@@ -34,6 +39,8 @@ cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_
                   bool global_l, cudaStream_t s);
 cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
                int nt, cudaStream_t s);
+cudaError_t launch_sparse(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int per_warp,
+                          int wpc, cudaStream_t s);
 void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s);
 size_t dense_smem_bytes(int n, int nt, bool global_l);
 size_t dense_factor_doubles(int n);

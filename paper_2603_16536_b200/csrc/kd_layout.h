@@ -26,7 +26,7 @@ enum GeomShape : int32_t { G_SPHERE = 0, G_PLANE = 1, G_BOX = 2 };
 // `a` is always the moving geom (ContactPoint::geom_a), `b` the other one.
 enum PairKind : int32_t { P_SPHERE_SPHERE = 0, P_SPHERE_PLANE = 1, P_BOX_PLANE = 2 };
 enum RowKind : int32_t { ROW_BILATERAL = 0, ROW_LIMIT = 1, ROW_CONTACT = 2 };
-enum Backend : int32_t { BE_NONE = -1, BE_DENSE_SMEM = 0, BE_DENSE_GLOBAL = 1, BE_MATRIX_FREE = 2 };
+enum Backend : int32_t { BE_NONE = -1, BE_DENSE_SMEM = 0, BE_DENSE_GLOBAL = 1, BE_MATRIX_FREE = 2, BE_SPARSE = 3 };
 
 enum JointFlags : int32_t {
   JF_PD = 1,
@@ -63,9 +63,43 @@ struct DevModel {
   int32_t nb, nj, ng, npairs;
   int32_t n_bil, n_dyn, n_limited, max_contacts;
   int32_t row_cap, body_off, joint_off, geom_off;
-  int32_t pair_off, pad0, pad1, pad2;
+  int32_t pair_off, sn, pad1, pad2;  // sn: model has a supernodal plan (DevSnPlan)
   double gravity[3];
   double pad3;
+};
+
+// ---- supernodal sparse-LLT plan (kd_snplan.h), one per model, immutable.
+// D entry of the Gram phase: D(s, t), s >= t (slot order).
+struct SnGram {
+  uint16_t dst;  // Lv index
+  uint16_t s, t; // slots
+  uint16_t flags;
+};
+enum SnGramFlags : uint16_t {
+  SG_DIAG = 1,
+  SG_TWO = 2,  // two shared bodies
+  SG_S1 = 4,   // side of s for the first (smaller) shared body
+  SG_T1 = 8,   // side of t for the first shared body
+  SG_S2 = 16,  // sides for the second shared body
+  SG_T2 = 32,
+};
+enum SnOpKind : uint16_t { SN_NOP = 0, SN_OFF = 1, SN_DIAG = 2 };
+struct SnOp {  // factor op: acc = Lv[dst] - sum Lv[a] Lv[b]; OFF: *Lv[aux]; DIAG: rsqrt
+  uint16_t dst, aux, nterm, kind;
+  uint32_t toff, pad;
+};
+struct SnSOp {  // solve op (dst == 0xffff: no-op)
+  uint16_t dst, nterm;
+  uint32_t toff;
+};
+struct SnPhase {
+  int32_t off, steps, mode, pad;  // ops at off + step * 32 + lane; mode 0 = A, 1 = B
+};
+struct DevSnPlan {
+  int32_t S, nLv, n_jd, lim_base;
+  int32_t gram_off, n_gram, pair_off, slotpos_off;
+  int32_t fph_off, n_fph, sph_off, n_sph;
+  int32_t smem_doubles, pad0, pad1, pad2;  // per-warp shared-memory footprint
 };
 
 // Per-world indexing (prefix sums over model capacities).
@@ -170,6 +204,16 @@ struct BatchView {
   double* lslab;    // dense-global factor storage
   double* hist;     // [n_worlds][hist_cap]
   int32_t* error_count;
+  // supernodal plans (indexed by model; S == 0: none)
+  const DevSnPlan* snplan;
+  const SnGram* sn_gram;
+  const SnOp* sn_fops;
+  const uint32_t* sn_fterms;
+  const SnSOp* sn_sops;
+  const uint32_t* sn_sterms;
+  const SnPhase* sn_phases;
+  const int32_t* sn_pair_slot;
+  const uint16_t* sn_slot_pos;
 };
 
 struct StepParams {
@@ -177,6 +221,7 @@ struct StepParams {
   double beta, contact_margin, impact_thr, bias_clamp, lim_margin_ang, lim_margin_lin;
   int32_t max_iters, acceleration, restart, fixed_mode;
   int32_t cr_iters, warm_start, moreau, backend;  // backend: KD_BACKEND_*
+  int32_t sparse, pad0;                            // supernodal path enabled for planned models
 };
 
 }  // namespace kd

@@ -1,0 +1,378 @@
+// kd_sparse.cu — K2s: supernodal sparse-LLT path, one warp per world.
+//
+// Same mathematics as K2 (kd_dense.cu) — the reference's Dense backend:
+//   assemble_dense  D = P (J M^-1 J^T + R) P + (eta+rho) I   (delassus.cpp:67-104)
+//   DenseDelassus   D = L L^T once per step, two triangular solves per PADMM
+//                   iteration                              (delassus.cpp:59-65)
+//   padmm_solve     De Saxce shift, solve, cone projection, dual update,
+//                   residual triple, Nesterov with restart (padmm.cpp:87-159)
+// but D is factored in a fill-reducing order using the model's static plan
+// (kd_snplan.h): for DR-Legs nnz(L) = 3.6k instead of n^2/2 = 24.6k and the
+// factor costs 34k FMA instead of 1.8M.  Everything a world needs (the factor
+// array Lv, the PADMM vectors) fits in ~53 KB of shared memory, so one warp owns
+// one world for the whole solve and a CTA holds several worlds of one model.
+// All synchronisation is __syncwarp: level-scheduled programs keep each level's
+// ops independent, and the plan was packed so the ops of a level are balanced
+// over the 32 lanes.
+//
+// Per-warp shared memory (doubles):  Lv[nLv] | v[S] | t[S] | vf x y z yh zh yp zp [S each]
+//                                    | int16 row2pos[S] | int16 slot2row[S]
+#include "kd_device.cuh"
+
+namespace kd {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ void project_soc(const double w[3], double mu, double y[3]) {  // padmm.cpp:19-37
+  const double wn = w[0];
+  const double tn = sqrt(w[1] * w[1] + w[2] * w[2]);
+  y[0] = w[0];
+  y[1] = w[1];
+  y[2] = w[2];
+  if (tn <= mu * wn) return;
+  if (mu * tn <= -wn) {
+    y[0] = y[1] = y[2] = 0.0;
+    return;
+  }
+  const double tau = (wn + mu * tn) / (1.0 + mu * mu);
+  y[0] = tau;
+  if (tn > 0) {
+    y[1] = mu * tau * w[1] / tn;
+    y[2] = mu * tau * w[2] / tn;
+  } else {
+    y[1] = y[2] = 0.0;
+  }
+}
+
+__device__ __forceinline__ int pad2(int x) { return (x + 1) & ~1; }
+
+}  // namespace
+
+__global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams sp, const int32_t* worlds, int count,
+                                                     int per_warp) {
+  extern __shared__ __align__(16) double smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int slot_idx = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (slot_idx >= count) return;
+  const int w = worlds[slot_idx];
+  WorldStep& ws = bv.wstep[w];
+  if (ws.backend != BE_SPARSE) return;
+  const DevWorld W = bv.worlds[w];
+  const DevSnPlan P = bv.snplan[W.model];
+  const DevModel M = bv.models[W.model];
+  const int S = P.S, Sp = pad2(S);
+  double* Lv = smem + (size_t)wid * per_warp;
+  double* v = Lv + pad2(P.nLv);
+  double* t = v + Sp;
+  double* vf_s = t + Sp;
+  double* x_s = vf_s + Sp;
+  double* y_s = x_s + Sp;
+  double* z_s = y_s + Sp;
+  double* yh_s = z_s + Sp;
+  double* zh_s = yh_s + Sp;
+  double* yp_s = zh_s + Sp;
+  double* zp_s = yp_s + Sp;
+  int16_t* row2pos = reinterpret_cast<int16_t*>(zp_s + Sp);
+  int16_t* slot2row = row2pos + Sp;
+
+  const int64_t R0 = W.row_off;
+  const int n = ws.n_rows;
+  const int n_lim = ws.n_limits, nc = ws.n_contacts;
+  const int n_jd = P.n_jd;
+  const int first_contact = n_jd + n_lim;
+  const uint16_t* slot_pos = bv.sn_slot_pos + P.slotpos_off;
+  long long t_prev = clock64();
+  auto stamp = [&](int k) {
+    if (lane == 0) {
+      const long long tc = clock64();
+      ws.phase_cycles[k] = tc - t_prev;
+      t_prev = tc;
+    }
+  };
+
+  // ---- 0. zero the factor array, map compact rows <-> planned slots
+  for (int e = lane; e < P.nLv; e += 32) Lv[e] = 0.0;
+  for (int s = lane; s < S; s += 32) {
+    v[s] = 0.0;
+    slot2row[s] = s < n_jd ? (int16_t)s : (int16_t)-1;
+  }
+  for (int r = lane; r < n_jd; r += 32) row2pos[r] = (int16_t)slot_pos[r];
+  __syncwarp();
+  {
+    const int32_t* lk = bv.lkey + 2 * R0;
+    const DevJoint* mj = bv.joints + M.joint_off;
+    for (int r = n_jd + lane; r < first_contact; r += 32) {  // limit rows: (joint, bound) -> slot
+      const int slot = P.lim_base + 2 * mj[lk[2 * r]].limit_slot + lk[2 * r + 1];
+      slot2row[slot] = (int16_t)r;
+      row2pos[r] = (int16_t)slot_pos[slot];
+    }
+    const Contact* ct = bv.contacts + W.contact_off;
+    const int32_t* pslot = bv.sn_pair_slot + P.pair_off;
+    for (int c = lane; c < nc; c += 32) {  // contacts: (pair, index within the pair) -> slot
+      const int pr = ct[c].pair;
+      int k = 0;
+      while (c - k - 1 >= 0 && ct[c - k - 1].pair == pr) ++k;
+      const int slot = pslot[pr] + 3 * k;
+      for (int d = 0; d < 3; ++d) {
+        slot2row[slot + d] = (int16_t)(first_contact + 3 * c + d);
+        row2pos[first_contact + 3 * c + d] = (int16_t)slot_pos[slot + d];
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- 1. Gram: D(s, t) for every planned nonzero (delassus.cpp:67-104)
+  {
+    const RowJ* rj = bv.rowj + R0;
+    const double* scale = bv.scale + R0;
+    const double* reg = bv.reg + R0;
+    const double eta_rho = sp.eta + sp.rho;
+    const SnGram* gl = bv.sn_gram + P.gram_off;
+    for (int e = lane; e < P.n_gram; e += 32) {
+      const SnGram g = gl[e];
+      const int rs = slot2row[g.s], rt = slot2row[g.t];
+      if (rs < 0 || rt < 0) {  // inactive slot: identity row
+        if (g.flags & SG_DIAG) Lv[g.dst] = 1.0;
+        continue;
+      }
+      const double* jm = rj[rs].JM + ((g.flags & SG_S1) ? 6 : 0);
+      const double* jj = rj[rt].J + ((g.flags & SG_T1) ? 6 : 0);
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s += jm[k] * jj[k];
+      if (g.flags & SG_TWO) {
+        const double* jm2 = rj[rs].JM + ((g.flags & SG_S2) ? 6 : 0);
+        const double* jj2 = rj[rt].J + ((g.flags & SG_T2) ? 6 : 0);
+        double s2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s2 += jm2[k] * jj2[k];
+        s += s2;
+      }
+      if (g.flags & SG_DIAG) s += reg[rs];
+      double d = (scale[rs] * s) * scale[rt];
+      if (g.flags & SG_DIAG) d += eta_rho;
+      Lv[g.dst] = d;
+    }
+  }
+  __syncwarp();
+  stamp(0);
+
+  // ---- 2. numeric factor + supernode diagonal-block inverses (level-scheduled)
+  {
+    bool bad = false;
+    const SnPhase* ph = bv.sn_phases + P.fph_off;
+    for (int l = 0; l < P.n_fph; ++l) {
+      const SnPhase q = ph[l];
+      for (int st = 0; st < q.steps; ++st) {
+        const SnOp o = bv.sn_fops[q.off + 32 * st + lane];
+        if (o.kind == SN_NOP) continue;
+        const uint32_t* tm = bv.sn_fterms + o.toff;
+        double acc = Lv[o.dst];
+        for (int k = 0; k < o.nterm; ++k) {
+          const uint32_t tt = tm[k];
+          acc -= Lv[tt & 0xffff] * Lv[tt >> 16];
+        }
+        if (o.kind == SN_DIAG) {
+          if (!(acc > 0.0)) bad = true;
+          Lv[o.dst] = rsqrt(acc);
+        } else {
+          Lv[o.dst] = acc * Lv[o.aux];
+        }
+      }
+      __syncwarp();
+    }
+    if (__any_sync(FULL, bad) && lane == 0) {
+      ws.fail = 1;
+      atomicAdd(bv.error_count, 1);
+    }
+  }
+  stamp(2);
+
+  // ---- 3. PADMM (padmm.cpp:87-159); units = bilateral/limit rows and contact triples
+  const int n_units = first_contact + nc;
+  const double eta = sp.eta, rho = sp.rho;
+  const double* rmu = bv.rmu + R0;
+  for (int u = lane; u < n_units; u += 32) {
+    const bool con = u >= first_contact;
+    const int r0 = con ? first_contact + 3 * (u - first_contact) : u;
+    const int nr = con ? 3 : 1;
+    double x[3] = {0, 0, 0}, y[3] = {0, 0, 0};
+    
+#pragma unroll
+      for (int d = 0; d < 3; ++d) if (d < nr) {
+      x[d] = bv.x0[R0 + r0 + d];
+      vf_s[r0 + d] = bv.vf[R0 + r0 + d];
+      const double z = bv.z0[R0 + r0 + d];
+      z_s[r0 + d] = z;
+      zh_s[r0 + d] = z;
+      x_s[r0 + d] = x[d];
+    }
+    if (con) project_soc(x, rmu[r0], y);  // y = Pi_K(x0)
+    else y[0] = u >= n_jd ? fmax(0.0, x[0]) : x[0];
+    
+#pragma unroll
+      for (int d = 0; d < 3; ++d) if (d < nr) {
+      y_s[r0 + d] = y[d];
+      yh_s[r0 + d] = y[d];
+    }
+    // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
+    const double s0 = con ? rmu[r0] * hypot(zh_s[r0 + 1], zh_s[r0 + 2]) : 0.0;
+    
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (d < nr)
+      v[row2pos[r0 + d]] = -((((vf_s[r0 + d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * y[d]) - zh_s[r0 + d]);
+  }
+  __syncwarp();
+  double a = 1.0, prev = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  double r_p = 0, r_d = 0, r_c = 0;
+  int restarts = 0, it = 1;
+  bool converged = false;
+  const int hcap = bv.hist_cap;
+  const SnPhase* sph = bv.sn_phases + P.sph_off;
+  for (it = 1; it <= sp.max_iters; ++it) {
+    // x = D^-1 rhs: forward then backward substitution (phase A / B per level)
+    for (int l = 0; l < P.n_sph; ++l) {
+      const SnPhase q = sph[l];
+      if (q.mode == 0) {
+        for (int st = 0; st < q.steps; ++st) {
+          const SnSOp o = bv.sn_sops[q.off + 32 * st + lane];
+          if (o.dst == 0xffff) continue;
+          const uint32_t* tm = bv.sn_sterms + o.toff;
+          double acc = v[o.dst];
+          for (int k = 0; k < o.nterm; ++k) {
+            const uint32_t tt = tm[k];
+            acc -= Lv[tt & 0xffff] * v[tt >> 16];
+          }
+          t[o.dst] = acc;
+        }
+      } else {
+        for (int st = 0; st < q.steps; ++st) {
+          const SnSOp o = bv.sn_sops[q.off + 32 * st + lane];
+          if (o.dst == 0xffff) continue;
+          const uint32_t* tm = bv.sn_sterms + o.toff;
+          double acc = 0.0;
+          for (int k = 0; k < o.nterm; ++k) {
+            const uint32_t tt = tm[k];
+            acc += Lv[tt & 0xffff] * t[tt >> 16];
+          }
+          v[o.dst] = acc;
+        }
+      }
+      __syncwarp();
+    }
+    double rp = 0.0, dmax = 0.0, rc = 0.0;
+    for (int u = lane; u < n_units; u += 32) {
+      const bool con = u >= first_contact;
+      const int r0 = con ? first_contact + 3 * (u - first_contact) : u;
+      const int nr = con ? 3 : 1;
+      double x[3] = {0, 0, 0}, wv[3] = {0, 0, 0}, yn[3] = {0, 0, 0};
+      
+#pragma unroll
+      for (int d = 0; d < 3; ++d) if (d < nr) {
+        x[d] = v[row2pos[r0 + d]];
+        x_s[r0 + d] = x[d];
+        wv[d] = x[d] - zh_s[r0 + d] / rho;
+      }
+      if (con) project_soc(wv, rmu[r0], yn);
+      else yn[0] = u >= n_jd ? fmax(0.0, wv[0]) : wv[0];
+      double ymax = 0.0, zmax = 0.0;
+      
+#pragma unroll
+      for (int d = 0; d < 3; ++d) if (d < nr) {
+        const double zn = zh_s[r0 + d] - rho * (x[d] - yn[d]);
+        const double yo = y_s[r0 + d];
+        rp = fmax(rp, fabs(x[d] - yn[d]));
+        dmax = fmax(dmax, fabs(yn[d] - yo));
+        ymax = fmax(ymax, fabs(yn[d]));
+        zmax = fmax(zmax, fabs(zn));
+        yp_s[r0 + d] = yo;
+        zp_s[r0 + d] = z_s[r0 + d];
+        y_s[r0 + d] = yn[d];
+        z_s[r0 + d] = zn;
+      }
+      if (u >= n_jd) rc = fmax(rc, fmin(ymax, zmax));
+    }
+    r_p = warp_max(rp);
+    r_d = rho * warp_max(dmax);
+    r_c = warp_max(rc);
+    const double combined = fmax(r_p, fmax(r_d, r_c));
+    if (lane == 0 && it <= hcap) bv.hist[(int64_t)w * hcap + it - 1] = combined;
+    if (!sp.fixed_mode && combined < sp.eps) {
+      converged = true;
+      break;
+    }
+    // nesterov_update (padmm.cpp:58-71)
+    bool restart = false;
+    double beta = 0.0;
+    if (sp.acceleration) {
+      restart = sp.restart && combined > prev;
+      if (restart) {
+        a = 1.0;
+        ++restarts;
+      } else {
+        const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));
+        beta = (a - 1.0) / an;
+        a = an;
+      }
+    }
+    const bool extrapolate = sp.acceleration && !restart;
+    for (int u = lane; u < n_units; u += 32) {
+      const bool con = u >= first_contact;
+      const int r0 = con ? first_contact + 3 * (u - first_contact) : u;
+      const int nr = con ? 3 : 1;
+      
+#pragma unroll
+      for (int d = 0; d < 3; ++d) if (d < nr) {
+        const double y = y_s[r0 + d], z = z_s[r0 + d];
+        yh_s[r0 + d] = extrapolate ? y + beta * (y - yp_s[r0 + d]) : y;
+        zh_s[r0 + d] = extrapolate ? z + beta * (z - zp_s[r0 + d]) : z;
+      }
+      const double s0 = con ? rmu[r0] * hypot(zh_s[r0 + 1], zh_s[r0 + 2]) : 0.0;
+      
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (d < nr)
+        v[row2pos[r0 + d]] =
+            -((((vf_s[r0 + d] + (d == 0 ? s0 : 0.0)) - eta * x_s[r0 + d]) - rho * yh_s[r0 + d]) - zh_s[r0 + d]);
+    }
+    prev = combined;
+    __syncwarp();
+  }
+  stamp(4);
+  // outputs (padmm.cpp:147-157)
+  for (int r = lane; r < n; r += 32) {
+    bv.lam[R0 + r] = y_s[r];
+    bv.zo[R0 + r] = z_s[r];
+  }
+  if (lane == 0) {
+    const int done = min(it, sp.max_iters);
+    ws.iterations = done;
+    ws.r_p = r_p;
+    ws.r_d = r_d;
+    ws.r_c = r_c;
+    ws.restarts = restarts;
+    ws.converged = (converged || fmax(r_p, fmax(r_d, r_c)) < sp.eps) ? 1 : 0;
+    ws.cr_iterations = 0;
+    ws.cr_breakdown = 0;
+    for (int i = done; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
+  }
+}
+
+cudaError_t launch_sparse(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int per_warp,
+                          int wpc, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const size_t smem = (size_t)per_warp * wpc * sizeof(double);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    const cudaError_t e = cudaFuncSetAttribute(sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  sparse_kernel<<<(count + wpc - 1) / wpc, 32 * wpc, smem, s>>>(bv, sp, worlds, count, per_warp);
+  return cudaGetLastError();
+}
+
+}  // namespace kd

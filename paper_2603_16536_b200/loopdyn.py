@@ -100,6 +100,25 @@ class Model:
         _check(lib().kd_joint_coordinate(self.handle, int(joint), _capi.dptr(p), C.byref(out)))
         return out.value
 
+    SPARSE_PLAN_FIELDS = ("slots", "nnz_L", "lv_len", "supernodes", "solve_levels", "factor_levels",
+                          "factor_terms", "solve_terms", "dense_factor_terms", "factor_crit", "solve_crit",
+                          "solve_phases")
+
+    def sparse_plan_info(self) -> Optional[dict]:
+        """Statistics of the supernodal sparse-LLT plan (kd_snplan.h), or None
+        if the model has none (its dense worlds then use the dense kernel)."""
+        st = np.zeros(12, np.int64)
+        if lib().kd_model_sparse_plan_info(self.handle, _capi.i64ptr(st)) != 0:
+            return None
+        return dict(zip(self.SPARSE_PLAN_FIELDS, (int(x) for x in st)))
+
+    def sparse_plan_selftest(self, seed: int = 1) -> float:
+        """Host-only check of the plan: max relative error of its factor/solve
+        programs against a dense Cholesky on a random SPD system."""
+        out = C.c_double()
+        _check(lib().kd_model_sparse_plan_selftest(self.handle, int(seed), C.byref(out)))
+        return out.value
+
     def initial_state(self) -> "WorldState":
         """initial_state (stepper.cpp:97-106)."""
         poses = np.array([list(b.position) + list(_normalized(b.orientation)) for b in self.scene.bodies],
@@ -315,6 +334,14 @@ class WorldBatch:
         _check(lib().kd_batch_get_timing(self.handle, _capi.dptr(ms), C.byref(n)))
         return {"assemble_ms": ms[0], "dense_ms": ms[1], "matrix_free_ms": ms[2], "recover_ms": ms[3],
                 "launches": n.value}
+
+    def kernels(self):
+        """Per world, the device kernel that solved the last step:
+        'none' | 'dense' | 'supernodal' | 'cr'."""
+        self._ensure()
+        out = np.zeros(max(1, self.n_worlds), np.int32)
+        _check(lib().kd_batch_get_kernels(self.handle, _capi.i32ptr(out)))
+        return [_capi.KERNEL_NAMES[int(k)] for k in out[: self.n_worlds]]
 
     def phase_cycles(self):
         """clock64 cycles per fused-kernel phase of the last step, [n_worlds, 8]."""
