@@ -275,9 +275,10 @@ int kd_batch_get_kernels(kd_batch* batch, int32_t* out);
 /* Supernodal sparse-LLT plan of a model (the factorization the device uses for
  * the reference's Dense backend, DenseDelassus delassus.cpp:59-65, on models
  * whose static row-capacity pattern admits one).  stats[0..11] = slots S,
- * nnz(L), per-world fp64 array length, supernodes, solve levels, factor
- * levels, factor FMA terms, solve FMA terms per PADMM iteration, dense-LLT
- * terms S^3/6, factor critical path, solve critical path, solve phases.
+ * nnz(L), per-world fp64 array length, supernodes, solve levels, solve
+ * program words, factor FMAs, solve FMA terms per PADMM iteration, dense-LLT
+ * FMAs S^3/6, per-world shared-memory doubles, solve critical path (terms on
+ * the busiest lane, summed over phases), solve phases.
  * Returns KD_ERR_INVALID_ARGUMENT with the reason if the model has no plan. */
 int kd_model_sparse_plan_info(const kd_model* model, int64_t* stats12);
 /* Host self-test of the plan (no device): a random SPD system with the plan's

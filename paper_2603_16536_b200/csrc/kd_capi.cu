@@ -90,7 +90,7 @@ struct kd_batch {
   Bin global_bin, cr_auto_bin, cr_all_bin;
   // supernodal sparse-LLT bins: one per planned model (worlds of one model per CTA)
   struct SnBin {
-    int model = 0, per_warp = 0, wpc = 1;
+    int model = 0, per_warp = 0, wpc = 1, prog_words = 0;
     Bin bin;
   };
   std::vector<SnBin> sn_bins;
@@ -164,8 +164,8 @@ int kd_model_sparse_plan_info(const kd_model* mp, int64_t* st) {
   if (!mp || !st) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   if (!mp->m.sn) return fail(KD_ERR_INVALID_ARGUMENT, "model has no sparse plan: " + mp->m.sn_why);
   const SnPlanHost& p = *mp->m.sn;
-  const int64_t v[12] = {p.S, p.nnzL, p.nLv, p.n_super, p.s_levels, (int64_t)p.fphase.size(), p.factor_terms,
-                         p.solve_terms, p.dense_factor_terms, p.factor_crit, p.solve_crit, (int64_t)p.sphase.size()};
+  const int64_t v[12] = {p.S, p.nnzL, p.nLv, (int64_t)p.sup.size(), p.s_levels, (int64_t)p.prog.size(),
+                         p.factor_fma, p.solve_terms, p.dense_factor_fma, p.smem_doubles, p.solve_crit, p.n_sph};
   for (int k = 0; k < 12; ++k) st[k] = v[k];
   return KD_OK;
 }
@@ -324,7 +324,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     d.joint_off = (int)joints.size();
     d.geom_off = (int)geoms.size();
     d.pair_off = (int)pairs.size();
-    d.sn = (b->sparse && m.sn && (size_t)m.sn->smem_doubles * 8 <= kSnMaxSmem) ? 1 : 0;
+    d.sn = (b->sparse && m.sn &&
+            (size_t)m.sn->smem_doubles * 8 + (((size_t)m.sn->prog.size() * 4 + 15) & ~(size_t)15) <= kSnMaxSmem)
+               ? 1 : 0;
     for (int k = 0; k < 3; ++k) d.gravity[k] = m.gravity[k];
     bodies.insert(bodies.end(), m.bodies.begin(), m.bodies.end());
     joints.insert(joints.end(), m.joints.begin(), m.joints.end());
@@ -406,7 +408,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     kd_batch::SnBin sbn;
     sbn.model = i;
     sbn.per_warp = b->models[i].sn->smem_doubles;
-    sbn.wpc = (int)std::max<size_t>(1, std::min<size_t>(8, kSnMaxSmem / (8 * (size_t)sbn.per_warp)));
+    sbn.prog_words = (int)b->models[i].sn->prog.size();
+    const size_t prog_bytes = ((size_t)sbn.prog_words * 4 + 15) & ~(size_t)15;
+    sbn.wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (kSnMaxSmem - prog_bytes) / (8 * (size_t)sbn.per_warp)));
     for (int w = 0; w < n_worlds; ++w)
       if (world_model[w] == i) sbn.bin.worlds.push_back(w);
     if (!sbn.bin.worlds.empty()) b->sn_bins.push_back(sbn);
@@ -509,10 +513,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
   {  // supernodal plans, concatenated over models with relocated offsets
     std::vector<DevSnPlan> dp(n_models);
     std::vector<SnGram> gram;
-    std::vector<SnOp> fops;
-    std::vector<uint32_t> fterms, sterms;
-    std::vector<SnSOp> sops;
-    std::vector<SnPhase> phases;
+    std::vector<SnSuper> sups;
+    std::vector<uint32_t> tmap, prog;
     std::vector<int32_t> pslot;
     std::vector<uint16_t> spos;
     for (int i = 0; i < n_models; ++i) {
@@ -525,6 +527,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       d.n_jd = p.n_jd;
       d.lim_base = p.lim_base;
       d.smem_doubles = p.smem_doubles;
+      d.max_slots = p.max_slots;
+      d.n_sph = p.n_sph;
       d.gram_off = (int)gram.size();
       d.n_gram = (int)p.gram.size();
       gram.insert(gram.end(), p.gram.begin(), p.gram.end());
@@ -532,30 +536,18 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       pslot.insert(pslot.end(), p.pair_slot.begin(), p.pair_slot.end());
       d.slotpos_off = (int)spos.size();
       spos.insert(spos.end(), p.slot_pos.begin(), p.slot_pos.end());
-      const uint32_t fto = (uint32_t)fterms.size(), sto = (uint32_t)sterms.size();
-      const int fo = (int)fops.size(), so = (int)sops.size();
-      for (SnOp o : p.fops) {
-        o.toff += fto;
-        fops.push_back(o);
+      d.sup_off = (int)sups.size();
+      d.n_sup = (int)p.sup.size();
+      const int to = (int)tmap.size();
+      for (SnSuper u : p.sup) {
+        u.tmap_off += to;
+        sups.push_back(u);
       }
-      for (SnSOp o : p.sops) {
-        o.toff += sto;
-        sops.push_back(o);
-      }
-      fterms.insert(fterms.end(), p.fterms.begin(), p.fterms.end());
-      sterms.insert(sterms.end(), p.sterms.begin(), p.sterms.end());
-      d.fph_off = (int)phases.size();
-      d.n_fph = (int)p.fphase.size();
-      for (SnPhase q : p.fphase) {
-        q.off += fo;
-        phases.push_back(q);
-      }
-      d.sph_off = (int)phases.size();
-      d.n_sph = (int)p.sphase.size();
-      for (SnPhase q : p.sphase) {
-        q.off += so;
-        phases.push_back(q);
-      }
+      tmap.insert(tmap.end(), p.tmap.begin(), p.tmap.end());
+      while (prog.size() & 3) prog.push_back(0);  // 16-byte aligned blobs
+      d.prog_off = (int)prog.size();
+      d.prog_words = (int)p.prog.size();
+      prog.insert(prog.end(), p.prog.begin(), p.prog.end());
     }
     auto up = [&](auto*& dst, const auto& vec) -> cudaError_t {
       using T = typename std::remove_reference<decltype(vec)>::type::value_type;
@@ -567,11 +559,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     };
     KD_CK(up(v.snplan, dp));
     KD_CK(up(v.sn_gram, gram));
-    KD_CK(up(v.sn_fops, fops));
-    KD_CK(up(v.sn_fterms, fterms));
-    KD_CK(up(v.sn_sops, sops));
-    KD_CK(up(v.sn_sterms, sterms));
-    KD_CK(up(v.sn_phases, phases));
+    KD_CK(up(v.sn_sup, sups));
+    KD_CK(up(v.sn_tmap, tmap));
+    KD_CK(up(v.sn_prog, prog));
     KD_CK(up(v.sn_pair_slot, pslot));
     KD_CK(up(v.sn_slot_pos, spos));
   }
@@ -717,7 +707,7 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
     mark(1);
     if (c->backend != KD_BACKEND_MATRIX_FREE) {
       for (const auto& sbn : b->sn_bins) {
-        KD_CK(launch_sparse(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.per_warp, sbn.wpc, s));
+        KD_CK(launch_sparse(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.per_warp, sbn.wpc, sbn.prog_words, s));
         ++b->launches;
       }
       for (const Bin& bin : b->dense_bins) {

@@ -40,7 +40,7 @@ cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_
 cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
                int nt, cudaStream_t s);
 cudaError_t launch_sparse(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int per_warp,
-                          int wpc, cudaStream_t s);
+                          int wpc, int prog_words, cudaStream_t s);
 void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s);
 size_t dense_smem_bytes(int n, int nt, bool global_l);
 size_t dense_factor_doubles(int n);

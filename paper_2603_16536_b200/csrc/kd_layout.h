@@ -83,23 +83,30 @@ enum SnGramFlags : uint16_t {
   SG_S2 = 16,  // sides for the second shared body
   SG_T2 = 32,
 };
-enum SnOpKind : uint16_t { SN_NOP = 0, SN_OFF = 1, SN_DIAG = 2 };
-struct SnOp {  // factor op: acc = Lv[dst] - sum Lv[a] Lv[b]; OFF: *Lv[aux]; DIAG: rsqrt
-  uint16_t dst, aux, nterm, kind;
-  uint32_t toff, pad;
+// One supernode: columns [c0, c0+w) of the factor in elimination order, with
+// m rows below the diagonal block.  Its dense panel ((w+m) x w, column-major,
+// odd column stride ld) lives at Lv[pb]; rows 0..w-1 are the supernode's own
+// positions, rows w.. its row structure.  X = L_SS^-1 (w x w, row stride ws)
+// lives at Lv[xb]; X's diagonal holds 1/L_jj.  The right-looking update of the
+// ancestors reads m(m+1)/2 target entries at tmap[tmap_off..]:
+// Lv index | ri << 16 | rj << 24.
+struct SnSuper {
+  int32_t c0, w, m, ld;
+  int32_t pb, xb, ws, tmap_off;
 };
-struct SnSOp {  // solve op (dst == 0xffff: no-op)
-  uint16_t dst, nterm;
-  uint32_t toff;
-};
-struct SnPhase {
-  int32_t off, steps, mode, pad;  // ops at off + step * 32 + lane; mode 0 = A, 1 = B
-};
+// Solve program (one u32 blob per model, copied to shared memory per CTA):
+//   phase (4 words): rec0 (word offset of its records), nsteps, mode, split
+//   record (2 words): dst | nterm << 16 ;  toff (word offset of the chunk's
+//     terms) | npart << 24 | owner << 30 | valid << 31
+//   term (1 word): Lv index | vector index << 16
+// mode 0 (A): t[dst] = v[dst] - sum Lv[a] v[b];  mode 1 (B): v[dst] = sum Lv[a] t[b].
+// A row's terms may be split over consecutive slots (chunks); its first chunk
+// (owner) adds the others' partial sums in slot order after a __syncwarp.
 struct DevSnPlan {
   int32_t S, nLv, n_jd, lim_base;
   int32_t gram_off, n_gram, pair_off, slotpos_off;
-  int32_t fph_off, n_fph, sph_off, n_sph;
-  int32_t smem_doubles, pad0, pad1, pad2;  // per-warp shared-memory footprint
+  int32_t sup_off, n_sup, prog_off, prog_words;
+  int32_t n_sph, max_slots, smem_doubles, pad0;  // smem_doubles: per-warp footprint
 };
 
 // Per-world indexing (prefix sums over model capacities).
@@ -207,11 +214,9 @@ struct BatchView {
   // supernodal plans (indexed by model; S == 0: none)
   const DevSnPlan* snplan;
   const SnGram* sn_gram;
-  const SnOp* sn_fops;
-  const uint32_t* sn_fterms;
-  const SnSOp* sn_sops;
-  const uint32_t* sn_sterms;
-  const SnPhase* sn_phases;
+  const SnSuper* sn_sup;
+  const uint32_t* sn_tmap;
+  const uint32_t* sn_prog;
   const int32_t* sn_pair_slot;
   const uint16_t* sn_slot_pos;
 };

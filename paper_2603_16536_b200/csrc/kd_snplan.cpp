@@ -8,9 +8,9 @@
 //      postorder so fundamental supernodes are contiguous;
 //   3. symbolic factor (column structures), fundamental supernodes, and the
 //      supernode level of each block for the triangular solves;
-//   4. instruction streams: factor (scalar left-looking Cholesky entries plus
-//      the inverse of every supernode's diagonal block), forward/backward solve
-//      phases; each level packed onto 32 lanes.
+//   4. per-world array layout (one dense panel per supernode + the inverse of
+//      its diagonal block), the ancestor-update target maps of the panel
+//      factor, and the chunked forward/backward solve program.
 #include "kd_snplan.h"
 
 #include <algorithm>
@@ -52,33 +52,6 @@ void symbolic(const BitMat& A, std::vector<std::vector<int>>& cs) {
         if (y != x) rx[y >> 6] |= 1ull << (y & 63);
     }
   }
-}
-
-// Longest-processing-time packing of one level's ops onto 32 lanes, laid out
-// [step][lane]; returns the step count and the heaviest lane's cost.
-template <class Op>
-void pack_level(const std::vector<Op>& ops, const std::vector<int>& cost, const Op& nop, std::vector<Op>& out,
-                int& steps, int& crit) {
-  std::vector<int> idx(ops.size());
-  std::iota(idx.begin(), idx.end(), 0);
-  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  std::vector<std::vector<int>> lanes(32);
-  std::vector<int64_t> load(32, 0);
-  for (int i : idx) {
-    int l = 0;
-    for (int k = 1; k < 32; ++k)
-      if (load[k] < load[l]) l = k;
-    lanes[l].push_back(i);
-    load[l] += cost[i];
-  }
-  steps = 0;
-  crit = 0;
-  for (int l = 0; l < 32; ++l) {
-    steps = std::max(steps, (int)lanes[l].size());
-    crit = std::max<int>(crit, (int)load[l]);
-  }
-  for (int s = 0; s < steps; ++s)
-    for (int l = 0; l < 32; ++l) out.push_back(s < (int)lanes[l].size() ? ops[lanes[l][s]] : nop);
 }
 
 }  // namespace
@@ -241,7 +214,6 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
   }
   sn_start.push_back(S);
   const int K = (int)sn_start.size() - 1;
-  p.n_super = K;
   std::vector<int> snid(S);
   for (int k = 0; k < K; ++k)
     for (int j = sn_start[k]; j < sn_start[k + 1]; ++j) snid[j] = k;
@@ -249,32 +221,69 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
   std::vector<std::vector<int>> rp(S);
   for (int j = 0; j < S; ++j)
     for (int i : cs[j]) rp[i].push_back(j);
-  // ---- Lv layout
-  std::vector<int32_t> Lidx((size_t)S * S, -1), Xidx;
-  std::vector<int> rpos(S);
+  // ---- Lv layout: one dense panel per supernode, then the X blocks
+  std::vector<int32_t> Lidx((size_t)S * S, -1);
   int nLv = 0;
-  for (int j = 0; j < S; ++j) {
-    rpos[j] = nLv++;
-    for (int i : cs[j]) Lidx[(size_t)i * S + j] = nLv++;
-  }
-  p.nnzL = nLv;
-  Xidx.assign((size_t)S * S, -1);
-  for (int k = 0; k < K; ++k)
-    for (int j = sn_start[k]; j < sn_start[k + 1]; ++j) {
-      Xidx[(size_t)j * S + j] = rpos[j];
-      for (int i = j + 1; i < sn_start[k + 1]; ++i) Xidx[(size_t)i * S + j] = nLv++;
+  p.sup.resize(K);
+  std::vector<int> qpos(S, -1);
+  for (int k = 0; k < K; ++k) {
+    SnSuper& u = p.sup[k];
+    const int c0 = sn_start[k], c1 = sn_start[k + 1];
+    std::vector<int> R;
+    for (int i : cs[c1 - 1]) R.push_back(i);
+    u.c0 = c0;
+    u.w = c1 - c0;
+    u.m = (int)R.size();
+    u.ld = (u.w + u.m) | 1;
+    u.pb = nLv;
+    nLv += u.ld * u.w;
+    if (u.m > 255 || u.w > 32) {
+      why = "supernode too large";
+      return false;
     }
+    for (int q = 0; q < u.w; ++q) qpos[c0 + q] = q;
+    for (int q = 0; q < u.m; ++q) qpos[R[q]] = u.w + q;
+    for (int j = c0; j < c1; ++j) {
+      Lidx[(size_t)j * S + j] = u.pb + (j - c0) * u.ld + (j - c0);
+      for (int i : cs[j]) Lidx[(size_t)i * S + j] = u.pb + (j - c0) * u.ld + qpos[i];
+    }
+    for (int q = 0; q < u.w; ++q) qpos[c0 + q] = -1;
+    for (int q = 0; q < u.m; ++q) qpos[R[q]] = -1;
+    p.nnzL += u.w * (u.w + 1) / 2 + u.w * u.m;
+  }
+  for (int k = 0; k < K; ++k) {  // X = L_SS^-1 lives (transposed) in the panel's unused upper triangle
+    SnSuper& u = p.sup[k];
+    u.ws = u.ld;
+    u.xb = u.pb;
+  }
   if (nLv >= 65535) {
     why = "factor too large for 16-bit indices";
     return false;
   }
   p.nLv = nLv;
-  {  // per-warp shared memory of kd_sparse.cu: Lv | v t | 8 PADMM vectors | 2 int16 maps
-    const int Sp = (S + 1) & ~1;
-    p.smem_doubles = ((nLv + 1) & ~1) + 10 * Sp + (Sp + 1) / 2 + 1;
-  }
   auto L = [&](int i, int j) { return Lidx[(size_t)i * S + j]; };
-  auto X = [&](int i, int j) { return Xidx[(size_t)i * S + j]; };
+  auto X = [&](int i, int j) {  // i >= j, same supernode
+    const SnSuper& u = p.sup[snid[j]];
+    return u.xb + (i - u.c0) * u.ws + (j - u.c0);
+  };
+  // ---- ancestor-update target maps
+  for (int k = 0; k < K; ++k) {
+    SnSuper& u = p.sup[k];
+    u.tmap_off = (int)p.tmap.size();
+    const int c1 = u.c0 + u.w;
+    const std::vector<int>& R = cs[c1 - 1];
+    for (int ri = 0; ri < u.m; ++ri)
+      for (int rj = 0; rj <= ri; ++rj) {
+        const int idx = L(R[ri], R[rj]);
+        if (idx < 0) {
+          why = "symbolic factor inconsistent";
+          return false;
+        }
+        p.tmap.push_back((uint32_t)idx | ((uint32_t)ri << 16) | ((uint32_t)rj << 24));
+      }
+    p.factor_fma += (int64_t)u.m * (u.m + 1) / 2 * u.w + (int64_t)(u.w + u.m) * u.w * u.w / 2;
+  }
+  p.dense_factor_fma = (int64_t)S * S * S / 6;
   // ---- Gram entries (slot order, s >= t)
   for (int s = 0; s < S; ++s)
     for (int t = 0; t <= s; ++t) {
@@ -289,7 +298,7 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       if (ns == 0) continue;
       SnGram g{};
       const int ps = p.slot_pos[s], pt = p.slot_pos[t];
-      g.dst = (uint16_t)(s == t ? rpos[ps] : L(std::max(ps, pt), std::min(ps, pt)));
+      g.dst = (uint16_t)L(std::max(ps, pt), std::min(ps, pt));
       g.s = (uint16_t)s;
       g.t = (uint16_t)t;
       uint16_t f = s == t ? SG_DIAG : 0;
@@ -303,144 +312,228 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       g.flags = f;
       p.gram.push_back(g);
     }
-  // ---- factor program, level-scheduled
-  {
-    std::vector<int> ready(nLv, 0);
-    struct Pending {
-      SnOp op;
-      std::vector<uint32_t> terms;
-    };
-    std::vector<std::vector<Pending>> levels;
-    auto add = [&](uint16_t kind, int dst, int aux, std::vector<uint32_t>&& terms) {
-      int lv = ready[dst];
-      if (kind == SN_OFF) lv = std::max(lv, ready[aux]);
-      for (uint32_t t : terms) lv = std::max({lv, ready[t & 0xffff], ready[t >> 16]});
-      ++lv;
-      ready[dst] = lv;
-      if ((int)levels.size() < lv) levels.resize(lv);
-      p.factor_terms += (int64_t)terms.size();
-      Pending pd;
-      pd.op = SnOp{(uint16_t)dst, (uint16_t)aux, (uint16_t)terms.size(), kind, 0, 0};
-      pd.terms = std::move(terms);
-      levels[lv - 1].push_back(std::move(pd));
-    };
-    for (int j = 0; j < S; ++j) {
-      std::vector<uint32_t> t;
-      for (int k : rp[j]) t.push_back((uint32_t)L(j, k) | ((uint32_t)L(j, k) << 16));
-      add(SN_DIAG, rpos[j], rpos[j], std::move(t));
-      for (int i : cs[j]) {
-        std::vector<uint32_t> u;
-        size_t a = 0, b = 0;
-        while (a < rp[i].size() && b < rp[j].size()) {  // common k < j, ascending
-          if (rp[i][a] == rp[j][b]) {
-            u.push_back((uint32_t)L(i, rp[i][a]) | ((uint32_t)L(j, rp[j][b]) << 16));
-            ++a;
-            ++b;
-          } else if (rp[i][a] < rp[j][b]) {
-            ++a;
-          } else {
-            ++b;
-          }
-        }
-        add(SN_OFF, L(i, j), rpos[j], std::move(u));
+  // ---- solve program over supernode levels
+  std::vector<int> slev(K, 0);
+  for (int k = 0; k < K; ++k)
+    for (int j = sn_start[k]; j < sn_start[k + 1]; ++j)
+      for (int i : cs[j])
+        if (snid[i] != k) slev[snid[i]] = std::max(slev[snid[i]], slev[k] + 1);
+  const int H = K ? *std::max_element(slev.begin(), slev.end()) + 1 : 0;
+  p.s_levels = H;
+  struct Row {
+    int dst;
+    std::vector<uint32_t> terms;
+  };
+  struct PhaseBuild {
+    int mode;
+    std::vector<Row> rows;
+  };
+  std::vector<PhaseBuild> phases;
+  auto term = [](int a, int v) { return (uint32_t)a | ((uint32_t)v << 16); };
+  for (int lv = 0; lv < H; ++lv) {  // forward: L y = b
+    PhaseBuild A{0, {}}, B{1, {}};
+    for (int k = 0; k < K; ++k) {
+      if (slev[k] != lv) continue;
+      const int c0 = sn_start[k], c1 = sn_start[k + 1];
+      for (int i = c0; i < c1; ++i) {
+        Row a{i, {}}, b{i, {}};
+        for (int j : rp[i])
+          if (j < c0) a.terms.push_back(term(L(i, j), j));
+        for (int q = c0; q <= i; ++q) b.terms.push_back(term(X(i, q), q));
+        A.rows.push_back(std::move(a));
+        B.rows.push_back(std::move(b));
       }
     }
-    for (int k = 0; k < K; ++k)
-      for (int j = sn_start[k]; j < sn_start[k + 1]; ++j)
-        for (int i = j + 1; i < sn_start[k + 1]; ++i) {
-          std::vector<uint32_t> t;
-          for (int q = j; q < i; ++q) t.push_back((uint32_t)L(i, q) | ((uint32_t)X(q, j) << 16));
-          add(SN_OFF, X(i, j), rpos[i], std::move(t));
-        }
-    const SnOp nop{0, 0, 0, SN_NOP, 0, 0};
-    for (auto& lvl : levels) {
-      std::vector<SnOp> ops;
-      std::vector<int> cost;
-      for (auto& pd : lvl) {
-        SnOp o = pd.op;
-        o.toff = (uint32_t)p.fterms.size();
-        p.fterms.insert(p.fterms.end(), pd.terms.begin(), pd.terms.end());
-        ops.push_back(o);
-        cost.push_back(2 + (int)pd.terms.size());
+    phases.push_back(std::move(A));
+    phases.push_back(std::move(B));
+  }
+  for (int lv = H - 1; lv >= 0; --lv) {  // backward: L^T x = y
+    PhaseBuild A{0, {}}, B{1, {}};
+    for (int k = 0; k < K; ++k) {
+      if (slev[k] != lv) continue;
+      const int c0 = sn_start[k], c1 = sn_start[k + 1];
+      for (int j = c0; j < c1; ++j) {
+        Row a{j, {}}, b{j, {}};
+        for (int i : cs[j])
+          if (i >= c1) a.terms.push_back(term(L(i, j), i));
+        for (int q = j; q < c1; ++q) b.terms.push_back(term(X(q, j), q));
+        A.rows.push_back(std::move(a));
+        B.rows.push_back(std::move(b));
       }
-      SnPhase ph{(int32_t)p.fops.size(), 0, 0, 0};
-      int crit = 0;
-      pack_level(ops, cost, nop, p.fops, ph.steps, crit);
-      p.factor_crit += crit;
-      p.fphase.push_back(ph);
+    }
+    phases.push_back(std::move(A));
+    phases.push_back(std::move(B));
+  }
+  // blob: phase table, then records, then terms
+  std::vector<uint32_t>& blob = p.prog;
+  const int nph = (int)phases.size();
+  p.n_sph = nph;
+  blob.assign(4 * nph, 0);
+  std::vector<uint32_t> terms_all;
+  struct Rec {
+    uint32_t w0, toff, flags;
+  };
+  std::vector<std::vector<Rec>> recs(nph);
+  std::vector<std::vector<std::vector<uint32_t>>> rec_terms(nph);
+  for (int ph = 0; ph < nph; ++ph) {
+    const PhaseBuild& P = phases[ph];
+    int maxn = 1;
+    for (const Row& r : P.rows) maxn = std::max(maxn, (int)r.terms.size());
+    // chunk size: minimise an issue-cost estimate (steps x chunk length, plus
+    // the combine pass when any row is split)
+    int bestC = maxn, bestSlots = 0;
+    double bestCost = 1e30;
+    for (int C = 1; C <= maxn; ++C) {
+      int slots = 0;
+      bool split = false;
+      for (const Row& r : P.rows) {
+        const int ch = std::max(1, ((int)r.terms.size() + C - 1) / C);
+        slots += ch;
+        split |= ch > 1;
+      }
+      const int steps = (slots + 31) / 32;
+      const double cost = steps * (4.0 * C + 24.0) + (split ? 60.0 : 0.0);
+      if (cost < bestCost || (cost == bestCost && C > bestC)) {
+        bestCost = cost;
+        bestC = C;
+        bestSlots = slots;
+      }
+    }
+    const int C = bestC;
+    const int steps = (bestSlots + 31) / 32;
+    bool split = false;
+    int crit = 0;
+    std::vector<int> lane_load(32, 0);
+    recs[ph].assign(32 * std::max(steps, 0), Rec{0, 0, 0});
+    rec_terms[ph].assign(recs[ph].size(), {});
+    int slot = 0;
+    for (const Row& r : P.rows) {
+      const int n = (int)r.terms.size();
+      const int ch = std::max(1, (n + C - 1) / C);
+      split |= ch > 1;
+      for (int c = 0; c < ch; ++c) {
+        const int b0 = c * C, b1 = std::min(n, b0 + C);
+        Rec& rc = recs[ph][slot];
+        rc.w0 = (uint32_t)r.dst | ((uint32_t)(b1 - b0) << 16);
+        rc.flags = (1u << 31) | (c == 0 ? (1u << 30) | ((uint32_t)(ch - 1) << 24) : 0u);
+        rec_terms[ph][slot].assign(r.terms.begin() + b0, r.terms.begin() + b1);
+        lane_load[slot & 31] += b1 - b0;
+        p.solve_terms += b1 - b0;
+        ++slot;
+      }
+    }
+    for (int l = 0; l < 32; ++l) crit = std::max(crit, lane_load[l]);
+    p.solve_crit += crit;
+    p.max_slots = std::max(p.max_slots, 32 * steps);
+    blob[4 * ph + 1] = (uint32_t)steps;
+    blob[4 * ph + 2] = (uint32_t)P.mode;
+    blob[4 * ph + 3] = split ? 1u : 0u;
+  }
+  for (int ph = 0; ph < nph; ++ph) {  // records (8-byte aligned)
+    if (blob.size() & 1) blob.push_back(0);
+    blob[4 * ph] = (uint32_t)blob.size();
+    for (size_t r = 0; r < recs[ph].size(); ++r) {
+      blob.push_back(recs[ph][r].w0);
+      blob.push_back(0);  // patched with the term offset below
     }
   }
-  // dense LLT of the capacity system, for the statistics
-  p.dense_factor_terms = (int64_t)S * S * S / 6;
-  // ---- solve program over supernode levels
-  {
-    std::vector<int> slev(K, 0);
-    for (int k = 0; k < K; ++k)
-      for (int j = sn_start[k]; j < sn_start[k + 1]; ++j)
-        for (int i : cs[j])
-          if (snid[i] != k) slev[snid[i]] = std::max(slev[snid[i]], slev[k] + 1);
-    const int H = K ? *std::max_element(slev.begin(), slev.end()) + 1 : 0;
-    p.s_levels = H;
-    const SnSOp nop{0xffff, 0, 0};
-    auto emit_phase = [&](int mode, std::vector<std::pair<int, std::vector<uint32_t>>>& rows) {
-      std::vector<SnSOp> ops;
-      std::vector<int> cost;
-      for (auto& r : rows) {
-        ops.push_back(SnSOp{(uint16_t)r.first, (uint16_t)r.second.size(), (uint32_t)p.sterms.size()});
-        p.sterms.insert(p.sterms.end(), r.second.begin(), r.second.end());
-        cost.push_back(2 + (int)r.second.size());
-        p.solve_terms += (int64_t)r.second.size();
+  for (int ph = 0; ph < nph; ++ph)
+    for (size_t r = 0; r < recs[ph].size(); ++r) {
+      const uint32_t toff = (uint32_t)blob.size();
+      blob.insert(blob.end(), rec_terms[ph][r].begin(), rec_terms[ph][r].end());
+      if (toff >= (1u << 24)) {
+        why = "solve program too large";
+        return false;
       }
-      SnPhase ph{(int32_t)p.sops.size(), 0, mode, 0};
-      int crit = 0;
-      pack_level(ops, cost, nop, p.sops, ph.steps, crit);
-      p.solve_crit += crit;
-      p.sphase.push_back(ph);
-    };
-    auto term = [](int a, int v) { return (uint32_t)a | ((uint32_t)v << 16); };
-    for (int lv = 0; lv < H; ++lv) {  // forward: L y = b
-      std::vector<std::pair<int, std::vector<uint32_t>>> A_, B_;
-      for (int k = 0; k < K; ++k) {
-        if (slev[k] != lv) continue;
-        const int c0 = sn_start[k], c1 = sn_start[k + 1];
-        for (int i = c0; i < c1; ++i) {
-          std::vector<uint32_t> t;
-          for (int j : rp[i])
-            if (j < c0) t.push_back(term(L(i, j), j));
-          A_.push_back({i, std::move(t)});
-          std::vector<uint32_t> u;
-          for (int q = c0; q <= i; ++q) u.push_back(term(X(i, q), q));
-          B_.push_back({i, std::move(u)});
-        }
-      }
-      emit_phase(0, A_);
-      emit_phase(1, B_);
+      blob[blob[4 * ph] + 2 * r + 1] = toff | recs[ph][r].flags;
     }
-    for (int lv = H - 1; lv >= 0; --lv) {  // backward: L^T x = y
-      std::vector<std::pair<int, std::vector<uint32_t>>> A_, B_;
-      for (int k = 0; k < K; ++k) {
-        if (slev[k] != lv) continue;
-        const int c0 = sn_start[k], c1 = sn_start[k + 1];
-        for (int j = c0; j < c1; ++j) {
-          std::vector<uint32_t> t;
-          for (int i : cs[j])
-            if (i >= c1) t.push_back(term(L(i, j), i));
-          A_.push_back({j, std::move(t)});
-          std::vector<uint32_t> u;
-          for (int q = j; q < c1; ++q) u.push_back(term(X(q, j), q));
-          B_.push_back({j, std::move(u)});
-        }
-      }
-      emit_phase(0, A_);
-      emit_phase(1, B_);
-    }
+  {  // per-warp shared memory of kd_sparse.cu: Lv | v t | 5 PADMM vectors | partials | 2 int16 maps
+    const int Sp = (S + 1) & ~1;
+    p.smem_doubles = ((nLv + 1) & ~1) + 7 * Sp + p.max_slots + (Sp + 1) / 2 + 1;
   }
   return true;
 }
 
+namespace {
+
+// The device algorithms of kd_sparse.cu on the host (self-test).
+bool cpu_factor(const SnPlanHost& p, std::vector<double>& Lv) {
+  bool ok = true;
+  for (const SnSuper& u : p.sup) {
+    double* P = Lv.data() + u.pb;
+    double* X = Lv.data() + u.xb;
+    for (int c = 0; c < u.w; ++c) {
+      const double d = P[c * u.ld + c];
+      if (!(d > 0.0)) ok = false;
+      const double r = 1.0 / std::sqrt(d);
+      for (int q = c + 1; q < u.w + u.m; ++q) P[c * u.ld + q] *= r;
+      X[c * u.ws + c] = r;  // the diagonal keeps 1/L_cc (L_cc itself is never read again)
+      for (int q = c + 1; q < u.w + u.m; ++q) {
+        const double lq = P[c * u.ld + q];
+        for (int j = c + 1; j <= std::min(q, u.w - 1); ++j) P[j * u.ld + q] -= lq * P[c * u.ld + j];
+      }
+    }
+    for (int j = 0; j < u.w; ++j)
+      for (int i = j + 1; i < u.w; ++i) {
+        double s = 0.0;
+        for (int q = j; q < i; ++q) s += P[q * u.ld + i] * X[q * u.ws + j];
+        X[i * u.ws + j] = -s * X[i * u.ws + i];
+      }
+    const int T = u.m * (u.m + 1) / 2;
+    for (int e = 0; e < T; ++e) {
+      const uint32_t te = p.tmap[u.tmap_off + e];
+      const int ri = (te >> 16) & 0xff, rj = te >> 24;
+      double s = 0.0;
+      for (int c = 0; c < u.w; ++c) s += P[c * u.ld + u.w + ri] * P[c * u.ld + u.w + rj];
+      Lv[te & 0xffff] -= s;
+    }
+  }
+  return ok;
+}
+
+void cpu_solve(const SnPlanHost& p, const std::vector<double>& Lv, std::vector<double>& v) {
+  const uint32_t* blob = p.prog.data();
+  std::vector<double> t(p.S, 0.0), part(std::max(1, p.max_slots), 0.0);
+  for (int ph = 0; ph < p.n_sph; ++ph) {
+    const uint32_t rec0 = blob[4 * ph], steps = blob[4 * ph + 1], mode = blob[4 * ph + 2];
+    auto finalize = [&](int dst, double s) {
+      if (mode == 0) t[dst] = v[dst] - s;
+      else v[dst] = s;
+    };
+    for (uint32_t slot = 0; slot < 32 * steps; ++slot) {
+      const uint32_t w0 = blob[rec0 + 2 * slot], w1 = blob[rec0 + 2 * slot + 1];
+      if (!(w1 >> 31)) continue;
+      const int dst = w0 & 0xffff, nt = w0 >> 16;
+      const uint32_t toff = w1 & 0xffffff;
+      double a0 = 0.0, a1 = 0.0;
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t tt = blob[toff + k];
+        const double prod = Lv[tt & 0xffff] * (mode == 0 ? v : t)[tt >> 16];
+        if (k & 1) a1 += prod;
+        else a0 += prod;
+      }
+      const double s = a0 + a1;
+      const bool owner = (w1 >> 30) & 1;
+      const int npart = (w1 >> 24) & 63;
+      if (owner && npart == 0) finalize(dst, s);
+      else part[slot] = s;
+    }
+    for (uint32_t slot = 0; slot < 32 * steps; ++slot) {
+      const uint32_t w0 = blob[rec0 + 2 * slot], w1 = blob[rec0 + 2 * slot + 1];
+      const int npart = (w1 >> 24) & 63;
+      if (!(w1 >> 31) || !((w1 >> 30) & 1) || npart == 0) continue;
+      double s = part[slot];
+      for (int q = 1; q <= npart; ++q) s += part[slot + q];
+      finalize(w0 & 0xffff, s);
+    }
+  }
+}
+
+}  // namespace
+
 bool sn_plan_cpu_solve(const SnPlanHost& p, const double* D, const uint8_t* active, const double* b, double* x) {
   const int S = p.S;
-  std::vector<double> Lv(p.nLv, 0.0), v(S, 0.0), t(S, 0.0);
+  std::vector<double> Lv(p.nLv, 0.0), v(S, 0.0);
   for (const SnGram& g : p.gram) {
     if (!active[g.s] || !active[g.t]) {
       if (g.flags & SG_DIAG) Lv[g.dst] = 1.0;
@@ -448,44 +541,9 @@ bool sn_plan_cpu_solve(const SnPlanHost& p, const double* D, const uint8_t* acti
     }
     Lv[g.dst] = D[(size_t)g.s * S + g.t];
   }
-  bool ok = true;
-  for (const SnPhase& ph : p.fphase)
-    for (int k = 0; k < 32 * ph.steps; ++k) {
-      const SnOp& o = p.fops[ph.off + k];
-      if (o.kind == SN_NOP) continue;
-      double acc = Lv[o.dst];
-      for (int q = 0; q < o.nterm; ++q) {
-        const uint32_t tt = p.fterms[o.toff + q];
-        acc -= Lv[tt & 0xffff] * Lv[tt >> 16];
-      }
-      if (o.kind == SN_DIAG) {
-        if (!(acc > 0.0)) ok = false;
-        Lv[o.dst] = 1.0 / std::sqrt(acc);
-      } else {
-        Lv[o.dst] = acc * Lv[o.aux];
-      }
-    }
+  const bool ok = cpu_factor(p, Lv);
   for (int s = 0; s < S; ++s) v[p.slot_pos[s]] = active[s] ? b[s] : 0.0;
-  for (const SnPhase& ph : p.sphase)
-    for (int k = 0; k < 32 * ph.steps; ++k) {
-      const SnSOp& o = p.sops[ph.off + k];
-      if (o.dst == 0xffff) continue;
-      if (ph.mode == 0) {
-        double acc = v[o.dst];
-        for (int q = 0; q < o.nterm; ++q) {
-          const uint32_t tt = p.sterms[o.toff + q];
-          acc -= Lv[tt & 0xffff] * v[tt >> 16];
-        }
-        t[o.dst] = acc;
-      } else {
-        double acc = 0.0;
-        for (int q = 0; q < o.nterm; ++q) {
-          const uint32_t tt = p.sterms[o.toff + q];
-          acc += Lv[tt & 0xffff] * t[tt >> 16];
-        }
-        v[o.dst] = acc;
-      }
-    }
+  cpu_solve(p, Lv, v);
   for (int s = 0; s < S; ++s) x[s] = v[p.slot_pos[s]];
   return ok;
 }

@@ -6,17 +6,17 @@
 //                   iteration                              (delassus.cpp:59-65)
 //   padmm_solve     De Saxce shift, solve, cone projection, dual update,
 //                   residual triple, Nesterov with restart (padmm.cpp:87-159)
-// but D is factored in a fill-reducing order using the model's static plan
+// but D is factored in the fill-reducing order of the model's static plan
 // (kd_snplan.h): for DR-Legs nnz(L) = 3.6k instead of n^2/2 = 24.6k and the
-// factor costs 34k FMA instead of 1.8M.  Everything a world needs (the factor
-// array Lv, the PADMM vectors) fits in ~53 KB of shared memory, so one warp owns
-// one world for the whole solve and a CTA holds several worlds of one model.
-// All synchronisation is __syncwarp: level-scheduled programs keep each level's
-// ops independent, and the plan was packed so the ops of a level are balanced
-// over the 32 lanes.
+// factor costs ~40k FMA instead of 1.8M.  Everything a world needs (panels,
+// X blocks, PADMM vectors) fits in ~55 KB of shared memory, so one warp owns
+// one world for the whole solve and a CTA holds several worlds of one model
+// plus one shared copy of the model's solve program.  After the program copy
+// (one __syncthreads) all synchronisation is __syncwarp.
 //
-// Per-warp shared memory (doubles):  Lv[nLv] | v[S] | t[S] | vf x y z yh zh yp zp [S each]
-//                                    | int16 row2pos[S] | int16 slot2row[S]
+// Shared memory: [solve program blob] then per warp (doubles):
+//   Lv[nLv] | v[S] | t[S] | vf y z yh zh [S each] | part[max_slots]
+//   | int16 row2pos[S] | int16 slot2row[S]
 #include "kd_device.cuh"
 
 namespace kd {
@@ -51,10 +51,20 @@ __device__ __forceinline__ int pad2(int x) { return (x + 1) & ~1; }
 }  // namespace
 
 __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams sp, const int32_t* worlds, int count,
-                                                     int per_warp) {
+                                                        int per_warp, int prog_words) {
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int slot_idx = blockIdx.x * (blockDim.x >> 5) + wid;
+  // the CTA's worlds share one model: stage its solve program once
+  uint32_t* prog = reinterpret_cast<uint32_t*>(smem);
+  {
+    const int w0 = worlds[blockIdx.x * (blockDim.x >> 5)];
+    const DevSnPlan P0 = bv.snplan[bv.worlds[w0].model];
+    const uint4* src = reinterpret_cast<const uint4*>(bv.sn_prog + P0.prog_off);
+    uint4* dst = reinterpret_cast<uint4*>(prog);
+    for (int i = threadIdx.x; i < (prog_words + 3) / 4; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
   if (slot_idx >= count) return;
   const int w = worlds[slot_idx];
   WorldStep& ws = bv.wstep[w];
@@ -63,18 +73,16 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   const DevSnPlan P = bv.snplan[W.model];
   const DevModel M = bv.models[W.model];
   const int S = P.S, Sp = pad2(S);
-  double* Lv = smem + (size_t)wid * per_warp;
+  double* Lv = smem + ((prog_words + 3) / 4) * 2 + (size_t)wid * per_warp;
   double* v = Lv + pad2(P.nLv);
   double* t = v + Sp;
   double* vf_s = t + Sp;
-  double* x_s = vf_s + Sp;
-  double* y_s = x_s + Sp;
+  double* y_s = vf_s + Sp;
   double* z_s = y_s + Sp;
   double* yh_s = z_s + Sp;
   double* zh_s = yh_s + Sp;
-  double* yp_s = zh_s + Sp;
-  double* zp_s = yp_s + Sp;
-  int16_t* row2pos = reinterpret_cast<int16_t*>(zp_s + Sp);
+  double* part = zh_s + Sp;
+  int16_t* row2pos = reinterpret_cast<int16_t*>(part + P.max_slots);
   int16_t* slot2row = row2pos + Sp;
 
   const int64_t R0 = W.row_off;
@@ -159,27 +167,61 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   __syncwarp();
   stamp(0);
 
-  // ---- 2. numeric factor + supernode diagonal-block inverses (level-scheduled)
+  // ---- 2. supernodal right-looking Cholesky (postorder; one warp, so every
+  // entry accumulates its updates in one fixed order) + X = L_SS^-1 per block
   {
     bool bad = false;
-    const SnPhase* ph = bv.sn_phases + P.fph_off;
-    for (int l = 0; l < P.n_fph; ++l) {
-      const SnPhase q = ph[l];
-      for (int st = 0; st < q.steps; ++st) {
-        const SnOp o = bv.sn_fops[q.off + 32 * st + lane];
-        if (o.kind == SN_NOP) continue;
-        const uint32_t* tm = bv.sn_fterms + o.toff;
-        double acc = Lv[o.dst];
-        for (int k = 0; k < o.nterm; ++k) {
-          const uint32_t tt = tm[k];
-          acc -= Lv[tt & 0xffff] * Lv[tt >> 16];
+    const SnSuper* sup = bv.sn_sup + P.sup_off;
+    for (int k = 0; k < P.n_sup; ++k) {
+      const SnSuper u = sup[k];
+      double* Pn = Lv + u.pb;
+      double* X = Lv + u.xb;
+      const int rows = u.w + u.m;
+      for (int c = 0; c < u.w; ++c) {
+        double* col = Pn + c * u.ld;
+        const double d = col[c];
+        if (!(d > 0.0)) bad = true;
+        const double r = rsqrt(d);
+        for (int q = c + 1 + lane; q < rows; q += 32) col[q] *= r;
+        __syncwarp();
+        if (lane == 0) X[c * u.ws + c] = r;  // X (= L_SS^-1, transposed into the upper triangle) keeps 1/L_cc
+        // trailing update of the panel's remaining columns
+        for (int q = c + 1 + lane; q < rows; q += 32) {
+          const double lq = col[q];
+          const int jmax = min(q, u.w - 1);
+          for (int j = c + 1; j <= jmax; ++j) Pn[j * u.ld + q] -= lq * col[j];
         }
-        if (o.kind == SN_DIAG) {
-          if (!(acc > 0.0)) bad = true;
-          Lv[o.dst] = rsqrt(acc);
-        } else {
-          Lv[o.dst] = acc * Lv[o.aux];
+        __syncwarp();
+      }
+      // X = L_SS^-1, lane j owns column j (X_ij = -(sum_{q=j}^{i-1} L_iq X_qj) / L_ii)
+      if (lane < u.w) {
+        const int j = lane;
+        for (int i = j + 1; i < u.w; ++i) {
+          double s0 = 0.0, s1 = 0.0;
+          int q = j;
+          for (; q + 1 < i; q += 2) {
+            s0 += Pn[q * u.ld + i] * X[q * u.ws + j];
+            s1 += Pn[(q + 1) * u.ld + i] * X[(q + 1) * u.ws + j];
+          }
+          if (q < i) s0 += Pn[q * u.ld + i] * X[q * u.ws + j];
+          X[i * u.ws + j] = -(s0 + s1) * X[i * u.ws + i];
         }
+      }
+      // ancestors: A_ij -= sum_c L_ic L_jc for i >= j in the row structure
+      const int T = u.m * (u.m + 1) / 2;
+      const uint32_t* tm = bv.sn_tmap + u.tmap_off;
+      for (int e = lane; e < T; e += 32) {
+        const uint32_t te = tm[e];
+        const double* a = Pn + u.w + ((te >> 16) & 0xff);
+        const double* b = Pn + u.w + (te >> 24);
+        double s0 = 0.0, s1 = 0.0;
+        int c = 0;
+        for (; c + 1 < u.w; c += 2) {
+          s0 += a[c * u.ld] * b[c * u.ld];
+          s1 += a[(c + 1) * u.ld] * b[(c + 1) * u.ld];
+        }
+        if (c < u.w) s0 += a[c * u.ld] * b[c * u.ld];
+        Lv[te & 0xffff] -= s0 + s1;
       }
       __syncwarp();
     }
@@ -190,7 +232,11 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   }
   stamp(2);
 
-  // ---- 3. PADMM (padmm.cpp:87-159); units = bilateral/limit rows and contact triples
+  // ---- 3. PADMM (padmm.cpp:87-159); units = bilateral/limit rows and contact triples.
+  // The solve result x stays in v (at the row's position) until the same lane
+  // overwrites it with the next right-hand side.  Nesterov's extrapolation is
+  // formed in the projection pass with the no-restart coefficient and undone
+  // in the rhs pass on a restart, so no previous-iterate vectors are kept.
   const int n_units = first_contact + nc;
   const double eta = sp.eta, rho = sp.rho;
   const double* rmu = bv.rmu + R0;
@@ -198,32 +244,27 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
     const bool con = u >= first_contact;
     const int r0 = con ? first_contact + 3 * (u - first_contact) : u;
     const int nr = con ? 3 : 1;
-    double x[3] = {0, 0, 0}, y[3] = {0, 0, 0};
-    
+    double x[3] = {0, 0, 0}, y[3] = {0, 0, 0}, zz[3] = {0, 0, 0};
 #pragma unroll
-      for (int d = 0; d < 3; ++d) if (d < nr) {
-      x[d] = bv.x0[R0 + r0 + d];
-      vf_s[r0 + d] = bv.vf[R0 + r0 + d];
-      const double z = bv.z0[R0 + r0 + d];
-      z_s[r0 + d] = z;
-      zh_s[r0 + d] = z;
-      x_s[r0 + d] = x[d];
-    }
+    for (int d = 0; d < 3; ++d)
+      if (d < nr) {
+        x[d] = bv.x0[R0 + r0 + d];
+        vf_s[r0 + d] = bv.vf[R0 + r0 + d];
+        zz[d] = bv.z0[R0 + r0 + d];
+        z_s[r0 + d] = zz[d];
+        zh_s[r0 + d] = zz[d];
+      }
     if (con) project_soc(x, rmu[r0], y);  // y = Pi_K(x0)
     else y[0] = u >= n_jd ? fmax(0.0, x[0]) : x[0];
-    
-#pragma unroll
-      for (int d = 0; d < 3; ++d) if (d < nr) {
-      y_s[r0 + d] = y[d];
-      yh_s[r0 + d] = y[d];
-    }
     // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
-    const double s0 = con ? rmu[r0] * hypot(zh_s[r0 + 1], zh_s[r0 + 2]) : 0.0;
-    
+    const double s0 = con ? rmu[r0] * hypot(zz[1], zz[2]) : 0.0;
 #pragma unroll
-      for (int d = 0; d < 3; ++d)
-        if (d < nr)
-      v[row2pos[r0 + d]] = -((((vf_s[r0 + d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * y[d]) - zh_s[r0 + d]);
+    for (int d = 0; d < 3; ++d)
+      if (d < nr) {
+        y_s[r0 + d] = y[d];
+        yh_s[r0 + d] = y[d];
+        v[row2pos[r0 + d]] = -((((vf_s[r0 + d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * y[d]) - zz[d]);
+      }
   }
   __syncwarp();
   double a = 1.0, prev = __longlong_as_double(0x7ff0000000000000ll);  // +inf
@@ -231,68 +272,85 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   int restarts = 0, it = 1;
   bool converged = false;
   const int hcap = bv.hist_cap;
-  const SnPhase* sph = bv.sn_phases + P.sph_off;
   for (it = 1; it <= sp.max_iters; ++it) {
-    // x = D^-1 rhs: forward then backward substitution (phase A / B per level)
+    // x = D^-1 rhs: forward then backward substitution, two phases per level
     for (int l = 0; l < P.n_sph; ++l) {
-      const SnPhase q = sph[l];
-      if (q.mode == 0) {
-        for (int st = 0; st < q.steps; ++st) {
-          const SnSOp o = bv.sn_sops[q.off + 32 * st + lane];
-          if (o.dst == 0xffff) continue;
-          const uint32_t* tm = bv.sn_sterms + o.toff;
-          double acc = v[o.dst];
-          for (int k = 0; k < o.nterm; ++k) {
-            const uint32_t tt = tm[k];
-            acc -= Lv[tt & 0xffff] * v[tt >> 16];
-          }
-          t[o.dst] = acc;
+      const uint4 ph = reinterpret_cast<const uint4*>(prog)[l];  // rec0, steps, mode, split
+      const bool modeA = ph.z == 0;
+      const double* src = modeA ? v : t;
+      for (uint32_t st = 0; st < ph.y; ++st) {
+        const int slot = 32 * st + lane;
+        const uint2 rc = reinterpret_cast<const uint2*>(prog + ph.x)[slot];
+        if (!(rc.y >> 31)) continue;
+        const int dst = rc.x & 0xffff, nt = rc.x >> 16;
+        const uint32_t* tm = prog + (rc.y & 0xffffff);
+        double a0 = 0.0, a1 = 0.0;
+        int k = 0;
+        for (; k + 1 < nt; k += 2) {
+          const uint32_t t0 = tm[k], t1 = tm[k + 1];
+          a0 += Lv[t0 & 0xffff] * src[t0 >> 16];
+          a1 += Lv[t1 & 0xffff] * src[t1 >> 16];
         }
-      } else {
-        for (int st = 0; st < q.steps; ++st) {
-          const SnSOp o = bv.sn_sops[q.off + 32 * st + lane];
-          if (o.dst == 0xffff) continue;
-          const uint32_t* tm = bv.sn_sterms + o.toff;
-          double acc = 0.0;
-          for (int k = 0; k < o.nterm; ++k) {
-            const uint32_t tt = tm[k];
-            acc += Lv[tt & 0xffff] * t[tt >> 16];
-          }
-          v[o.dst] = acc;
+        if (k < nt) {
+          const uint32_t t0 = tm[k];
+          a0 += Lv[t0 & 0xffff] * src[t0 >> 16];
+        }
+        const double sum = a0 + a1;
+        if (((rc.y >> 30) & 1) && ((rc.y >> 24) & 63) == 0) {
+          if (modeA) t[dst] = v[dst] - sum;
+          else v[dst] = sum;
+        } else {
+          part[slot] = sum;
+        }
+      }
+      if (ph.w) {  // owners add their rows' other chunks in slot order
+        __syncwarp();
+        for (uint32_t st = 0; st < ph.y; ++st) {
+          const int slot = 32 * st + lane;
+          const uint2 rc = reinterpret_cast<const uint2*>(prog + ph.x)[slot];
+          const int npart = (rc.y >> 24) & 63;
+          if (!(rc.y >> 31) || !((rc.y >> 30) & 1) || npart == 0) continue;
+          double sum = part[slot];
+          for (int q = 1; q <= npart; ++q) sum += part[slot + q];
+          const int dst = rc.x & 0xffff;
+          if (modeA) t[dst] = v[dst] - sum;
+          else v[dst] = sum;
         }
       }
       __syncwarp();
     }
+    // projection, dual update, residual partials; candidate extrapolation
+    const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));  // nesterov_next_coefficient
+    const double beta = (a - 1.0) / an;
     double rp = 0.0, dmax = 0.0, rc = 0.0;
     for (int u = lane; u < n_units; u += 32) {
       const bool con = u >= first_contact;
       const int r0 = con ? first_contact + 3 * (u - first_contact) : u;
       const int nr = con ? 3 : 1;
       double x[3] = {0, 0, 0}, wv[3] = {0, 0, 0}, yn[3] = {0, 0, 0};
-      
 #pragma unroll
-      for (int d = 0; d < 3; ++d) if (d < nr) {
-        x[d] = v[row2pos[r0 + d]];
-        x_s[r0 + d] = x[d];
-        wv[d] = x[d] - zh_s[r0 + d] / rho;
-      }
+      for (int d = 0; d < 3; ++d)
+        if (d < nr) {
+          x[d] = v[row2pos[r0 + d]];
+          wv[d] = x[d] - zh_s[r0 + d] / rho;
+        }
       if (con) project_soc(wv, rmu[r0], yn);
       else yn[0] = u >= n_jd ? fmax(0.0, wv[0]) : wv[0];
       double ymax = 0.0, zmax = 0.0;
-      
 #pragma unroll
-      for (int d = 0; d < 3; ++d) if (d < nr) {
-        const double zn = zh_s[r0 + d] - rho * (x[d] - yn[d]);
-        const double yo = y_s[r0 + d];
-        rp = fmax(rp, fabs(x[d] - yn[d]));
-        dmax = fmax(dmax, fabs(yn[d] - yo));
-        ymax = fmax(ymax, fabs(yn[d]));
-        zmax = fmax(zmax, fabs(zn));
-        yp_s[r0 + d] = yo;
-        zp_s[r0 + d] = z_s[r0 + d];
-        y_s[r0 + d] = yn[d];
-        z_s[r0 + d] = zn;
-      }
+      for (int d = 0; d < 3; ++d)
+        if (d < nr) {
+          const double zn = zh_s[r0 + d] - rho * (x[d] - yn[d]);
+          const double yo = y_s[r0 + d], zo = z_s[r0 + d];
+          rp = fmax(rp, fabs(x[d] - yn[d]));
+          dmax = fmax(dmax, fabs(yn[d] - yo));
+          ymax = fmax(ymax, fabs(yn[d]));
+          zmax = fmax(zmax, fabs(zn));
+          y_s[r0 + d] = yn[d];
+          z_s[r0 + d] = zn;
+          yh_s[r0 + d] = sp.acceleration ? yn[d] + beta * (yn[d] - yo) : yn[d];
+          zh_s[r0 + d] = sp.acceleration ? zn + beta * (zn - zo) : zn;
+        }
       if (u >= n_jd) rc = fmax(rc, fmin(ymax, zmax));
     }
     r_p = warp_max(rp);
@@ -305,38 +363,34 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
       break;
     }
     // nesterov_update (padmm.cpp:58-71)
-    bool restart = false;
-    double beta = 0.0;
-    if (sp.acceleration) {
-      restart = sp.restart && combined > prev;
-      if (restart) {
-        a = 1.0;
-        ++restarts;
-      } else {
-        const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));
-        beta = (a - 1.0) / an;
-        a = an;
-      }
+    const bool restart = sp.acceleration && sp.restart && combined > prev;
+    if (restart) {
+      a = 1.0;
+      ++restarts;
+    } else if (sp.acceleration) {
+      a = an;
     }
-    const bool extrapolate = sp.acceleration && !restart;
     for (int u = lane; u < n_units; u += 32) {
       const bool con = u >= first_contact;
       const int r0 = con ? first_contact + 3 * (u - first_contact) : u;
       const int nr = con ? 3 : 1;
-      
-#pragma unroll
-      for (int d = 0; d < 3; ++d) if (d < nr) {
-        const double y = y_s[r0 + d], z = z_s[r0 + d];
-        yh_s[r0 + d] = extrapolate ? y + beta * (y - yp_s[r0 + d]) : y;
-        zh_s[r0 + d] = extrapolate ? z + beta * (z - zp_s[r0 + d]) : z;
-      }
-      const double s0 = con ? rmu[r0] * hypot(zh_s[r0 + 1], zh_s[r0 + 2]) : 0.0;
-      
+      double zz[3] = {0, 0, 0};
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        if (d < nr)
-        v[row2pos[r0 + d]] =
-            -((((vf_s[r0 + d] + (d == 0 ? s0 : 0.0)) - eta * x_s[r0 + d]) - rho * yh_s[r0 + d]) - zh_s[r0 + d]);
+        if (d < nr) {
+          if (restart) {
+            yh_s[r0 + d] = y_s[r0 + d];
+            zh_s[r0 + d] = z_s[r0 + d];
+          }
+          zz[d] = zh_s[r0 + d];
+        }
+      const double s0 = con ? rmu[r0] * hypot(zz[1], zz[2]) : 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (d < nr) {
+          const int pos = row2pos[r0 + d];
+          v[pos] = -((((vf_s[r0 + d] + (d == 0 ? s0 : 0.0)) - eta * v[pos]) - rho * yh_s[r0 + d]) - zz[d]);
+        }
     }
     prev = combined;
     __syncwarp();
@@ -362,16 +416,16 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
 }
 
 cudaError_t launch_sparse(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int per_warp,
-                          int wpc, cudaStream_t s) {
+                          int wpc, int prog_words, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  const size_t smem = (size_t)per_warp * wpc * sizeof(double);
+  const size_t smem = ((size_t)prog_words + 3) / 4 * 16 + (size_t)per_warp * wpc * sizeof(double);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     const cudaError_t e = cudaFuncSetAttribute(sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  sparse_kernel<<<(count + wpc - 1) / wpc, 32 * wpc, smem, s>>>(bv, sp, worlds, count, per_warp);
+  sparse_kernel<<<(count + wpc - 1) / wpc, 32 * wpc, smem, s>>>(bv, sp, worlds, count, per_warp, prog_words);
   return cudaGetLastError();
 }
 

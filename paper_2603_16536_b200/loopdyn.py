@@ -100,8 +100,8 @@ class Model:
         _check(lib().kd_joint_coordinate(self.handle, int(joint), _capi.dptr(p), C.byref(out)))
         return out.value
 
-    SPARSE_PLAN_FIELDS = ("slots", "nnz_L", "lv_len", "supernodes", "solve_levels", "factor_levels",
-                          "factor_terms", "solve_terms", "dense_factor_terms", "factor_crit", "solve_crit",
+    SPARSE_PLAN_FIELDS = ("slots", "nnz_L", "lv_len", "supernodes", "solve_levels", "program_words",
+                          "factor_fma", "solve_terms", "dense_factor_fma", "smem_doubles_per_world", "solve_crit",
                           "solve_phases")
 
     def sparse_plan_info(self) -> Optional[dict]:

@@ -63,6 +63,6 @@ b.step(cfg, 1)
 pc = b.phase_cycles()
 its = np.array([x.iterations for x in b.diagnostics()[:148]])
 names = ["gram_scaled", "unused", "cholesky", "inverse", "padmm", "chol_panel", "chol_syrk", "chol_diag"]
-print(json.dumps({"phase_cycles_mean": {names[k]: float(pc[:, k].mean()) for k in range(8)},
+print(json.dumps({"kernel": b.kernels()[0], "phase_cycles_mean": {names[k]: float(pc[:, k].mean()) for k in range(8)},
                   "iters_mean": float(its.mean()),
                   "padmm_cycles_per_iter": float((pc[:, 4] / np.maximum(its, 1)).mean())}), flush=True)
