@@ -514,7 +514,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     std::vector<DevSnPlan> dp(n_models);
     std::vector<SnGram> gram;
     std::vector<SnSuper> sups;
-    std::vector<uint32_t> tmap, prog;
+    std::vector<SnGBody> gbody;
+    std::vector<uint32_t> tmap, prog, gslot, gpair;
     std::vector<int32_t> pslot;
     std::vector<uint16_t> spos;
     for (int i = 0; i < n_models; ++i) {
@@ -536,6 +537,20 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       pslot.insert(pslot.end(), p.pair_slot.begin(), p.pair_slot.end());
       d.slotpos_off = (int)spos.size();
       spos.insert(spos.end(), p.slot_pos.begin(), p.slot_pos.end());
+      d.kmax = p.kmax;
+      d.vreg = p.vreg;
+      d.gbody_off = (int)gbody.size();
+      d.n_gbody = (int)p.gbody.size();
+      {
+        const int so = (int)gslot.size(), po = (int)gpair.size();
+        for (SnGBody g : p.gbody) {
+          g.slot_off += so;
+          g.pair_off += po;
+          gbody.push_back(g);
+        }
+        gslot.insert(gslot.end(), p.gslot.begin(), p.gslot.end());
+        gpair.insert(gpair.end(), p.gpair.begin(), p.gpair.end());
+      }
       d.sup_off = (int)sups.size();
       d.n_sup = (int)p.sup.size();
       const int to = (int)tmap.size();
@@ -559,6 +574,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     };
     KD_CK(up(v.snplan, dp));
     KD_CK(up(v.sn_gram, gram));
+    KD_CK(up(v.sn_gbody, gbody));
+    KD_CK(up(v.sn_gslot, gslot));
+    KD_CK(up(v.sn_gpair, gpair));
     KD_CK(up(v.sn_sup, sups));
     KD_CK(up(v.sn_tmap, tmap));
     KD_CK(up(v.sn_prog, prog));

@@ -83,6 +83,13 @@ enum SnGramFlags : uint16_t {
   SG_S2 = 16,  // sides for the second shared body
   SG_T2 = 32,
 };
+// Gram by body (ascending): the k rows touching the body (slot | side << 16 at
+// gslot[slot_off..]) are staged, then its n_store + n_acc pairs (Lv index |
+// local i << 16 | local j << 24 at gpair[pair_off..]) are written / added.
+struct SnGBody {
+  int32_t slot_off, k, pair_off, n_store;
+  int32_t n_acc, pad0, pad1, pad2;
+};
 // One supernode: columns [c0, c0+w) of the factor in elimination order, with
 // m rows below the diagonal block.  Its dense panel ((w+m) x w, column-major,
 // odd column stride ld) lives at Lv[pb]; rows 0..w-1 are the supernode's own
@@ -102,11 +109,13 @@ struct SnSuper {
 // mode 0 (A): t[dst] = v[dst] - sum Lv[a] v[b];  mode 1 (B): v[dst] = sum Lv[a] t[b].
 // A row's terms may be split over consecutive slots (chunks); its first chunk
 // (owner) adds the others' partial sums in slot order after a __syncwarp.
+constexpr int kSnChunk = 8;  // max terms per solve chunk (the kernel's unrolled width)
 struct DevSnPlan {
   int32_t S, nLv, n_jd, lim_base;
   int32_t gram_off, n_gram, pair_off, slotpos_off;
   int32_t sup_off, n_sup, prog_off, prog_words;
   int32_t n_sph, max_slots, smem_doubles, pad0;  // smem_doubles: per-warp footprint
+  int32_t gbody_off, n_gbody, kmax, vreg;  // vreg: per-warp vector region (doubles)
 };
 
 // Per-world indexing (prefix sums over model capacities).
@@ -214,6 +223,9 @@ struct BatchView {
   // supernodal plans (indexed by model; S == 0: none)
   const DevSnPlan* snplan;
   const SnGram* sn_gram;
+  const SnGBody* sn_gbody;
+  const uint32_t* sn_gslot;
+  const uint32_t* sn_gpair;
   const SnSuper* sn_sup;
   const uint32_t* sn_tmap;
   const uint32_t* sn_prog;

@@ -312,6 +312,56 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       g.flags = f;
       p.gram.push_back(g);
     }
+  // ---- per-body Gram lists: bodies ascending; a body's rows in slot order.
+  // An entry shared by two bodies b1 < b2 is stored by b1 and accumulated by
+  // b2, which is assemble_dense's ascending body order (delassus.cpp:80-95).
+  {
+    const int nbod = (int)m.bodies.size();
+    std::vector<std::vector<uint32_t>> bsl(nbod);
+    std::vector<std::vector<int>> local(nbod, std::vector<int>(S, -1));
+    for (int sl = 0; sl < S; ++sl)
+      for (int u = 0; u < 2; ++u) {
+        const int b = sb[2 * sl + u];
+        if (b < 0) continue;
+        local[b][sl] = (int)bsl[b].size();
+        bsl[b].push_back((uint32_t)sl | ((uint32_t)u << 16));
+      }
+    std::vector<std::vector<uint32_t>> st(nbod), ac(nbod);
+    int kmax = 0;
+    for (int b = 0; b < nbod; ++b) kmax = std::max(kmax, (int)bsl[b].size());
+    const int Sp = (S + 1) & ~1;
+    if (kmax > 255) {
+      why = "a body carries too many rows for the staged Gram";
+      return false;
+    }
+    p.kmax = kmax;
+    p.vreg = std::max(7 * Sp, 12 * kmax + Sp);  // PADMM vectors, or Gram staging + P
+    for (const SnGram& g : p.gram) {
+      int bodies[2], ns = 0;
+      for (int u = 0; u < 2; ++u) {
+        const int b = sb[2 * g.s + u];
+        if (b >= 0 && (sb[2 * g.t] == b || sb[2 * g.t + 1] == b)) bodies[ns++] = b;
+      }
+      if (ns == 2 && bodies[1] < bodies[0]) std::swap(bodies[0], bodies[1]);
+      for (int k = 0; k < ns; ++k) {
+        const int b = bodies[k];
+        const uint32_t word = (uint32_t)g.dst | ((uint32_t)local[b][g.s] << 16) | ((uint32_t)local[b][g.t] << 24);
+        (k == 0 ? st[b] : ac[b]).push_back(word);
+      }
+    }
+    for (int b = 0; b < nbod; ++b) {
+      SnGBody gb{};
+      gb.slot_off = (int)p.gslot.size();
+      gb.k = (int)bsl[b].size();
+      p.gslot.insert(p.gslot.end(), bsl[b].begin(), bsl[b].end());
+      gb.pair_off = (int)p.gpair.size();
+      gb.n_store = (int)st[b].size();
+      gb.n_acc = (int)ac[b].size();
+      p.gpair.insert(p.gpair.end(), st[b].begin(), st[b].end());
+      p.gpair.insert(p.gpair.end(), ac[b].begin(), ac[b].end());
+      p.gbody.push_back(gb);
+    }
+  }
   // ---- solve program over supernode levels
   std::vector<int> slev(K, 0);
   for (int k = 0; k < K; ++k)
@@ -379,11 +429,12 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
     const PhaseBuild& P = phases[ph];
     int maxn = 1;
     for (const Row& r : P.rows) maxn = std::max(maxn, (int)r.terms.size());
-    // chunk size: minimise an issue-cost estimate (steps x chunk length, plus
-    // the combine pass when any row is split)
-    int bestC = maxn, bestSlots = 0;
+    // chunk size (<= kSnChunk, the device's unrolled width): minimise a
+    // latency estimate — each step costs about two dependent shared-memory
+    // round trips plus the chunk's FMA chain, a split phase one more pass
+    int bestC = 1, bestSlots = 0;
     double bestCost = 1e30;
-    for (int C = 1; C <= maxn; ++C) {
+    for (int C = 1; C <= std::min(maxn, kSnChunk); ++C) {
       int slots = 0;
       bool split = false;
       for (const Row& r : P.rows) {
@@ -392,7 +443,7 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
         split |= ch > 1;
       }
       const int steps = (slots + 31) / 32;
-      const double cost = steps * (4.0 * C + 24.0) + (split ? 60.0 : 0.0);
+      const double cost = steps * (100.0 + 3.0 * C) + (split ? 90.0 : 0.0);
       if (cost < bestCost || (cost == bestCost && C > bestC)) {
         bestCost = cost;
         bestC = C;
@@ -447,9 +498,9 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       }
       blob[blob[4 * ph] + 2 * r + 1] = toff | recs[ph][r].flags;
     }
-  {  // per-warp shared memory of kd_sparse.cu: Lv | v t | 5 PADMM vectors | partials | 2 int16 maps
+  {  // per-warp shared memory of kd_sparse.cu: Lv | v t + 5 PADMM vectors (or Gram staging) | partials | 2 int16 maps
     const int Sp = (S + 1) & ~1;
-    p.smem_doubles = ((nLv + 1) & ~1) + 7 * Sp + p.max_slots + (Sp + 1) / 2 + 1;
+    p.smem_doubles = ((nLv + 1) & ~1) + p.vreg + p.max_slots + (Sp + 1) / 2 + 1;
   }
   return true;
 }
@@ -505,14 +556,12 @@ void cpu_solve(const SnPlanHost& p, const std::vector<double>& Lv, std::vector<d
       if (!(w1 >> 31)) continue;
       const int dst = w0 & 0xffff, nt = w0 >> 16;
       const uint32_t toff = w1 & 0xffffff;
-      double a0 = 0.0, a1 = 0.0;
+      double pr[kSnChunk] = {};
       for (int k = 0; k < nt; ++k) {
         const uint32_t tt = blob[toff + k];
-        const double prod = Lv[tt & 0xffff] * (mode == 0 ? v : t)[tt >> 16];
-        if (k & 1) a1 += prod;
-        else a0 += prod;
+        pr[k] = Lv[tt & 0xffff] * (mode == 0 ? v : t)[tt >> 16];
       }
-      const double s = a0 + a1;
+      const double s = ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
       const bool owner = (w1 >> 30) & 1;
       const int npart = (w1 >> 24) & 63;
       if (owner && npart == 0) finalize(dst, s);

@@ -44,10 +44,15 @@ struct SnPlanHost {
   int smem_doubles = 0;  // per-warp shared-memory footprint of the device kernel
   int max_slots = 0;     // largest phase (slots) of the solve program
   int n_sph = 0;         // solve phases
+  int kmax = 0;          // most rows touching one body
+  int vreg = 0;          // per-warp vector region (doubles)
   std::vector<int32_t> pair_slot;   // per collision pair: first contact slot, -1 if unplanned
   std::vector<uint16_t> slot_pos;   // slot -> elimination position
   std::vector<int32_t> slot_body;   // 2 per slot: (body a, body b or -1)
   std::vector<SnGram> gram;
+  std::vector<SnGBody> gbody;       // per body: its rows and Gram pairs
+  std::vector<uint32_t> gslot;      // slot | side << 16
+  std::vector<uint32_t> gpair;      // Lv index | local row i << 16 | local row j << 24
   std::vector<SnSuper> sup;
   std::vector<uint32_t> tmap;
   std::vector<uint32_t> prog;       // solve program blob (see kd_layout.h)

@@ -15,7 +15,7 @@
 // (one __syncthreads) all synchronisation is __syncwarp.
 //
 // Shared memory: [solve program blob] then per warp (doubles):
-//   Lv[nLv] | v[S] | t[S] | vf y z yh zh [S each] | part[max_slots]
+//   Lv[nLv] | v[S] | t[S] | vf y z yh zh [S each] (Gram: row-block staging + P) | part[max_slots]
 //   | int16 row2pos[S] | int16 slot2row[S]
 #include "kd_device.cuh"
 
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   double* z_s = y_s + Sp;
   double* yh_s = z_s + Sp;
   double* zh_s = yh_s + Sp;
-  double* part = zh_s + Sp;
+  double* part = v + P.vreg;
   int16_t* row2pos = reinterpret_cast<int16_t*>(part + P.max_slots);
   int16_t* slot2row = row2pos + Sp;
 
@@ -102,10 +102,7 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
 
   // ---- 0. zero the factor array, map compact rows <-> planned slots
   for (int e = lane; e < P.nLv; e += 32) Lv[e] = 0.0;
-  for (int s = lane; s < S; s += 32) {
-    v[s] = 0.0;
-    slot2row[s] = s < n_jd ? (int16_t)s : (int16_t)-1;
-  }
+  for (int s = lane; s < S; s += 32) slot2row[s] = s < n_jd ? (int16_t)s : (int16_t)-1;
   for (int r = lane; r < n_jd; r += 32) row2pos[r] = (int16_t)slot_pos[r];
   __syncwarp();
   {
@@ -131,38 +128,63 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   }
   __syncwarp();
 
-  // ---- 1. Gram: D(s, t) for every planned nonzero (delassus.cpp:67-104)
+  // ---- 1. Gram D = P (J M^-1 J^T + R) P + (eta+rho) I (delassus.cpp:67-104),
+  // body by body in ascending order: stage the body's row blocks (JM and J of
+  // the side touching it; inactive slots stage zeros), then every planned pair
+  // of its rows is written (first shared body) or added (second).
   {
     const RowJ* rj = bv.rowj + R0;
-    const double* scale = bv.scale + R0;
+    double* stJM = v;                      // scratch: the PADMM vectors are not live yet
+    double* stJ = v + 6 * P.kmax;
+    double* Ps = v + P.vreg - Sp;          // P per compact row
+    for (int r = lane; r < n; r += 32) Ps[r] = bv.scale[R0 + r];
+    const SnGBody* gbl = bv.sn_gbody + P.gbody_off;
+    for (int b = 0; b < P.n_gbody; ++b) {
+      const SnGBody gb = gbl[b];
+      for (int l = lane; l < gb.k; l += 32) {
+        const uint32_t e = bv.sn_gslot[gb.slot_off + l];
+        const int r = slot2row[e & 0xffff];
+        const int off = (e >> 16) ? 6 : 0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          stJM[6 * l + k] = r >= 0 ? rj[r].JM[off + k] : 0.0;
+          stJ[6 * l + k] = r >= 0 ? rj[r].J[off + k] : 0.0;
+        }
+      }
+      __syncwarp();
+      const uint32_t* pw = bv.sn_gpair + gb.pair_off;
+      for (int e = lane; e < gb.n_store + gb.n_acc; e += 32) {
+        const uint32_t q = pw[e];
+        const double* a = stJM + 6 * ((q >> 16) & 0xff);
+        const double* c = stJ + 6 * (q >> 24);
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s += a[k] * c[k];
+        if (e < gb.n_store) Lv[q & 0xffff] = s;
+        else Lv[q & 0xffff] += s;
+      }
+      __syncwarp();
+    }
+    // + R on the diagonal, P scaling, + (eta+rho) I; inactive slots -> identity
     const double* reg = bv.reg + R0;
     const double eta_rho = sp.eta + sp.rho;
     const SnGram* gl = bv.sn_gram + P.gram_off;
     for (int e = lane; e < P.n_gram; e += 32) {
       const SnGram g = gl[e];
       const int rs = slot2row[g.s], rt = slot2row[g.t];
-      if (rs < 0 || rt < 0) {  // inactive slot: identity row
-        if (g.flags & SG_DIAG) Lv[g.dst] = 1.0;
+      const bool diag = g.flags & SG_DIAG;
+      if (rs < 0 || rt < 0) {
+        if (diag) Lv[g.dst] = 1.0;
         continue;
       }
-      const double* jm = rj[rs].JM + ((g.flags & SG_S1) ? 6 : 0);
-      const double* jj = rj[rt].J + ((g.flags & SG_T1) ? 6 : 0);
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) s += jm[k] * jj[k];
-      if (g.flags & SG_TWO) {
-        const double* jm2 = rj[rs].JM + ((g.flags & SG_S2) ? 6 : 0);
-        const double* jj2 = rj[rt].J + ((g.flags & SG_T2) ? 6 : 0);
-        double s2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) s2 += jm2[k] * jj2[k];
-        s += s2;
-      }
-      if (g.flags & SG_DIAG) s += reg[rs];
-      double d = (scale[rs] * s) * scale[rt];
-      if (g.flags & SG_DIAG) d += eta_rho;
+      double s = Lv[g.dst];
+      if (diag) s += reg[rs];
+      double d = (Ps[rs] * s) * Ps[rt];
+      if (diag) d += eta_rho;
       Lv[g.dst] = d;
     }
+    __syncwarp();
+    for (int s = lane; s < S; s += 32) v[s] = 0.0;  // inactive positions stay zero through every solve
   }
   __syncwarp();
   stamp(0);
@@ -189,7 +211,17 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
         for (int q = c + 1 + lane; q < rows; q += 32) {
           const double lq = col[q];
           const int jmax = min(q, u.w - 1);
-          for (int j = c + 1; j <= jmax; ++j) Pn[j * u.ld + q] -= lq * col[j];
+          int j = c + 1;
+          for (; j + 3 <= jmax; j += 4) {  // loads first: the stores cannot alias them
+            const double c0 = col[j], c1 = col[j + 1], c2 = col[j + 2], c3 = col[j + 3];
+            double* p0 = Pn + j * u.ld + q;
+            const double p00 = p0[0], p01 = p0[u.ld], p02 = p0[2 * u.ld], p03 = p0[3 * u.ld];
+            p0[0] = p00 - lq * c0;
+            p0[u.ld] = p01 - lq * c1;
+            p0[2 * u.ld] = p02 - lq * c2;
+            p0[3 * u.ld] = p03 - lq * c3;
+          }
+          for (; j <= jmax; ++j) Pn[j * u.ld + q] -= lq * col[j];
         }
         __syncwarp();
       }
@@ -284,17 +316,16 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
         if (!(rc.y >> 31)) continue;
         const int dst = rc.x & 0xffff, nt = rc.x >> 16;
         const uint32_t* tm = prog + (rc.y & 0xffffff);
-        double a0 = 0.0, a1 = 0.0;
-        int k = 0;
-        for (; k + 1 < nt; k += 2) {
-          const uint32_t t0 = tm[k], t1 = tm[k + 1];
-          a0 += Lv[t0 & 0xffff] * src[t0 >> 16];
-          a1 += Lv[t1 & 0xffff] * src[t1 >> 16];
-        }
-        if (k < nt) {
-          const uint32_t t0 = tm[k];
-          a0 += Lv[t0 & 0xffff] * src[t0 >> 16];
-        }
+        // all index words, then all operand loads, then a fixed-order tree:
+        // two shared-memory round trips per chunk instead of one per term
+        uint32_t tw[kSnChunk];
+#pragma unroll
+        for (int k = 0; k < kSnChunk; ++k) tw[k] = k < nt ? tm[k] : 0u;
+        double pr[kSnChunk];
+#pragma unroll
+        for (int k = 0; k < kSnChunk; ++k) pr[k] = k < nt ? Lv[tw[k] & 0xffff] * src[tw[k] >> 16] : 0.0;
+        const double a0 = ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+        const double a1 = ((pr[4] + pr[5]) + (pr[6] + pr[7]));
         const double sum = a0 + a1;
         if (((rc.y >> 30) & 1) && ((rc.y >> 24) & 63) == 0) {
           if (modeA) t[dst] = v[dst] - sum;
