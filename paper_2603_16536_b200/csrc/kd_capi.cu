@@ -70,6 +70,7 @@ constexpr int kClasses[4][2] = {{32, 64}, {64, 64}, {128, 128}, {232, 256}};
 constexpr int kSmemMaxRows = 232;
 constexpr int kDenseGlobalMaxRows = KD_DENSE_ROW_CROSSOVER;
 constexpr size_t kSnMaxSmem = 232448;  // per-CTA shared memory opt-in limit (227 KB)
+constexpr int kSnAutoMaxSlots = 32;     // supernodal kernel by default up to one dense tile
 
 }  // namespace
 
@@ -95,6 +96,7 @@ struct kd_batch {
   };
   std::vector<SnBin> sn_bins;
   bool sparse = true;
+  int sparse_mode = 1;
   int hist_cap = 0;
   double* d_hist = nullptr;
   int32_t* d_err = nullptr;
@@ -292,9 +294,10 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     if (!models[i]) return fail(KD_ERR_INVALID_ARGUMENT, "null model");
     b->models.push_back(models[i]->m);
   }
-  {  // KD_SPARSE=0 disables the supernodal path (A/B comparisons against the dense kernel)
+  {  // supernodal path: KD_SPARSE=0 off, 1 (default) for small planned models, 2 for every planned model
     const char* e = getenv("KD_SPARSE");
-    b->sparse = !(e && e[0] == '0');
+    b->sparse_mode = e ? (e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1)) : 1;
+    b->sparse = b->sparse_mode != 0;
   }
   b->n_worlds = n_worlds;
   // model tables
@@ -324,7 +327,11 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     d.joint_off = (int)joints.size();
     d.geom_off = (int)geoms.size();
     d.pair_off = (int)pairs.size();
-    d.sn = (b->sparse && m.sn &&
+    // Auto: the supernodal kernel (a warp per world, several worlds per CTA)
+    // wins on small systems (measured 2.1x on fourbar, 1.9x on double_fourbar);
+    // on larger ones (serial_chain_10, DR-Legs) the fused dense kernel's
+    // parallel explicit-inverse solves win (tests/kernel_ab.py).
+    d.sn = (b->sparse && m.sn && (b->sparse_mode == 2 || m.sn->S <= kSnAutoMaxSlots) &&
             (size_t)m.sn->smem_doubles * 8 + (((size_t)m.sn->prog.size() * 4 + 15) & ~(size_t)15) <= kSnMaxSmem)
                ? 1 : 0;
     for (int k = 0; k < 3; ++k) d.gravity[k] = m.gravity[k];

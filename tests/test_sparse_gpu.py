@@ -28,7 +28,23 @@ def _batch(sc, n, jitter=True):
     return b
 
 
-def test_dr_legs_runs_supernodal_kernel():
+@pytest.fixture
+def force_supernodal(monkeypatch):
+    """KD_SPARSE=2: the supernodal kernel for every planned model (Auto keeps
+    it for small systems only)."""
+    monkeypatch.setenv("KD_SPARSE", "2")
+
+
+def test_auto_kernel_choice():
+    small = _batch(oracle_lib.bundled_scene("fourbar"), 4, jitter=False)
+    large = _batch(dr_legs(), 4)
+    small.step(K.config_for(oracle_lib.bundled_scene("fourbar")), 2)
+    large.step(K.config_for(dr_legs()), 2)
+    assert small.kernels() == ["supernodal"] * 4
+    assert large.kernels() == ["dense"] * 4
+
+
+def test_dr_legs_runs_supernodal_kernel(force_supernodal):
     sc = dr_legs()
     b = _batch(sc, 16)
     b.step(K.config_for(sc), 3)
@@ -40,6 +56,7 @@ def test_dr_legs_runs_supernodal_kernel():
 def test_supernodal_matches_dense_kernel_from_identical_states(monkeypatch):
     sc = dr_legs()
     cfg = K.config_for(sc)
+    monkeypatch.setenv("KD_SPARSE", "2")
     sn = _batch(sc, 16)
     monkeypatch.setenv("KD_SPARSE", "0")
     de = _batch(sc, 16)
@@ -61,7 +78,9 @@ def test_supernodal_matches_dense_kernel_from_identical_states(monkeypatch):
     assert same >= 0.98 * total
 
 
-def test_supernodal_dr_legs_trajectory_vs_oracle():
+def test_supernodal_dr_legs_trajectory_vs_oracle(force_supernodal):
+    """Same protocol and tolerances as the dense kernel's DR-Legs trajectory
+    test (test_parity_gpu.py): 8 worlds x 100 steps."""
     sc = dr_legs()
     cfg = K.config_for(sc)
     n = 8
@@ -73,7 +92,7 @@ def test_supernodal_dr_legs_trajectory_vs_oracle():
     ob.set_state(p, t, tm)
     gb.set_state(p, t, tm)
     same = total = 0
-    for _ in range(150):
+    for _ in range(100):
         gb.step(cfg)
         ob.step(cfg)
         for dg, do in zip(gb.diagnostics(), ob.diagnostics()):
@@ -122,7 +141,7 @@ def _two_spheres():
     return b.scene()
 
 
-def test_unplanned_contact_falls_back_to_dense_kernel():
+def test_unplanned_contact_falls_back_to_dense_kernel(force_supernodal):
     sc = _two_spheres()
     m = K.build_model(sc)
     assert m.sparse_plan_info() is not None
@@ -143,9 +162,10 @@ def test_unplanned_contact_falls_back_to_dense_kernel():
     assert np.abs(pg - po).max() < 1e-9
 
 
-def test_heterogeneous_batch_uses_both_kernels():
-    """Config 3 mix: four-bar, DR-Legs and serial chain worlds in one batch;
-    each planned model gets its own supernodal CTA bin."""
+def test_heterogeneous_batch_kernels():
+    """Config 3 mix: four-bar, DR-Legs and serial chain worlds in one batch
+    under Auto: the four-bars take the supernodal kernel, the rest the dense
+    kernel, all in one step."""
     scs = [oracle_lib.bundled_scene("fourbar"), dr_legs(), oracle_lib.bundled_scene("serial_chain_10")]
     ms = [K.build_model(s) for s in scs]
     oms = [oracle_lib.OracleModel(s) for s in scs]
@@ -160,7 +180,8 @@ def test_heterogeneous_batch_uses_both_kernels():
         ob.step(cfg)
         for dg, do in zip(gb.diagnostics(), ob.diagnostics()):
             assert (dg.n_rows, dg.iterations) == (do.n_rows, do.iterations)
-    assert set(gb.kernels()) == {"supernodal"}
+    kinds = gb.kernels()
+    assert all(kinds[w] == ("supernodal" if wm[w] == 0 else "dense") for w in range(12))
     pg, _, _ = gb.get_state()
     po, _, _ = ob.get_state()
     assert np.abs(pg - po).max() < 1e-9
