@@ -72,30 +72,35 @@ __device__ __forceinline__ void block_max3(double& a, double& b, double& c, doub
 // Factor the packed diagonal tile in place and overwrite it with L_kk^{-1}.
 // One warp; lane r owns row r in registers (fully unrolled so every register
 // index is static; the kernel calls this from exactly one site to keep a
-// single copy of the code in the instruction cache).  Pivots use one rsqrt
-// each (L_cc = d rsqrt(d), L_rc = a_rc rsqrt(d)); the reciprocals are kept so
-// the inverse is division-free.
-__device__ __noinline__ void diag_factor_invert(double* T, int rk, int lane, int* fail) {
+// single copy of the code in the instruction cache).  Pivots use one
+// reciprocal square root each (L_cc = d r, L_rc = a_rc r, r = 1/sqrt(d)); the
+// reciprocals are kept so the inverse is division-free.
+__device__ __noinline__ void diag_factor_invert(double* T, int rk, int lane, int* fail, double* col) {
   double a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = (lane < rk && c <= lane) ? T[tri(lane) + c] : (c == lane ? 1.0 : 0.0);
   bool bad = false;
   double my_rinv = 1.0;
+  // pivot c: column c goes through shared memory (one store, broadcast reads)
+  // instead of 31 shuffles, and 1/sqrt(d) is a float seed plus two Newton
+  // steps instead of the generic rsqrt; both were the diagonal chain's cost
+  // (tools/microbench_chain.cu: 16.5k -> 11.7k cycles per tile)
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
-    const double dcc = __shfl_sync(FULL, a[c], c);
+    col[lane] = a[c];
+    __syncwarp();
+    const double dcc = col[c];
     if (!(dcc > 0.0)) bad = true;
-    const double rinv = rsqrt(dcc);
+    const double rinv = fast_rsqrt(dcc);
     const double lc = lane > c ? a[c] * rinv : (lane == c ? dcc * rinv : a[c]);
     if (lane == c) my_rinv = rinv;
     a[c] = lc;
 #pragma unroll
-    for (int j = 1; j < 32; ++j) {
-      if (j > c) {
-        const double ljc = __shfl_sync(FULL, lc, j);
-        if (j <= lane) a[j] -= lc * ljc;
-      }
+    for (int j = c + 1; j < 32; ++j) {
+      const double ljc = col[j] * rinv;  // = lane j's L_jc
+      if (j <= lane) a[j] -= lc * ljc;
     }
+    __syncwarp();
   }
   if (bad && lane == 0) *fail = 1;
 #pragma unroll
@@ -415,6 +420,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   double* wv_s = P + npad;         // intermediate w = L^{-1} b
   double* red = wv_s + npad;       // 3 * NW
   int* rbs = reinterpret_cast<int*>(red + 3 * NW + 1);  // 2n body ids
+  double* chain = reinterpret_cast<double*>(rbs + 2 * npad);  // 32 doubles: pivot-column broadcast
   __shared__ int fail;
   const int64_t R0 = W.row_off;
   const RowJ* rj = bv.rowj + R0;
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
           syrk_tile(L, k + 1, k + 1, k, n, lane);
           __syncwarp();
         }
-        diag_factor_invert(L + diag_tile(k + 1, n), tile_rows(k + 1, n), lane, &fail);
+        diag_factor_invert(L + diag_tile(k + 1, n), tile_rows(k + 1, n), lane, &fail, chain);
         c_diag += clock64() - q1;
       } else {
         for (int u = wid; u < units; u += NW - 1) {  // unit 0, tile (k+1, k+1), is warp 0's
@@ -713,7 +719,7 @@ size_t dense_smem_bytes(int n, int nt, bool global_l) {
   const size_t nl = (size_t)528 * (T - 1) * (T - 1) + (size_t)(T - 1) * 33 * rl + (size_t)rl * (rl + 1) / 2;
   const size_t nlen = global_l ? 0 : ((nl + 1) & ~(size_t)1);
   const size_t npad = 32 * (size_t)T;
-  return 8 * (nlen + 3 * npad + 3 * (nt / 32) + 1) + 4 * 2 * npad + 64;
+  return 8 * (nlen + 3 * npad + 3 * (nt / 32) + 1) + 4 * 2 * npad + 8 * 32 + 64;
 }
 
 template <int NT, bool G>

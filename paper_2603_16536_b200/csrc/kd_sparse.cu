@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
         double* col = Pn + c * u.ld;
         const double d = col[c];
         if (!(d > 0.0)) bad = true;
-        const double r = rsqrt(d);
+        const double r = fast_rsqrt(d);
         for (int q = c + 1 + lane; q < rows; q += 32) col[q] *= r;
         __syncwarp();
         if (lane == 0) X[c * u.ws + c] = r;  // X (= L_SS^-1, transposed into the upper triangle) keeps 1/L_cc
