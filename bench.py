@@ -23,6 +23,13 @@ iterations; settled steps ~35).
           loopdyn solver; the reference itself cannot be built here: no Eigen)
           on the host's cores, same scene/config, a bounded world sample.
 
+Other BASELINE configs (`--workload`, each its own JSON line; the default line
+is dr_legs): fourbar (configs[0]'s scene batched, 16384 worlds), hetero
+(configs[2]: four-bar / DR-Legs / serial_chain_10 by w % 3, 16384 worlds),
+closed_chain (configs[3]: 1024 ladder worlds, n = 340 -> matrix-free CR),
+sphere_pile (configs[4] substitute: 100 spheres in a bin, 8192 worlds per GPU,
+CR).  The roofline object then describes the workload's dominant kernel family.
+
 Multi-GPU: one process per GPU (torchrun); rank r owns global worlds
 [r*W, (r+1)*W): worlds are independent, so there is no collective on the data
 path ("scaling": "weak"); one all-reduce of the elapsed time at the end.
@@ -47,13 +54,39 @@ METRIC = "world-steps/sec (DR Legs worlds, dense PADMM step)"
 UNIT = "world-steps/s"
 
 
+def workloads():
+    """name -> (scene builders, world -> model index, default worlds per GPU, BASELINE config)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from paper_2603_16536_b200.scenes import closed_chain, dr_legs, sphere_pile
+
+    def bundled(name):
+        def make():
+            from paper_2603_16536_b200.scene import parse_scene_obj
+            with open(os.path.join(ROOT, "tests", "golden", "scenes_bundle.json")) as f:
+                return parse_scene_obj(json.load(f)[name], name)
+        return make
+    return {
+        "dr_legs": ([dr_legs], lambda w: 0, 4096, "configs[1]: DR Legs biped, 4096 worlds, Cholesky path"),
+        "fourbar": ([bundled("fourbar")], lambda w: 0, 16384, "configs[0]: the four-bar scene, batched"),
+        "hetero": ([bundled("fourbar"), dr_legs, bundled("serial_chain_10")], lambda w: w % 3, 16384,
+                   "configs[2]: four-bar / DR Legs / serial_chain_10 by world % 3 (main.cpp:202)"),
+        "closed_chain": ([lambda: closed_chain(22)], lambda w: 0, 1024,
+                         "configs[3]: 22-cell parallelogram ladder, n = 340 rows -> matrix-free CR"),
+        "sphere_pile": ([lambda: sphere_pile(100)], lambda w: 0, 8192,
+                        "configs[4] substitute: 100 spheres in a 5-plane bin (box-box is rejected, "
+                        "model.cpp:56-62), matrix-free CR"),
+    }
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--settle", type=int, default=50)
-    ap.add_argument("--worlds-per-gpu", type=int, default=4096)
+    ap.add_argument("--worlds-per-gpu", type=int, default=0, help="0: the workload's default")
+    ap.add_argument("--workload", default="dr_legs",
+                    choices=["dr_legs", "fourbar", "hetero", "closed_chain", "sphere_pile"])
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -140,50 +173,76 @@ def algorithmic_bytes_path(n, nb, iters, s=8):
     return algorithmic_bytes_k2(n, nb, iters, s) + s * ((14 * np.asarray(n) + 13 * nb) + (13 * np.asarray(n) + 13 * nb))
 
 
+def algorithmic_bytes_cr(n, nb, iters, applies, s=8):
+    """SURVEY.md §8d matrix-free model with the applies actually executed
+    (2 + CR iterations per solve, delassus.cpp:156-187):
+    (14n + 13nb) + 24n + A (30n + 12nb) + I 10n + (13n + 13nb)."""
+    n = np.asarray(n, np.float64)
+    return s * ((14 * n + 13 * nb) + 24 * n + np.asarray(applies) * (30 * n + 12 * nb) + np.asarray(iters) * 10 * n
+                + (13 * n + 13 * nb))
+
+
 def algorithmic_flops(n, iters):
     """n^3/3 + I (2n^2 + 20n) (Gram terms omitted: < 2%)."""
     n = np.asarray(n, np.float64)
     return n ** 3 / 3 + np.asarray(iters) * (2 * n * n + 20 * n)
 
 
-def build_world_batch(K, scene, n_local, rank, seed, device):
+def build_world_batch(K, scenes, mix, n_local, rank, seed, device):
     from paper_2603_16536_b200 import sharding
-    m = K.build_model(scene)
+    models = [K.build_model(sc) for sc in scenes]
+    worlds = sharding.world_range(n_local, rank)
     b = K.WorldBatch(device=device)
-    for _ in range(n_local):
-        b.add_world(m)
+    for w in worlds:
+        b.add_world(models[mix(w)])
     p, _, tm = b.get_state()
     # The jitter stream is global and world-major (main.cpp:199-211): rank r
     # keeps the slice of global worlds [r*W, (r+1)*W).
-    t = sharding.jitter_slice(m.initial_state().twists, m.n_bodies, sharding.world_range(n_local, rank), seed)
+    if len(models) == 1:
+        t = sharding.jitter_slice(models[0].initial_state().twists, models[0].n_bodies, worlds, seed)
+    else:
+        init = [m.initial_state().twists for m in models]
+        t = sharding.jitter_slice_mixed(lambda w: init[mix(w)], worlds, seed)
     b.set_state(p, t, tm)
-    return b, m
+    return b, models
 
 
-def cpu_baseline(args, scene, cfg, quick=False):
-    """The CPU oracle (restated reference solver) on this host's cores."""
+def cpu_baseline(args, wl, cfg, quick=False):
+    """The CPU oracle (restated reference solver) on this host's cores, on a
+    bounded sample of the workload's global world list."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib
     import paper_2603_16536_b200 as K
+    scenes, mix, W, _ = wl
     cores = os.cpu_count() or 1
-    n = min(args.worlds_per_gpu, max(32, 8 * cores)) if quick else min(args.worlds_per_gpu, max(64, 32 * cores))
-    om = oracle_lib.OracleModel(scene)
-    ob = oracle_lib.OracleBatch([om], [0] * n, n_threads=cores)
+    heavy = args.workload in ("closed_chain", "sphere_pile")
+    if heavy:
+        n = min(W, 2 * cores if quick else 8 * cores)
+    else:
+        n = min(W, max(32, 8 * cores)) if quick else min(W, max(64, 32 * cores))
+    sc = [f() for f in scenes]
+    oms = [oracle_lib.OracleModel(x) for x in sc]
+    wm = [mix(w) for w in range(n)]
+    ob = oracle_lib.OracleBatch(oms, wm, n_threads=cores)
     p, t, tm = ob.get_state()
-    t = K.bench_jitter(t, [om.n_bodies] * n, seed=args.seed)
+    t = K.bench_jitter(t, [oms[m].n_bodies for m in wm], seed=args.seed)
     ob.set_state(p, t, tm)
-    settle = args.settle if not quick else min(args.settle, 20)
-    ob.step(cfg, settle + (args.warmup if not quick else 1))
-    steps = args.steps if not quick else 3
+    settle = min(args.settle, 20) if (quick or heavy) else args.settle
+    ob.step(cfg, settle + (1 if (quick or heavy) else args.warmup))
+    steps = 3 if (quick or heavy) else args.steps
     t0 = time.perf_counter()
     ob.step(cfg, steps)
     dt = time.perf_counter() - t0
     d = ob.diagnostics()
     its = float(np.mean([d[w].iterations for w in range(n)]))
     return {"value": n * steps / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{n} DR-Legs worlds (first {n} of the global batch, same jitter), {settle} settle steps, "
-                      f"{steps} timed steps, std::thread pool of {cores} threads (batch_step, batch.cpp:74-110)",
+            "sample": f"{n} {args.workload} worlds (first {n} of the global batch, same jitter), {settle} settle "
+                      f"steps, {steps} timed steps, std::thread pool of {cores} threads (batch_step, batch.cpp:74-110)",
             "mean_padmm_iterations": its}
+
+
+def metric_for(workload):
+    return METRIC if workload == "dr_legs" else f"world-steps/sec ({workload} worlds)"
 
 
 def run_reference(args):
@@ -191,19 +250,31 @@ def run_reference(args):
     if rank != 0:
         return 0
     import paper_2603_16536_b200 as K
-    from paper_2603_16536_b200.scenes import dr_legs
-    scene = dr_legs()
-    cfg = K.config_for(scene)
-    cb = cpu_baseline(args, scene, cfg)
-    out = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": "dr_legs", "worlds_sampled": cb["sample"], "dt": cfg.dt,
-                      "integrator": cfg.integrator, "settle_steps": args.settle},
+    wl = workloads()[args.workload]
+    if args.worlds_per_gpu:
+        wl = (wl[0], wl[1], args.worlds_per_gpu, wl[3])
+    cfg = K.config_for(wl[0][0]())
+    cb = cpu_baseline(args, wl, cfg)
+    out = {"metric": metric_for(args.workload), "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": args.workload, "baseline_config": wl[3], "worlds_sampled": cb["sample"],
+                      "dt": cfg.dt, "integrator": cfg.integrator, "settle_steps": args.settle},
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
+
+
+def ncu_traffic(kernel, worlds_in_launch):
+    """dram bytes (read + write) per launch from the committed ncu capture
+    (profiles/ncu_traffic.json, per world), scaled to this launch's worlds."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f)[kernel]
+        return rec["bytes_per_world"] * worlds_in_launch, rec["source"]
+    except Exception:
+        return None, None
 
 
 def main():
@@ -218,11 +289,14 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2603_16536_b200 as K
-    from paper_2603_16536_b200.scenes import dr_legs
-    scene = dr_legs()
-    cfg = K.config_for(scene)
-    W = args.worlds_per_gpu
-    b, model = build_world_batch(K, scene, W, rank, args.seed, local)
+    wl = workloads()[args.workload]
+    W = args.worlds_per_gpu or wl[2]
+    wl = (wl[0], wl[1], W, wl[3])
+    scenes = [f() for f in wl[0]]
+    cfg = K.config_for(scenes[0])  # one StepConfig, from the first scene (main.cpp:194)
+    b, models = build_world_batch(K, scenes, wl[1], W, rank, args.seed, local)
+    wmodel = [wl[1](w) for w in range(rank * W, (rank + 1) * W)]
+    nb_w = np.array([models[m].n_bodies for m in wmodel])
     # settle + warm-up (untimed)
     b.step(cfg, args.settle)
     b.step(cfg, max(3, args.warmup))
@@ -255,24 +329,47 @@ def main():
     value = total_worlds * args.steps / (ms_max / 1e3)
 
     # ---- roofline pass: per-family device time (events on the batch stream) +
-    # per-world n and iterations of every step
+    # per-world n, iterations and kernel of every step
     b.enable_timing(True)
     rsteps = max(5, min(10, args.steps))
-    bytes_k2 = bytes_path = flops = 0.0
+    bytes_dense = bytes_cr = bytes_path = flops = 0.0
+    kern_count = {}
     for _ in range(rsteps):
         b.step(cfg, 1)
         d = b.diagnostics()
+        kinds = b.kernels()
         n = np.array([d[w].n_rows for w in range(W)])
         it = np.array([d[w].iterations for w in range(W)])
-        bytes_k2 += float(algorithmic_bytes_k2(n, model.n_bodies, it).sum())
-        bytes_path += float(algorithmic_bytes_path(n, model.n_bodies, it).sum())
+        cri = np.array([d[w].cr_iterations for w in range(W)])
+        on_cr = np.array([k == "cr" for k in kinds])
+        on_dense = np.array([k in ("dense", "supernodal") for k in kinds])
+        for k in kinds:
+            kern_count[k] = kern_count.get(k, 0) + 1
+        bytes_dense += float((algorithmic_bytes_k2(n, nb_w, it) * on_dense).sum())
+        bytes_cr += float((algorithmic_bytes_cr(n, nb_w, it, 2 * it + cri) * on_cr).sum())
+        bytes_path += float((algorithmic_bytes_path(n, nb_w, it) * on_dense).sum())
         flops += float(algorithmic_flops(n, it).sum())
     tim = b.timing()
     launches_per_step = tim["launches"] / rsteps
-    k2_ms = tim["dense_ms"] / rsteps
+    dense_ms = tim["dense_ms"] / rsteps
+    cr_ms = tim["matrix_free_ms"] / rsteps
     step_ms_fam = (tim["assemble_ms"] + tim["dense_ms"] + tim["matrix_free_ms"] + tim["recover_ms"]) / rsteps
     peak, peak_kind = measured_peaks()
-    achieved = (bytes_k2 / rsteps) / (k2_ms / 1e3) / 1e9
+    if cr_ms > dense_ms:
+        fam, fam_ms, fam_bytes = "cr", cr_ms, bytes_cr / rsteps
+        kname = "cr_kernel (K2b: matrix-free Delassus apply + warm-started Conjugate Residual + PADMM)"
+        note = ("SURVEY.md §8d matrix-free model with the applies executed; J rows stream from L2/HBM every "
+                "apply, the n-vectors stay in shared memory")
+    else:
+        fam, fam_ms, fam_bytes = "dense", dense_ms, bytes_dense / rsteps
+        kname = ("dense_kernel (K2: Delassus assembly + Cholesky + explicit-inverse PADMM, smem-resident)"
+                 if kern_count.get("dense", 0) >= kern_count.get("supernodal", 0) else
+                 "sparse_kernel (K2s: supernodal sparse LLT + PADMM, one warp per world)")
+        note = ("operand-touch model of SURVEY.md §8d (the reference's dense algorithm); the factor and X are "
+                "shared-memory resident, so HBM is not the binding roof (see DESIGN.md)")
+    achieved = fam_bytes / (fam_ms / 1e3) / 1e9
+    worlds_in_launch = sum(v for k, v in kern_count.items() if (k == "cr") == (fam == "cr") and k != "none") / rsteps
+    traffic, traffic_src = ncu_traffic(kname.split(" ")[0], worlds_in_launch)
     d = b.diagnostics()
     rows_mean = float(np.mean([d[w].n_rows for w in range(W)]))
     from paper_2603_16536_b200 import sharding
@@ -309,30 +406,33 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline(args, scene, cfg, quick=True)
+            cpu = cpu_baseline(args, wl, cfg, quick=True)
         except Exception as ex:  # the oracle is test infrastructure; report, don't fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
 
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "dr_legs", "worlds_per_gpu": W, "global_worlds": total_worlds,
-                       "bodies": model.n_bodies, "joints": model.info.n_joints, "loops": model.n_loops,
+            "config": {"workload": args.workload, "baseline_config": wl[3], "worlds_per_gpu": W,
+                       "global_worlds": total_worlds, "models": [m.name for m in models],
+                       "bodies": [m.n_bodies for m in models], "joints": [m.info.n_joints for m in models],
+                       "loops": [m.n_loops for m in models],
                        "rows_mean": rows_mean, "padmm_iterations_mean": iters_mean, "dt": cfg.dt,
                        "integrator": cfg.integrator, "backend": cfg.backend, "settle_steps": args.settle,
+                       "kernels": {k: v / rsteps for k, v in kern_count.items()},
                        "jitter": "mt19937_64(seed=1), normal(0,1e-3) (main.cpp:199-211)",
-                       "l2": "working set (>300 MB/GPU of rows + factors) exceeds the 126 MB L2; no flush",
+                       "l2": "not flushed: per-step scratch (rows, factors, caches) of all worlds exceeds the "
+                             "126 MB L2",
                        "parallelism": f"worlds sharded over {ws} GPU(s), no data-path collective"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "dense_kernel (K2: Delassus assembly + Cholesky + PADMM, smem-resident)",
-                         "k2_ms_per_launch": k2_ms, "k2_share_of_step": k2_ms / step_ms_fam,
-                         "algorithmic_bytes_per_launch": bytes_k2 / rsteps,
-                         "path_bytes_per_step": bytes_path / rsteps,
-                         "note": "operand-touch model of BASELINE.md §3; the factor is smem-resident, so "
-                                 "HBM is not the binding roof (see DESIGN.md)",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_kind": peak_kind, "kernel": kname,
+                         "kernel_ms_per_launch": fam_ms, "kernel_share_of_step": fam_ms / step_ms_fam,
+                         "algorithmic_bytes_per_launch": fam_bytes,
+                         "path_bytes_per_step": bytes_path / rsteps if fam == "dense" else None,
+                         "note": note,
                          "fp64": {"achieved_tflops": flops / rsteps / (step_ms_fam / 1e3) / 1e12,
                                   "peak_tflops": 37.0, "peak_kind": "nominal B200 FP64"}},
             "clocks": clocks,

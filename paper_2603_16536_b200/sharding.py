@@ -35,6 +35,18 @@ def jitter_slice(initial_twists: np.ndarray, n_bodies: int, worlds: range, seed:
     return full[6 * n_bodies * worlds.start:].copy()
 
 
+def jitter_slice_mixed(world_twists, worlds: range, seed: int = 1, sigma: float = 1e-3):
+    """Heterogeneous batches: `world_twists(w)` gives global world w's initial
+    twists (6 per body); the stream runs over worlds [0, worlds.stop) in world
+    order (main.cpp:199-211) and the block `worlds` is kept."""
+    from .loopdyn import bench_jitter
+    per = [np.asarray(world_twists(w), dtype=np.float64).reshape(-1) for w in range(worlds.stop)]
+    nb = [p.size // 6 for p in per]
+    full = bench_jitter(np.concatenate(per), nb, seed=seed, sigma=sigma)
+    off = 6 * sum(nb[:worlds.start])
+    return full[off:].copy()
+
+
 def local_stats(diags, n_worlds: int) -> dict:
     """Per-step statistics of one rank's worlds (kd_step_diag array)."""
     its = [diags[w].iterations for w in range(n_worlds)]
