@@ -13,6 +13,8 @@
 // the roofline).
 #include "kd_device.cuh"
 
+#include <algorithm>
+
 namespace kd {
 
 namespace {
@@ -25,10 +27,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   __syncthreads();
   if (lane == 0) red[wid] = v;
   __syncthreads();
-  double s = red[0];
-#pragma unroll
-  for (int k = 1; k < NW; ++k) s += red[k];
-  return s;
+  // every warp reduces the NW partials with the same fixed butterfly
+  return warp_sum(lane < NW ? red[lane] : 0.0);
 }
 
 template <int NT>
@@ -45,15 +45,9 @@ __device__ __forceinline__ void block_max3(double& a, double& b, double& c, doub
     red[3 * wid + 2] = c;
   }
   __syncthreads();
-  a = red[0];
-  b = red[1];
-  c = red[2];
-#pragma unroll
-  for (int k = 1; k < NW; ++k) {
-    a = fmax(a, red[3 * k]);
-    b = fmax(b, red[3 * k + 1]);
-    c = fmax(c, red[3 * k + 2]);
-  }
+  a = warp_max(lane < NW ? red[3 * lane] : 0.0);  // residuals are >= 0
+  b = warp_max(lane < NW ? red[3 * lane + 1] : 0.0);
+  c = warp_max(lane < NW ? red[3 * lane + 2] : 0.0);
 }
 
 struct CrCtx {
@@ -66,35 +60,62 @@ struct CrCtx {
   const double* dadd;   // smem: P^2 R + (eta + rho)
   const double* binv;   // smem: per body [inv_mass, Iwinv(9)]
   double* scratch;      // smem: 6 nb
+  const double* ja;     // smem: P-scaled J rows (12 per row), or null (stream J from global)
+  const int32_t* rbs;   // smem copies of rb / cptr / clist when staged
+  const int32_t* cps;
+  const int32_t* cls;
 };
 
-// out = D_{eta,rho} v   (MatrixFreeDelassus::apply)
+// out = D_{eta,rho} v   (MatrixFreeDelassus::apply).  When the world's rows
+// fit, ja = P J (bake_jacobian's first product, delassus.cpp:130-154) and the
+// row/body index lists are staged in shared memory once per step, so an apply
+// reads no global memory; otherwise J streams from L2/HBM every apply.  Both
+// paths perform the same floating-point operations.
 template <int NT>
 __device__ void apply_op(const CrCtx& c, const double* v, double* out) {
   const int tid = threadIdx.x;
   __syncthreads();
-  for (int u = tid; u < 6 * c.nb; u += NT) {
-    const int b = u / 6, k = u - 6 * b;
-    double s = 0.0;
-    for (int e = c.cptr[b]; e < c.cptr[b + 1]; ++e) {
-      const int code = c.clist[e];
-      const int r = code >> 1;
-      s += (c.P[r] * c.rj[r].J[6 * (code & 1) + k]) * v[r];
+  if (c.ja) {
+    for (int u = tid; u < 6 * c.nb; u += NT) {
+      const int b = u / 6, k = u - 6 * b;
+      double s = 0.0;
+      const int e1 = c.cps[b + 1];
+      for (int e = c.cps[b]; e < e1; ++e) {
+        const int code = c.cls[e];
+        const int r = code >> 1;
+        s += c.ja[12 * r + 6 * (code & 1) + k] * v[r];
+      }
+      c.scratch[u] = s;
     }
-    c.scratch[u] = s;
+  } else {
+    for (int u = tid; u < 6 * c.nb; u += NT) {
+      const int b = u / 6, k = u - 6 * b;
+      double s = 0.0;
+      for (int e = c.cptr[b]; e < c.cptr[b + 1]; ++e) {
+        const int code = c.clist[e];
+        const int r = code >> 1;
+        s += (c.P[r] * c.rj[r].J[6 * (code & 1) + k]) * v[r];
+      }
+      c.scratch[u] = s;
+    }
   }
   __syncthreads();
   for (int r = tid; r < c.n; r += NT) {
     const double p = c.P[r];
     double s = c.dadd[r] * v[r];
     for (int side = 0; side < 2; ++side) {
-      const int b = c.rb[2 * r + side];
+      const int b = c.ja ? c.rbs[2 * r + side] : c.rb[2 * r + side];
       if (b < 0) continue;
-      const double* J = c.rj[r].J + 6 * side;
       const double* bi = c.binv + 10 * b;
       double ja[6];
+      if (c.ja) {
 #pragma unroll
-      for (int k = 0; k < 6; ++k) ja[k] = p * J[k];
+        for (int k = 0; k < 6; ++k) ja[k] = c.ja[12 * r + 6 * side + k];
+      } else {
+        const double* J = c.rj[r].J + 6 * side;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) ja[k] = p * J[k];
+      }
       // jma = fold_inverse_mass(ja) (delassus.cpp:12-17)
       double jm[6];
       jm[0] = ja[0] * bi[0];
@@ -138,8 +159,9 @@ __device__ __forceinline__ void project_soc(const double w[3], double mu, double
 
 }  // namespace
 
-template <int NT>
-__global__ void __launch_bounds__(NT, 1) cr_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds,
+                                                  int smem_doubles) {
   extern __shared__ __align__(16) double smem[];
   const int w = bin_worlds[blockIdx.x];
   WorldStep& ws = bv.wstep[w];
@@ -166,6 +188,12 @@ __global__ void __launch_bounds__(NT, 1) cr_kernel(BatchView bv, StepParams sp, 
   double* binv = vf + n;       // 10 nb
   double* scratch = binv + 10 * nb;  // 6 nb
   double* red = scratch + 6 * nb;    // 3 * NW
+  // optional staging (runtime n): ja[12 n] | int rb[2n] | cptr[nb+1] | clist[2n]
+  double* ja_s = red + 3 * (NT / 32) + 1;
+  int32_t* rb_s = reinterpret_cast<int32_t*>(ja_s + 12 * n);
+  int32_t* cp_s = rb_s + 2 * n;
+  int32_t* cl_s = cp_s + nb + 1;
+  const bool staged = (ja_s - smem) + 12 * n + (4 * n + nb + 2) / 2 + 1 <= smem_doubles;
 
   const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
   for (int r = tid; r < n; r += NT) {
@@ -181,8 +209,24 @@ __global__ void __launch_bounds__(NT, 1) cr_kernel(BatchView bv, StepParams sp, 
     binv[10 * b] = B.inv_mass;
     for (int k = 0; k < 9; ++k) binv[10 * b + 1 + k] = B.Iwinv[k];
   }
-  CrCtx c{n, nb, bv.rowj + R0, bv.rbody + 2 * R0, bv.csr_ptr + W.body_off + w, bv.csr + 2 * R0, P, dadd, binv,
-          scratch};
+  CrCtx c{n,       nb,      bv.rowj + R0, bv.rbody + 2 * R0, bv.csr_ptr + W.body_off + w, bv.csr + 2 * R0, P, dadd,
+          binv,    scratch, nullptr,      nullptr,           nullptr,                     nullptr};
+  if (staged) {
+    __syncthreads();  // P
+    const int32_t* cptr_g = bv.csr_ptr + W.body_off + w;
+    const int32_t* cl_g = bv.csr + 2 * R0;
+    for (int e = tid; e < 12 * n; e += NT) {
+      const int r = e / 12, k = e - 12 * r;
+      ja_s[e] = P[r] * bv.rowj[R0 + r].J[k];  // bake_jacobian: ja = P J
+    }
+    for (int e = tid; e < 2 * n; e += NT) rb_s[e] = bv.rbody[2 * R0 + e];
+    for (int b = tid; b <= nb; b += NT) cp_s[b] = cptr_g[b];
+    for (int e = tid; e < 2 * n; e += NT) cl_s[e] = cl_g[e];
+    c.ja = ja_s;
+    c.rbs = rb_s;
+    c.cps = cp_s;
+    c.cls = cl_s;
+  }
   const int n_jd = n - ws.n_limits - 3 * ws.n_contacts;
   const int first_contact = n_jd + ws.n_limits;
   const int n_units = first_contact + ws.n_contacts;
@@ -353,27 +397,38 @@ __global__ void __launch_bounds__(NT, 1) cr_kernel(BatchView bv, StepParams sp, 
 }
 
 size_t cr_smem_bytes(int n, int nb, int nt) { return 8 * ((size_t)13 * n + 16 * (size_t)nb + 3 * (nt / 32) + 8); }
+// with the optional per-step staging of P J and the index lists
+static size_t cr_staged_bytes(int n, int nb, int nt) {
+  return 8 * ((size_t)25 * n + 16 * (size_t)nb + 3 * (nt / 32) + 8 + ((size_t)4 * n + nb + 2) / 2 + 2);
+}
 
-template <int NT>
+template <int NT, int MINB>
 static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap,
                                int nbcap, cudaStream_t s) {
-  const size_t smem = cr_smem_bytes(ncap, nbcap, NT);
+  const size_t smem = std::max(cr_smem_bytes(ncap, nbcap, NT),
+                               std::min<size_t>(232448 / MINB, cr_staged_bytes(ncap, nbcap, NT)));
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(cr_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = cudaFuncSetAttribute(cr_kernel<NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  cr_kernel<NT><<<count, NT, smem, s>>>(bv, sp, worlds);
+  cr_kernel<NT, MINB><<<count, NT, smem, s>>>(bv, sp, worlds, (int)(smem / 8));
   return cudaGetLastError();
 }
 
 cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
                       int nt, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  if (nt <= 128) return launch_cr_t<128>(bv, sp, worlds, count, ncap, nbcap, s);
-  if (nt <= 256) return launch_cr_t<256>(bv, sp, worlds, count, ncap, nbcap, s);
-  return launch_cr_t<512>(bv, sp, worlds, count, ncap, nbcap, s);
+  // two resident CTAs per SM whenever their (staged) shared memory fits: the
+  // kernel is synchronisation/latency bound, so a second world hides it
+  if (cr_staged_bytes(ncap, nbcap, 256) <= 232448 / 2) {
+    if (nt <= 128) return launch_cr_t<128, 2>(bv, sp, worlds, count, ncap, nbcap, s);
+    return launch_cr_t<256, 2>(bv, sp, worlds, count, ncap, nbcap, s);
+  }
+  if (nt <= 128) return launch_cr_t<128, 1>(bv, sp, worlds, count, ncap, nbcap, s);
+  if (nt <= 256) return launch_cr_t<256, 1>(bv, sp, worlds, count, ncap, nbcap, s);
+  return launch_cr_t<512, 1>(bv, sp, worlds, count, ncap, nbcap, s);
 }
 
 }  // namespace kd

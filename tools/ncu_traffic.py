@@ -1,0 +1,28 @@
+"""Record dram traffic per world of a kernel from one `ncu --set full` capture
+into profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
+
+usage: python tools/ncu_traffic.py report.ncu-rep KERNEL_NAME WORLDS_IN_LAUNCH
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+rep, kernel, worlds = sys.argv[1], sys.argv[2], int(sys.argv[3])
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                      "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr, units, vals = rows[0], rows[1], rows[2]
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+tot = 0.0
+for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+    i = hdr.index(k)
+    tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+data = json.load(open(path)) if os.path.exists(path) else {}
+data[kernel] = {"bytes_per_world": tot / worlds, "bytes_per_launch": tot, "worlds_in_launch": worlds,
+                "source": os.path.basename(rep)}
+json.dump(data, open(path, "w"), indent=1)
+print(kernel, data[kernel])
