@@ -266,12 +266,13 @@ def run_reference(args):
     return 0
 
 
-def ncu_traffic(kernel, worlds_in_launch):
-    """dram bytes (read + write) per launch from the committed ncu capture
-    (profiles/ncu_traffic.json, per world), scaled to this launch's worlds."""
+def ncu_traffic(kernel, workload, worlds_in_launch):
+    """dram bytes (read + write) per launch from the committed ncu capture of
+    this kernel on this workload's model (profiles/ncu_traffic.json, per
+    world), scaled to this launch's worlds; None if there is no capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            rec = json.load(f)[kernel]
+            rec = json.load(f)[f"{kernel}@{workload}"]
         return rec["bytes_per_world"] * worlds_in_launch, rec["source"]
     except Exception:
         return None, None
@@ -369,7 +370,7 @@ def main():
                 "shared-memory resident, so HBM is not the binding roof (see DESIGN.md)")
     achieved = fam_bytes / (fam_ms / 1e3) / 1e9
     worlds_in_launch = sum(v for k, v in kern_count.items() if (k == "cr") == (fam == "cr") and k != "none") / rsteps
-    traffic, traffic_src = ncu_traffic(kname.split(" ")[0], worlds_in_launch)
+    traffic, traffic_src = ncu_traffic(kname.split(" ")[0], args.workload, worlds_in_launch)
     d = b.diagnostics()
     rows_mean = float(np.mean([d[w].n_rows for w in range(W)]))
     from paper_2603_16536_b200 import sharding
@@ -385,7 +386,8 @@ def main():
     if not args.no_e2e:
         p_all, t_all, tm_all = b.get_state()
         halves = []
-        H = (W + 1) // 2
+        # split only when each half still fills the GPU several times over
+        H = (W + 1) // 2 if W >= 8 * torch.cuda.get_device_properties(local).multi_processor_count else W
         for lo, hi in ((0, H), (H, W)):
             if hi <= lo:
                 continue

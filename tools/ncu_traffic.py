@@ -1,7 +1,7 @@
 """Record dram traffic per world of a kernel from one `ncu --set full` capture
 into profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
 
-usage: python tools/ncu_traffic.py report.ncu-rep KERNEL_NAME WORLDS_IN_LAUNCH
+usage: python tools/ncu_traffic.py report.ncu-rep KERNEL_NAME WORKLOAD WORLDS_IN_LAUNCH
 """
 import csv
 import io
@@ -10,7 +10,8 @@ import os
 import subprocess
 import sys
 
-rep, kernel, worlds = sys.argv[1], sys.argv[2], int(sys.argv[3])
+rep, kernel, workload, worlds = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+key = f"{kernel}@{workload}"
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                       "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -22,7 +23,7 @@ for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
     tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
 data = json.load(open(path)) if os.path.exists(path) else {}
-data[kernel] = {"bytes_per_world": tot / worlds, "bytes_per_launch": tot, "worlds_in_launch": worlds,
+data[key] = {"bytes_per_world": tot / worlds, "bytes_per_launch": tot, "worlds_in_launch": worlds,
                 "source": os.path.basename(rep)}
 json.dump(data, open(path, "w"), indent=1)
-print(kernel, data[kernel])
+print(key, data[key])
