@@ -136,26 +136,6 @@ __device__ void apply_op(const CrCtx& c, const double* v, double* out) {
   __syncthreads();
 }
 
-__device__ __forceinline__ void project_soc(const double w[3], double mu, double y[3]) {
-  const double wn = w[0];
-  const double tn = sqrt(w[1] * w[1] + w[2] * w[2]);
-  y[0] = w[0];
-  y[1] = w[1];
-  y[2] = w[2];
-  if (tn <= mu * wn) return;
-  if (mu * tn <= -wn) {
-    y[0] = y[1] = y[2] = 0.0;
-    return;
-  }
-  const double tau = (wn + mu * tn) / (1.0 + mu * mu);
-  y[0] = tau;
-  if (tn > 0) {
-    y[1] = mu * tau * w[1] / tn;
-    y[2] = mu * tau * w[2] / tn;
-  } else {
-    y[1] = y[2] = 0.0;
-  }
-}
 
 }  // namespace
 
@@ -196,6 +176,7 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
   const bool staged = (ja_s - smem) + 12 * n + (4 * n + nb + 2) / 2 + 1 <= smem_doubles;
 
   const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
+  const double inv_rho = 1.0 / rho;  // w = x - z_hat * (1/rho): no division in the loop
   for (int r = tid; r < n; r += NT) {
     const double p = bv.scale[R0 + r];
     P[r] = p;
@@ -242,7 +223,7 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
     } else {
       const int r = first_contact + 3 * (u - first_contact);
       double wv[3] = {xs[r], xs[r + 1], xs[r + 2]}, yn[3];
-      project_soc(wv, rmu[r], yn);
+      project_soc(wv, rmu[r], 1.0 / (1.0 + rmu[r] * rmu[r]), yn);
       for (int d = 0; d < 3; ++d) yv[r + d] = yn[d];
     }
   }
@@ -263,7 +244,7 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
     // rhs = -(v_f + s - eta x - rho y_hat - z_hat)
     for (int r = tid; r < n; r += NT) {
       double s = 0.0;
-      if (r >= first_contact && ((r - first_contact) % 3) == 0) s = rmu[r] * hypot(zh[r + 1], zh[r + 2]);
+      if (r >= first_contact && ((r - first_contact) % 3) == 0) s = rmu[r] * fast_sqrt(zh[r + 1] * zh[r + 1] + zh[r + 2] * zh[r + 2]);
       rhs[r] = -((((vf[r] + s) - eta * xs[r]) - rho * yh[r]) - zh[r]);
     }
     // ---- cr_solve(op, rhs, x, budget)
@@ -322,8 +303,8 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
       const int r = u < first_contact ? u : first_contact + 3 * (u - first_contact);
       const int nr = u < first_contact ? 1 : 3;
       double wv[3], yn[3];
-      for (int d = 0; d < nr; ++d) wv[d] = xs[r + d] - zh[r + d] / rho;
-      if (u >= first_contact) project_soc(wv, rmu[r], yn);
+      for (int d = 0; d < nr; ++d) wv[d] = xs[r + d] - zh[r + d] * inv_rho;
+      if (u >= first_contact) project_soc(wv, rmu[r], 1.0 / (1.0 + rmu[r] * rmu[r]), yn);
       else if (u >= n_jd) yn[0] = fmax(0.0, wv[0]);
       else yn[0] = wv[0];
       double ymax = 0.0, zmax = 0.0;

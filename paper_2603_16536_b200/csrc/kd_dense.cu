@@ -377,27 +377,6 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T) {
   __syncthreads();
 }
 
-// SOC projection of one contact triple (padmm.cpp:19-37)
-__device__ __forceinline__ void project_soc(const double w[3], double mu, double y[3]) {
-  const double wn = w[0];
-  const double tn = sqrt(w[1] * w[1] + w[2] * w[2]);
-  y[0] = w[0];
-  y[1] = w[1];
-  y[2] = w[2];
-  if (tn <= mu * wn) return;
-  if (mu * tn <= -wn) {
-    y[0] = y[1] = y[2] = 0.0;
-    return;
-  }
-  const double tau = (wn + mu * tn) / (1.0 + mu * mu);
-  y[0] = tau;
-  if (tn > 0) {
-    y[1] = mu * tau * w[1] / tn;
-    y[2] = mu * tau * w[2] / tn;
-  } else {
-    y[1] = y[2] = 0.0;
-  }
-}
 
 }  // namespace
 
@@ -581,7 +560,9 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   const int kind = !has_unit ? ROW_BILATERAL : (tid < n_jd ? ROW_BILATERAL : (tid < first_contact ? ROW_LIMIT : ROW_CONTACT));
   const int nr = !has_unit ? 0 : (kind == ROW_CONTACT ? 3 : 1);
   const double mu = has_unit ? bv.rmu[R0 + row0] : 0.0;
+  const double inv_1pmu2 = 1.0 / (1.0 + mu * mu);
   const double eta = sp.eta, rho = sp.rho;
+  const double inv_rho = 1.0 / rho;  // w = x - z_hat / rho as x - z_hat * (1/rho): no division in the loop
   double v[3] = {0, 0, 0}, x[3] = {0, 0, 0}, y[3] = {0, 0, 0}, z[3] = {0, 0, 0}, yh[3], zh[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
@@ -592,7 +573,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     }
   }
   // y = Pi_K(x0)
-  if (kind == ROW_CONTACT) project_soc(x, mu, y);
+  if (kind == ROW_CONTACT) project_soc(x, mu, inv_1pmu2, y);
   else if (kind == ROW_LIMIT) y[0] = fmax(0.0, x[0]);
   else y[0] = x[0];
 #pragma unroll
@@ -607,7 +588,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   const int hcap = bv.hist_cap;
   // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
   auto write_rhs = [&]() {
-    const double s0 = kind == ROW_CONTACT ? mu * hypot(zh[1], zh[2]) : 0.0;  // desaxce_shift (padmm.cpp:44-52)
+    const double s0 = kind == ROW_CONTACT ? mu * fast_sqrt(zh[1] * zh[1] + zh[2] * zh[2]) : 0.0;  // desaxce_shift (padmm.cpp:44-52)
 #pragma unroll
     for (int d = 0; d < 3; ++d)
       if (d < nr) xv[row0 + d] = -((((v[d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * yh[d]) - zh[d]);
@@ -620,11 +601,11 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       if (d < nr) x[d] = xv[row0 + d];
-      wv[d] = x[d] - zh[d] / rho;
+      wv[d] = x[d] - zh[d] * inv_rho;
       yp[d] = y[d];
       zp[d] = z[d];
     }
-    if (kind == ROW_CONTACT) project_soc(wv, mu, yn);
+    if (kind == ROW_CONTACT) project_soc(wv, mu, inv_1pmu2, yn);
     else {
       yn[0] = kind == ROW_LIMIT ? fmax(0.0, wv[0]) : wv[0];
       yn[1] = yn[2] = 0.0;

@@ -25,26 +25,6 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ __forceinline__ void project_soc(const double w[3], double mu, double y[3]) {  // padmm.cpp:19-37
-  const double wn = w[0];
-  const double tn = sqrt(w[1] * w[1] + w[2] * w[2]);
-  y[0] = w[0];
-  y[1] = w[1];
-  y[2] = w[2];
-  if (tn <= mu * wn) return;
-  if (mu * tn <= -wn) {
-    y[0] = y[1] = y[2] = 0.0;
-    return;
-  }
-  const double tau = (wn + mu * tn) / (1.0 + mu * mu);
-  y[0] = tau;
-  if (tn > 0) {
-    y[1] = mu * tau * w[1] / tn;
-    y[2] = mu * tau * w[2] / tn;
-  } else {
-    y[1] = y[2] = 0.0;
-  }
-}
 
 __device__ __forceinline__ int pad2(int x) { return (x + 1) & ~1; }
 
@@ -271,6 +251,7 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   // in the rhs pass on a restart, so no previous-iterate vectors are kept.
   const int n_units = first_contact + nc;
   const double eta = sp.eta, rho = sp.rho;
+  const double inv_rho = 1.0 / rho;  // w = x - z_hat * (1/rho): no division in the loop
   const double* rmu = bv.rmu + R0;
   for (int u = lane; u < n_units; u += 32) {
     const bool con = u >= first_contact;
@@ -286,10 +267,10 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
         z_s[r0 + d] = zz[d];
         zh_s[r0 + d] = zz[d];
       }
-    if (con) project_soc(x, rmu[r0], y);  // y = Pi_K(x0)
+    if (con) project_soc(x, rmu[r0], 1.0 / (1.0 + rmu[r0] * rmu[r0]), y);  // y = Pi_K(x0)
     else y[0] = u >= n_jd ? fmax(0.0, x[0]) : x[0];
     // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
-    const double s0 = con ? rmu[r0] * hypot(zz[1], zz[2]) : 0.0;
+    const double s0 = con ? rmu[r0] * fast_sqrt(zz[1] * zz[1] + zz[2] * zz[2]) : 0.0;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
       if (d < nr) {
@@ -363,9 +344,9 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
       for (int d = 0; d < 3; ++d)
         if (d < nr) {
           x[d] = v[row2pos[r0 + d]];
-          wv[d] = x[d] - zh_s[r0 + d] / rho;
+          wv[d] = x[d] - zh_s[r0 + d] * inv_rho;
         }
-      if (con) project_soc(wv, rmu[r0], yn);
+      if (con) project_soc(wv, rmu[r0], 1.0 / (1.0 + rmu[r0] * rmu[r0]), yn);
       else yn[0] = u >= n_jd ? fmax(0.0, wv[0]) : wv[0];
       double ymax = 0.0, zmax = 0.0;
 #pragma unroll
@@ -415,7 +396,7 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
           }
           zz[d] = zh_s[r0 + d];
         }
-      const double s0 = con ? rmu[r0] * hypot(zz[1], zz[2]) : 0.0;
+      const double s0 = con ? rmu[r0] * fast_sqrt(zz[1] * zz[1] + zz[2] * zz[2]) : 0.0;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
         if (d < nr) {
