@@ -15,10 +15,11 @@ iterations; settled steps ~35).
           (CUDA events on the solver's stream, state resident in HBM).
   e2e     same metric through the C-ABI with HOST state: every step uploads
           poses+twists from pinned host memory, steps, and downloads them.
-  roofline  dominant kernel (fused dense K2): algorithmic bytes per launch
-          (BASELINE.md §3 operand-touch model, the K2 terms, actual n and
-          PADMM iterations per world) / its average launch time, against the
-          measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  roofline  dominant kernel family: algorithmic bytes per launch (SURVEY §8d
+          models, actual n and PADMM iterations per world, from extra steps)
+          / its average launch time measured with CUDA events on the solver
+          stream during the timed region, against the measured HBM copy
+          bandwidth (MEASURED_PEAKS.json).
   cpu_baseline  the fp64 CPU oracle (oracle/, a restatement of the reference
           loopdyn solver; the reference itself cannot be built here: no Eigen)
           on the host's cores, same scene/config, a bounded world sample.
@@ -313,7 +314,9 @@ def main():
     sampler.start()
     time.sleep(0.3)
     barrier()
-    b.enable_timing(False)
+    # per-family CUDA events on the solver stream stay on through the timed
+    # region (recorded without synchronising, resolved after it)
+    b.enable_timing(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(ext)
     b.step_async(cfg, args.steps)
@@ -321,6 +324,8 @@ def main():
     b.sync()
     barrier()
     ms = e0.elapsed_time(e1)
+    tim_timed = b.timing()
+    b.enable_timing(False)
     clocks = sampler.stop()
     t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
     if dist is not None:
@@ -329,9 +334,8 @@ def main():
     total_worlds = W * ws
     value = total_worlds * args.steps / (ms_max / 1e3)
 
-    # ---- roofline pass: per-family device time (events on the batch stream) +
-    # per-world n, iterations and kernel of every step
-    b.enable_timing(True)
+    # ---- roofline pass: per-world n, iterations and kernel of a few more
+    # (statistically identical) steps for the algorithmic byte model
     rsteps = max(5, min(10, args.steps))
     bytes_dense = bytes_cr = bytes_path = flops = 0.0
     kern_count = {}
@@ -350,11 +354,12 @@ def main():
         bytes_cr += float((algorithmic_bytes_cr(n, nb_w, it, 2 * it + cri) * on_cr).sum())
         bytes_path += float((algorithmic_bytes_path(n, nb_w, it) * on_dense).sum())
         flops += float(algorithmic_flops(n, it).sum())
-    tim = b.timing()
-    launches_per_step = tim["launches"] / rsteps
-    dense_ms = tim["dense_ms"] / rsteps
-    cr_ms = tim["matrix_free_ms"] / rsteps
-    step_ms_fam = (tim["assemble_ms"] + tim["dense_ms"] + tim["matrix_free_ms"] + tim["recover_ms"]) / rsteps
+    # kernel-family times per step from the timed region itself
+    tim = tim_timed
+    launches_per_step = tim["launches"] / args.steps
+    dense_ms = tim["dense_ms"] / args.steps
+    cr_ms = tim["matrix_free_ms"] / args.steps
+    step_ms_fam = (tim["assemble_ms"] + tim["dense_ms"] + tim["matrix_free_ms"] + tim["recover_ms"]) / args.steps
     peak, peak_kind = measured_peaks()
     if cr_ms > dense_ms:
         fam, fam_ms, fam_bytes = "cr", cr_ms, bytes_cr / rsteps
@@ -376,7 +381,6 @@ def main():
     from paper_2603_16536_b200 import sharding
     run_stats = sharding.reduce_stats(dist, sharding.local_stats(d, W), device=f"cuda:{local}")
     iters_mean = run_stats["mean_iterations"]
-    b.enable_timing(False)
 
     # ---- end-to-end through the C-ABI with host (pinned) state buffers.  The
     # worlds are split into two half-batches on two streams, so one half's

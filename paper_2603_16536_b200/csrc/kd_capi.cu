@@ -102,11 +102,17 @@ struct kd_batch {
   int32_t* d_err = nullptr;
   bool timing = false;
   cudaEvent_t ev[6] = {};
+  // per-step family events recorded without synchronising: resolved lazily
+  // (kd_batch_get_timing / kd_batch_sync), so timing can stay on inside a
+  // timed region without perturbing it
+  std::vector<cudaEvent_t> evpool;  // 5 per step
+  size_t ev_used = 0, ev_done = 0;
   double ms[4] = {0, 0, 0, 0};
   int64_t launches = 0;
   ~kd_batch() {
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -682,8 +688,24 @@ int kd_batch_get_history(kd_batch* b, double* out) {
   return KD_OK;
 }
 
+static int resolve_timing(kd_batch* b) {
+  if (b->ev_done == b->ev_used) return KD_OK;
+  KD_CK(cudaEventSynchronize(b->evpool[b->ev_used - 1]));
+  for (size_t k = b->ev_done; k < b->ev_used; k += 5)
+    for (int i = 0; i < 4; ++i) {
+      float t = 0.f;
+      KD_CK(cudaEventElapsedTime(&t, b->evpool[k + i], b->evpool[k + i + 1]));
+      b->ms[i] += t;
+    }
+  b->ev_done = b->ev_used = 0;
+  return KD_OK;
+}
+
 int kd_batch_enable_timing(kd_batch* b, int32_t on) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
+  const int rc = resolve_timing(b);
+  if (rc != KD_OK) return rc;
   b->timing = on != 0;
   for (double& m : b->ms) m = 0.0;
   b->launches = 0;
@@ -692,6 +714,9 @@ int kd_batch_enable_timing(kd_batch* b, int32_t on) {
 
 int kd_batch_get_timing(kd_batch* b, double* ms4, int64_t* launches) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
+  const int rc = resolve_timing(b);
+  if (rc != KD_OK) return rc;
   if (ms4)
     for (int i = 0; i < 4; ++i) ms4[i] = b->ms[i];
   if (launches) *launches = b->launches;
@@ -722,9 +747,16 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
   const BatchView& v = b->view;
   cudaStream_t s = b->stream;
   auto mark = [&](int i) {
-    if (b->timing) cudaEventRecord(b->ev[i], s);
+    if (b->timing) cudaEventRecord(b->evpool[b->ev_used + i], s);
   };
   for (int k = 0; k < n_steps; ++k) {
+    if (b->timing) {
+      while (b->evpool.size() < b->ev_used + 5) {
+        cudaEvent_t e;
+        KD_CK(cudaEventCreate(&e));
+        b->evpool.push_back(e);
+      }
+    }
     mark(0);
     launch_assemble(v, sp, s);
     KD_CK(cudaGetLastError());
@@ -755,14 +787,7 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
     KD_CK(cudaGetLastError());
     ++b->launches;
     mark(4);
-    if (b->timing) {  // per-family device time, CUDA events on the batch stream
-      KD_CK(cudaEventSynchronize(b->ev[4]));
-      for (int i = 0; i < 4; ++i) {
-        float t = 0.f;
-        cudaEventElapsedTime(&t, b->ev[i], b->ev[i + 1]);
-        b->ms[i] += t;
-      }
-    }
+    if (b->timing) b->ev_used += 5;  // per-family device time, resolved lazily
   }
   return KD_OK;
 }
@@ -771,6 +796,10 @@ int kd_batch_sync(kd_batch* b) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
   KD_CK(cudaSetDevice(b->device));
   KD_CK(cudaStreamSynchronize(b->stream));
+  {
+    const int rc = resolve_timing(b);
+    if (rc != KD_OK) return rc;
+  }
   int32_t err[4];
   KD_CK(cudaMemcpy(err, b->d_err, 16, cudaMemcpyDeviceToHost));
   if (err[0]) return fail(KD_ERR_SPD_FAILURE, "Delassus factorization failed on an SPD system (" +
