@@ -210,6 +210,12 @@ int kd_batch_step(kd_batch* batch, const kd_step_config* cfg, int32_t n_steps);
 int kd_batch_step_async(kd_batch* batch, const kd_step_config* cfg, int32_t n_steps);
 int kd_batch_sync(kd_batch* batch);
 int kd_batch_stream(kd_batch* batch, void** stream);
+/* Zero-copy access to the device-resident state: device
+ * pointers to the pose (7 doubles per body) and twist (6 per body) storage in
+ * the WorldBatch layout (batch.hpp:41-42) and to the per-world time.  They
+ * stay valid for the batch's lifetime; work on them must be ordered with the
+ * batch stream (kd_batch_stream). */
+int kd_batch_device_state(kd_batch* batch, double** poses, double** twists, double** time);
 /* Async state copies with caller-provided (pinned) host buffers, on the batch stream. */
 int kd_batch_set_state_async(kd_batch* batch, const double* poses, const double* twists);
 int kd_batch_get_state_async(kd_batch* batch, double* poses, double* twists);

@@ -832,6 +832,14 @@ int kd_batch_stream(kd_batch* b, void** stream) {
   return KD_OK;
 }
 
+int kd_batch_device_state(kd_batch* b, double** poses, double** twists, double** time) {
+  if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  if (poses) *poses = b->view.poses;
+  if (twists) *twists = b->view.twists;
+  if (time) *time = b->view.time;
+  return KD_OK;
+}
+
 int kd_batch_set_state_async(kd_batch* b, const double* poses, const double* twists) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
   if (poses && b->pose_len)

@@ -295,6 +295,26 @@ class WorldBatch:
         _check(lib().kd_batch_stream(self.handle, C.byref(s)))
         return s.value or 0
 
+    def device_state(self):
+        """Zero-copy views of the device-resident state for PyTorch (RL
+        wrappers, PAPER §2 Warp<->PyTorch interop): (poses [pose_len],
+        twists [twist_len], time [n_worlds]) as float64 CUDA tensors sharing
+        the batch's memory (__cuda_array_interface__).  Order work on them with
+        the batch stream (`torch.cuda.ExternalStream(batch.stream())`)."""
+        import torch
+        self._ensure()
+        p, t, tm = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib().kd_batch_device_state(self.handle, C.byref(p), C.byref(t), C.byref(tm)))
+
+        class _View:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                                 "version": 3, "strides": None, "stream": None}
+        dev = torch.device("cuda", self.device)
+        return (torch.as_tensor(_View(p.value, self.pose_len), device=dev),
+                torch.as_tensor(_View(t.value, self.twist_len), device=dev),
+                torch.as_tensor(_View(tm.value, self.n_worlds), device=dev))
+
     def set_state_async(self, poses, twists):
         """Host->device state copy on the batch stream (pass pinned buffers)."""
         _check(lib().kd_batch_set_state_async(self.handle, _capi.dptr(poses), _capi.dptr(twists)))
