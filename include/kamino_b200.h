@@ -216,6 +216,18 @@ int kd_batch_stream(kd_batch* batch, void** stream);
  * stay valid for the batch's lifetime; work on them must be ordered with the
  * batch stream (kd_batch_stream). */
 int kd_batch_device_state(kd_batch* batch, double** poses, double** twists, double** time);
+
+/* Batched forward kinematics on the device (fk_solve, fk.hpp:33; SURVEY §8f
+ * rank 2): for every active world, Gauss-Newton with Levenberg damping on
+ * [bilateral f; coordinate - target] from the world's current poses, which
+ * are overwritten with the result (twists and time untouched).  joints /
+ * values are n_worlds x n_targets (joint index, target coordinate) per world;
+ * tolerance / max_iters / lm_initial are FkConfig (fk.hpp:19-23).  Per-world
+ * outputs (each may be NULL): iterations, residual_inf, converged.  Models with
+ * more than 36 bodies return KD_ERR_CAPACITY (the normal matrix must fit in
+ * one CTA's shared memory). */
+int kd_batch_fk(kd_batch* batch, const int32_t* joints, const double* values, int32_t n_targets, double tolerance,
+                int32_t max_iters, double lm_initial, int32_t* iterations, double* residual_inf, uint8_t* converged);
 /* Async state copies with caller-provided (pinned) host buffers, on the batch stream. */
 int kd_batch_set_state_async(kd_batch* batch, const double* poses, const double* twists);
 int kd_batch_get_state_async(kd_batch* batch, double* poses, double* twists);

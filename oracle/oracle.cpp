@@ -1712,4 +1712,146 @@ void batch_step(WorldBatch& batch, const StepConfig& cfg, int n_threads) {
   for (std::thread& t : pool) t.join();
 }
 
+// ---------------------------------------------------------------- fk (fk.cpp:7-106)
+namespace {
+
+// fk_residual (fk.cpp:9-24): [bilateral f; coordinate - target], revolute
+// differences wrapped with std::remainder(d, 2 pi).
+Vec fk_residual(const MechanismModel& m, const std::vector<std::pair<int, double>>& targets,
+                const std::vector<Pose>& poses) {
+  Vec r = build_bilateral(m, poses).f;
+  for (const auto& [joint, target] : targets) {
+    double d = joint_coordinate(m, joint, poses) - target;
+    if (m.joints[joint].type == JointType::Revolute) d = std::remainder(d, 2.0 * M_PI);
+    r.push_back(d);
+  }
+  return r;
+}
+
+// fk_jacobian (fk.cpp:28-52): rows x 6 nb, the angular block of each
+// world-frame row post-multiplied by R_i (local chart, q <- q exp(delta/2)).
+std::vector<double> fk_jacobian(const MechanismModel& m, const std::vector<std::pair<int, double>>& targets,
+                                const std::vector<Pose>& poses, int& n_rows) {
+  const BilateralBlock bb = build_bilateral(m, poses);
+  const int nf = (int)bb.rows.size(), nt = (int)targets.size(), nc = 6 * m.n_bodies();
+  n_rows = nf + nt;
+  std::vector<double> j((size_t)n_rows * nc, 0.0);
+  auto scatter = [&](int out, const JacobianRow& row) {
+    for (int side = 0; side < 2; ++side) {
+      const int b = side == 0 ? row.body_a : row.body_b;
+      if (b < 0) continue;
+      const Row6& blk = side == 0 ? row.block_a : row.block_b;
+      const Mat3 rot = poses[b].rotation();
+      double* dst = j.data() + (size_t)out * nc + 6 * b;
+      for (int k = 0; k < 3; ++k) dst[k] = blk[k];
+      for (int c = 0; c < 3; ++c) dst[3 + c] = blk[3] * rot(0, c) + blk[4] * rot(1, c) + blk[5] * rot(2, c);
+    }
+  };
+  for (int r = 0; r < nf; ++r) scatter(r, bb.rows[r]);
+  for (int k = 0; k < nt; ++k) scatter(nf + k, coordinate_rate_row(m, targets[k].first, poses));
+  return j;
+}
+
+// apply_update (fk.cpp:54-62)
+std::vector<Pose> fk_apply_update(const std::vector<Pose>& poses, const Vec& delta) {
+  std::vector<Pose> out = poses;
+  for (size_t b = 0; b < out.size(); ++b) {
+    out[b].position = out[b].position + Vec3{delta[6 * b], delta[6 * b + 1], delta[6 * b + 2]};
+    out[b].orientation = (out[b].orientation * quat_exp(Vec3{0.5 * delta[6 * b + 3], 0.5 * delta[6 * b + 4],
+                                                             0.5 * delta[6 * b + 5]}))
+                             .normalized();
+  }
+  return out;
+}
+
+double norm2(const Vec& v) {
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return std::sqrt(s);
+}
+double norm_inf(const Vec& v) {
+  double s = 0.0;
+  for (double x : v) s = std::max(s, std::abs(x));
+  return s;
+}
+
+}  // namespace
+
+FkResult fk_solve(const MechanismModel& m, const std::vector<std::pair<int, double>>& targets,
+                  const std::vector<Pose>& initial_poses, const FkConfig& cfg) {
+  FkResult res;
+  res.poses = initial_poses;
+  Vec r = fk_residual(m, targets, res.poses);
+  double r_norm = norm2(r);
+  res.residual_inf = norm_inf(r);
+  if (res.residual_inf < cfg.tolerance) {
+    res.converged = true;
+    return res;  // already consistent, poses untouched
+  }
+  const int nc = 6 * m.n_bodies();
+  double lm = cfg.lm_initial;
+  for (int iter = 0; iter < cfg.max_iters; ++iter) {
+    res.iterations = iter + 1;
+    int nr = 0;
+    const std::vector<double> j = fk_jacobian(m, targets, res.poses, nr);
+    // normal = J^T J + lm I ; g = -J^T r
+    std::vector<double> a((size_t)nc * nc, 0.0);
+    Vec g(nc, 0.0);
+    for (int p = 0; p < nc; ++p) {
+      for (int q = 0; q <= p; ++q) {
+        double s = 0.0;
+        for (int k = 0; k < nr; ++k) s += j[(size_t)k * nc + p] * j[(size_t)k * nc + q];
+        a[(size_t)p * nc + q] = s;
+      }
+      a[(size_t)p * nc + p] += lm;
+      double t = 0.0;
+      for (int k = 0; k < nr; ++k) t += j[(size_t)k * nc + p] * r[k];
+      g[p] = -t;
+    }
+    // unblocked LLT (lower) and the two substitutions
+    bool spd = true;
+    for (int c = 0; c < nc && spd; ++c) {
+      double d = a[(size_t)c * nc + c];
+      for (int k = 0; k < c; ++k) d -= a[(size_t)c * nc + k] * a[(size_t)c * nc + k];
+      if (!(d > 0.0)) spd = false;
+      d = std::sqrt(d);
+      a[(size_t)c * nc + c] = d;
+      for (int i = c + 1; i < nc; ++i) {
+        double v = a[(size_t)i * nc + c];
+        for (int k = 0; k < c; ++k) v -= a[(size_t)i * nc + k] * a[(size_t)c * nc + k];
+        a[(size_t)i * nc + c] = v / d;
+      }
+    }
+    if (!spd) break;
+    Vec delta = g;
+    for (int i = 0; i < nc; ++i) {
+      for (int k = 0; k < i; ++k) delta[i] -= a[(size_t)i * nc + k] * delta[k];
+      delta[i] /= a[(size_t)i * nc + i];
+    }
+    for (int i = nc - 1; i >= 0; --i) {
+      for (int k = i + 1; k < nc; ++k) delta[i] -= a[(size_t)k * nc + i] * delta[k];
+      delta[i] /= a[(size_t)i * nc + i];
+    }
+    const std::vector<Pose> cand = fk_apply_update(res.poses, delta);
+    const Vec r_c = fk_residual(m, targets, cand);
+    const double cn = norm2(r_c);
+    if (cn < r_norm) {
+      res.poses = cand;
+      r = r_c;
+      r_norm = cn;
+      res.residual_inf = norm_inf(r);
+      lm = std::max(lm / 10.0, 1e-12);
+      if (res.residual_inf < cfg.tolerance) {
+        res.converged = true;
+        return res;
+      }
+    } else {
+      lm *= 10.0;
+      if (lm > 1e10) break;  // stuck; report the best iterate
+    }
+  }
+  res.converged = res.residual_inf < cfg.tolerance;
+  return res;
+}
+
 }  // namespace oracle

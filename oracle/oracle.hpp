@@ -526,4 +526,23 @@ class WorldBatch {
 };
 void batch_step(WorldBatch& batch, const StepConfig& cfg, int n_threads = 0);
 
+// ---------------------------------------------------------------- fk (fk.hpp:13-33, fk.cpp)
+struct FkConfig {
+  double tolerance = 1e-8;  // on |r|_inf
+  int max_iters = 100;
+  double lm_initial = 1e-6;  // Levenberg damping: x10 on reject, /10 on accept
+};
+struct FkResult {
+  std::vector<Pose> poses;
+  double residual_inf = 0.0;
+  int iterations = 0;
+  bool converged = false;
+};
+// Gauss-Newton with Levenberg damping on [bilateral f; coordinate - target].
+// The reference solves the normal equations with Eigen's LDLT; the oracle
+// uses an unblocked LLT (SPD thanks to the damping), so agreement with Eigen
+// itself is to rounding, not bits.
+FkResult fk_solve(const MechanismModel& m, const std::vector<std::pair<int, double>>& targets,
+                  const std::vector<Pose>& initial_poses, const FkConfig& cfg = {});
+
 }  // namespace oracle

@@ -456,4 +456,32 @@ int or_batch_dump_limits(void* bp, int32_t w, int32_t* keys2, int32_t cap, int32
   return KD_OK;
 }
 
+// fk_solve (fk.cpp) on one world: poses7 in/out (nb x 7), targets (joint, value).
+int or_fk_solve(const void* mp, const int32_t* joints, const double* values, int32_t n_targets, double* poses7,
+                double tol, int32_t max_iters, double lm_initial, double* residual_inf, int32_t* iterations,
+                int32_t* converged) {
+  const MechanismModel& m = *static_cast<const OrModel*>(mp)->m;
+  std::vector<std::pair<int, double>> t;
+  for (int k = 0; k < n_targets; ++k) t.push_back({joints[k], values[k]});
+  FkConfig cfg;
+  cfg.tolerance = tol;
+  cfg.max_iters = max_iters;
+  cfg.lm_initial = lm_initial;
+  try {
+    const FkResult r = fk_solve(m, t, poses_from(m, poses7), cfg);
+    for (int b = 0; b < m.n_bodies(); ++b) {
+      const Pose& p = r.poses[b];
+      double* o = poses7 + 7 * b;
+      o[0] = p.position.x, o[1] = p.position.y, o[2] = p.position.z;
+      o[3] = p.orientation.w, o[4] = p.orientation.x, o[5] = p.orientation.y, o[6] = p.orientation.z;
+    }
+    *residual_inf = r.residual_inf;
+    *iterations = r.iterations;
+    *converged = r.converged ? 1 : 0;
+    return KD_OK;
+  } catch (const ModelError& e) {
+    return fail(e.code + 1, e.what());
+  }
+}
+
 }  // extern "C"

@@ -1671,6 +1671,130 @@ TEST(acc8_energy, "acceptance.cpp:281 #8 pendulum energy: euler < 2%, moreau <= 
   CHECK(mj <= eu);
 }
 
+// ---------------------------------------------------------------- fk (test_fk.cpp)
+namespace {
+std::vector<Pose> fk_initial(const MechanismModel& m) {
+  std::vector<Pose> p;
+  for (const BodySpec& b : m.bodies) p.push_back(b.initial_pose);
+  return p;
+}
+double body_plane_angle(const Pose& pose) {  // test_fk.cpp:26-30
+  const Vec3 x_axis = pose.orientation * Vec3{1, 0, 0};
+  return std::atan2(x_axis.y, x_axis.x);
+}
+// oracles::solve_fourbar (oracles.hpp:61-79), branch +1
+bool solve_fourbar(double crank_angle, double& coupler_angle, double& rocker_angle, double ground = 2.0,
+                   double crank = 0.5, double coupler = 2.0, double rocker = 1.5) {
+  const double ax = crank * std::cos(crank_angle), ay = crank * std::sin(crank_angle);
+  const double dx = ground - ax, dy = -ay;
+  const double d = std::sqrt(dx * dx + dy * dy);
+  if (d > coupler + rocker || d < std::abs(coupler - rocker)) return false;
+  const double alpha = (d * d + coupler * coupler - rocker * rocker) / (2.0 * d);
+  const double h = std::sqrt(std::max(0.0, coupler * coupler - alpha * alpha));
+  const double ux = dx / d, uy = dy / d;
+  const double bx = ax + alpha * ux - h * uy, by = ay + alpha * uy + h * ux;
+  coupler_angle = std::atan2(by - ay, bx - ax);
+  rocker_angle = std::atan2(by, bx - ground);
+  return true;
+}
+}  // namespace
+
+TEST(fk_consistent, "test_fk.cpp:33 fk on an already-consistent input returns immediately, poses untouched") {
+  const MechanismModel m = build_model(load("fourbar").scene);
+  const std::vector<Pose> init = fk_initial(m);
+  const FkResult r = fk_solve(m, {{0, joint_coordinate(m, 0, init)}}, init);
+  CHECK(r.converged);
+  CHECK(r.iterations == 0);
+  for (size_t b = 0; b < r.poses.size(); ++b) {
+    CHECK(r.poses[b].position.x == init[b].position.x && r.poses[b].position.y == init[b].position.y &&
+          r.poses[b].position.z == init[b].position.z);
+    CHECK(r.poses[b].orientation.w == init[b].orientation.w && r.poses[b].orientation.z == init[b].orientation.z);
+  }
+}
+
+TEST(fk_two_link, "test_fk.cpp:49 fk on a serial two-link chain matches composed transforms") {
+  SceneDescription s;
+  for (int i = 0; i < 2; ++i) {
+    SceneBody b;
+    b.name = "link" + std::to_string(i);
+    b.inertia = Mat3::identity();
+    b.inertia(0, 0) = 1e-4;
+    b.inertia(1, 1) = 0.02;
+    b.inertia(2, 2) = 0.02;
+    b.pose.position = Vec3{0.5 + i, 0.0, 0.0};
+    s.bodies.push_back(b);
+  }
+  SceneJoint j0;
+  j0.name = "q0";
+  j0.type = "revolute";
+  j0.parent = "world";
+  j0.child = "link0";
+  j0.frame_in_child.position = Vec3{-0.5, 0, 0};
+  j0.axis = Vec3{0, 0, 1};
+  s.joints.push_back(j0);
+  SceneJoint j1 = j0;
+  j1.name = "q1";
+  j1.parent = "link0";
+  j1.child = "link1";
+  j1.frame_in_parent.position = Vec3{0.5, 0, 0};
+  s.joints.push_back(j1);
+  const MechanismModel m = build_model(s);
+  const double q0 = 0.4, q1 = -0.9;
+  const FkResult r = fk_solve(m, {{0, q0}, {1, q1}}, fk_initial(m));
+  REQUIRE(r.converged);
+  CHECK(r.residual_inf < 1e-8);
+  const Vec3 elbow{std::cos(q0), std::sin(q0), 0.0};
+  const Vec3 com0 = 0.5 * elbow;
+  const Vec3 com1 = elbow + 0.5 * Vec3{std::cos(q0 + q1), std::sin(q0 + q1), 0.0};
+  CHECK(norm(r.poses[0].position - com0) < 1e-7);
+  CHECK(norm(r.poses[1].position - com1) < 1e-7);
+  CHECK(approx(body_plane_angle(r.poses[0]), q0, 1e-7));
+  CHECK(approx(body_plane_angle(r.poses[1]), q0 + q1, 1e-7));
+}
+
+TEST(fk_fourbar, "test_fk.cpp:95 fk on the four-bar matches the analytic position solution") {
+  const MechanismModel m = build_model(load("fourbar").scene);
+  for (double delta : {0.1, 0.4, -0.3, 0.9}) {
+    const double crank = M_PI / 2 + delta;
+    const FkResult r = fk_solve(m, {{0, crank}}, fk_initial(m));
+    REQUIRE(r.converged);
+    CHECK(r.residual_inf < 1e-8);
+    double ca = 0, ra = 0;
+    REQUIRE(solve_fourbar(crank, ca, ra));
+    CHECK(approx(body_plane_angle(r.poses[1]), ca, 1e-6));
+    CHECK(approx(body_plane_angle(r.poses[2]), ra, 1e-6));
+  }
+}
+
+TEST(fk_no_close, "test_fk.cpp:114 fk flags non-convergence when the loop cannot close") {
+  const json j = json::parse(R"json({
+    "name": "fourbar_long_crank", "gravity": [0, -9.81, 0],
+    "bodies": [
+      {"name": "crank", "mass": 1.0, "inertia": [1e-4, 0.2, 0.2],
+       "position": [0.0, 0.75, 0.0], "orientation": [0.7071067811865476, 0, 0, 0.7071067811865476]},
+      {"name": "coupler", "mass": 1.0, "inertia": [1e-4, 0.1, 0.1],
+       "position": [0.43014417303072305, 1.2450961153538151, 0.0],
+       "orientation": [0.964439823436757, 0.0, 0.0, -0.26430252925251585]},
+      {"name": "rocker", "mass": 1.0, "inertia": [1e-4, 0.1, 0.1],
+       "position": [0.930144173030723, 0.49509611535381526, 0.0],
+       "orientation": [0.6558537741224968, 0.0, 0.0, 0.7548879565665867]}],
+    "joints": [
+      {"name": "crank_pivot", "type": "revolute", "parent": "world", "child": "crank",
+       "parent_position": [0, 0, 0], "child_position": [-0.75, 0, 0], "axis": [0, 0, 1]},
+      {"name": "crank_coupler", "type": "revolute", "parent": "crank", "child": "coupler",
+       "parent_position": [0.75, 0, 0], "child_position": [-0.5, 0, 0], "axis": [0, 0, 1]},
+      {"name": "coupler_rocker", "type": "revolute", "parent": "coupler", "child": "rocker",
+       "parent_position": [0.5, 0, 0], "child_position": [0.5, 0, 0], "axis": [0, 0, 1]},
+      {"name": "rocker_ground", "type": "revolute", "parent": "world", "child": "rocker",
+       "parent_position": [1, 0, 0], "child_position": [-0.5, 0, 0], "axis": [0, 0, 1]}],
+    "geoms": []})json");
+  const MechanismModel m = build_model(scene_from_json(j).scene);
+  const FkResult r = fk_solve(m, {{0, M_PI}}, fk_initial(m));
+  CHECK(!r.converged);
+  CHECK(r.residual_inf > 1e-3);
+  CHECK((int)r.poses.size() == m.n_bodies());
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::fprintf(stderr, "usage: %s scenes_bundle.json [filter]\n", argv[0]);

@@ -220,6 +220,8 @@ KD_ONLY = {
     "batch_get_state_async": (C.c_int, [_H, c_double_p, c_double_p]),
     "abi_sizes": (C.c_int, [c_int32_p, C.c_int32]),
     "batch_get_kernels": (C.c_int, [_H, c_int32_p]),
+    "batch_fk": (C.c_int, [_H, c_int32_p, c_double_p, C.c_int32, C.c_double, C.c_int32, C.c_double, c_int32_p,
+                           c_double_p, c_uint8_p]),
     "batch_device_state": (C.c_int, [_H, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "model_sparse_plan_info": (C.c_int, [_H, c_int64_p]),
     "model_sparse_plan_selftest": (C.c_int, [_H, C.c_uint64, c_double_p]),

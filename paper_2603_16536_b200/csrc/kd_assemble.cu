@@ -17,92 +17,11 @@
 // the reference.  Work per world is small (~10^4 flops), so 8 worlds share a
 // 256-thread CTA and the grid covers the batch once.
 #include "kd_device.cuh"
+#include "kd_joint.cuh"
 
 namespace kd {
 
 namespace {
-
-struct Frames {
-  V3 ap, ac;  // anchors
-  M3 Rp, Rc;  // joint frames in world
-};
-
-// joint_world_frames (model.cpp:309-324)
-__device__ __forceinline__ Frames joint_frames(const DevJoint& j, const BodyS* bs) {
-  Frames f;
-  if (j.parent < 0) {
-    f.ap = ld3(j.fp_pos);
-    f.Rp = ldm(j.fp_R);
-  } else {
-    const BodyS& p = bs[j.parent];
-    f.ap = add(ld3(p.ep), qapply(ldq(p.eq), ld3(j.fp_pos)));
-    f.Rp = mmul(ldm(p.eR), ldm(j.fp_R));
-  }
-  const BodyS& c = bs[j.child];
-  f.ac = add(ld3(c.ep), qapply(ldq(c.eq), ld3(j.fc_pos)));
-  f.Rc = mmul(ldm(c.eR), ldm(j.fc_R));
-  return f;
-}
-
-// joint_coordinate (model.cpp:326-340)
-__device__ __forceinline__ double joint_coord(const DevJoint& j, const Frames& f) {
-  if (j.type == J_REVOLUTE) {
-    Q4 rel = qfrom(mmul(mtrans(f.Rp), f.Rc));
-    if (rel.w < 0) rel = Q4{-rel.w, -rel.x, -rel.y, -rel.z};
-    return 2.0 * atan2(dot(ld3(j.axis), V3{rel.x, rel.y, rel.z}), rel.w);
-  }
-  return dot(ld3(j.axis), mvec(mtrans(f.Rp), sub(f.ac, f.ap)));
-}
-
-__device__ __forceinline__ void put_row(RowJ* rj, int32_t* rb, int r, int ba, int bb, V3 al, V3 aa, V3 bl, V3 ba3) {
-  double* J = rj[r].J;
-  J[0] = al.x; J[1] = al.y; J[2] = al.z; J[3] = aa.x; J[4] = aa.y; J[5] = aa.z;
-  J[6] = bl.x; J[7] = bl.y; J[8] = bl.z; J[9] = ba3.x; J[10] = ba3.y; J[11] = ba3.z;
-  rb[2 * r] = ba;
-  rb[2 * r + 1] = bb;
-}
-
-// JacobianRow::dot (constraints.hpp:25-30)
-__device__ __forceinline__ double row_dot(const double* J, int ba, int bb, const double* u) {
-  double s = 0.0;
-  if (ba >= 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) t += J[k] * u[6 * ba + k];
-    s += t;
-  }
-  if (bb >= 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) t += J[6 + k] * u[6 * bb + k];
-    s += t;
-  }
-  return s;
-}
-
-// coordinate_rate_row (constraints.cpp:160-187): returns blocks via out params.
-__device__ __forceinline__ void rate_row(const DevJoint& j, const Frames& f, const BodyS* bs, V3& al, V3& aa, V3& bl,
-                                         V3& bang) {
-  const V3 axis_w = mvec(f.Rp, ld3(j.axis));
-  const V3 z{0, 0, 0};
-  if (j.type == J_REVOLUTE) {
-    al = z;
-    aa = axis_w;
-    bl = z;
-    bang = (j.parent >= 0) ? neg(axis_w) : z;
-  } else {
-    const V3 lever = sub(f.ac, ld3(bs[j.child].ep));
-    al = axis_w;
-    aa = vmat(neg(axis_w), skew(lever));
-    if (j.parent >= 0) {
-      bl = neg(axis_w);
-      bang = vmat(axis_w, skew(sub(f.ac, ld3(bs[j.parent].ep))));
-    } else {
-      bl = z;
-      bang = z;
-    }
-  }
-}
 
 // One contact of the narrow phase.
 struct CP {
@@ -281,27 +200,11 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
     if (ji < M.nj) {
       j = mj[ji];
       fr = joint_frames(j, bs);
-      const M3 wpt = mtrans(fr.Rp);
       const int child = j.child;
-      const V3 lever_c = sub(fr.ac, ld3(bs[child].ep));
-      const V3 f_pos = mvec(wpt, sub(fr.ac, fr.ap));
-      const M3 c_ang = mmul(mscl(-1.0, wpt), skew(lever_c));
-      M3 p_lin = mzero(), p_ang = mzero();
-      if (j.parent >= 0) {
-        p_lin = mscl(-1.0, wpt);
-        p_ang = mmul(wpt, skew(sub(fr.ac, ld3(bs[j.parent].ep))));
-      }
       const int pb = j.parent;
-      V3 f_rot{0, 0, 0};
-      M3 r_ang = mzero();
-      if (j.type != J_SPHERICAL) {
-        const M3 rel = mmul(wpt, fr.Rc);
-        f_rot = so3_log(rel);
-        r_ang = mmul(left_jacobian_inverse(f_rot), wpt);
-      }
       const V3 z3{0, 0, 0};
       int r = j.row_offset;
-      auto emit = [&](V3 al, V3 aa, V3 bl, V3 bang, double fval) {
+      joint_bilateral_rows(j, fr, bs, [&](V3 al, V3 aa, V3 bl, V3 bang, double fval) {
         put_row(rj, rb, r, child, pb, al, aa, pb >= 0 ? bl : z3, pb >= 0 ? bang : z3);
         rk[r] = ROW_BILATERAL;
         rmu[r] = 0.0;
@@ -309,45 +212,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
         bias[r] = fmin(fmax(-bgain * fval, -sp.bias_clamp), sp.bias_clamp);  // clamp_abs
         f_inf = fmax(f_inf, fabs(fval));
         ++r;
-      };
-      auto emit_pos = [&](int k) { emit(mrow(wpt, k), mrow(c_ang, k), mrow(p_lin, k), mrow(p_ang, k), comp(f_pos, k)); };
-      auto emit_rot = [&](int k) { emit(z3, mrow(r_ang, k), z3, neg(mrow(r_ang, k)), comp(f_rot, k)); };
-      // push_combined (constraints.cpp:77-87): weights^T applied to a 3-row block
-      auto emit_comb = [&](bool pos, const double* wv) {
-        V3 al{0, 0, 0}, aa{0, 0, 0}, bl{0, 0, 0}, bang{0, 0, 0};
-        for (int k = 0; k < 3; ++k) {
-          const double wk = wv[k];
-          if (pos) {
-            al = add(al, scl(wk, mrow(wpt, k)));
-            aa = add(aa, scl(wk, mrow(c_ang, k)));
-            bl = add(bl, scl(wk, mrow(p_lin, k)));
-            bang = add(bang, scl(wk, mrow(p_ang, k)));
-          } else {
-            aa = add(aa, scl(wk, mrow(r_ang, k)));
-            bang = add(bang, scl(wk, neg(mrow(r_ang, k))));
-          }
-        }
-        emit(al, aa, bl, bang, dot(ld3(wv), pos ? f_pos : f_rot));
-      };
-      switch (j.type) {
-        case J_FIXED:
-          for (int k = 0; k < 3; ++k) emit_pos(k);
-          for (int k = 0; k < 3; ++k) emit_rot(k);
-          break;
-        case J_REVOLUTE:
-          for (int k = 0; k < 3; ++k) emit_pos(k);
-          emit_comb(false, j.comp0);
-          emit_comb(false, j.comp1);
-          break;
-        case J_PRISMATIC:
-          emit_comb(true, j.comp0);
-          emit_comb(true, j.comp1);
-          for (int k = 0; k < 3; ++k) emit_rot(k);
-          break;
-        default:
-          for (int k = 0; k < 3; ++k) emit_pos(k);
-          break;
-      }
+      });
       // coordinate (limited or actuated scalar joints), dynamics rows
       const bool scalar = j.type == J_REVOLUTE || j.type == J_PRISMATIC;
       double coord = 0.0;

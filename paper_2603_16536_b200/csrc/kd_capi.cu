@@ -840,6 +840,55 @@ int kd_batch_device_state(kd_batch* b, double** poses, double** twists, double**
   return KD_OK;
 }
 
+int kd_batch_fk(kd_batch* b, const int32_t* joints, const double* values, int32_t nt, double tol, int32_t max_iters,
+                double lm0, int32_t* iterations, double* residual_inf, uint8_t* converged) {
+  if (!b || nt < 0 || (nt > 0 && (!joints || !values))) return fail(KD_ERR_INVALID_ARGUMENT, "invalid arguments");
+  if (b->n_worlds == 0) return KD_OK;
+  KD_CK(cudaSetDevice(b->device));
+  size_t smem = 0;
+  for (int w = 0; w < b->n_worlds; ++w) {
+    const HostModel& m = b->models[b->world_model[w]];
+    for (int k = 0; k < nt; ++k) {
+      const int j = joints[(size_t)w * nt + k];
+      if (j < 0 || j >= (int)m.joints.size()) return fail(KD_ERR_INVALID_ARGUMENT, "target joint index out of range");
+      const int t = m.joints[j].type;
+      if (t != J_REVOLUTE && t != J_PRISMATIC)
+        return fail(KD_ERR_MODEL_WRONG_JOINT_TYPE, "joint '" + m.joint_names[j] + "' has no scalar coordinate");
+    }
+    smem = std::max(smem, fk_smem_bytes((int)m.bodies.size(), m.n_bil + nt));
+  }
+  if (smem > 232448) return fail(KD_ERR_CAPACITY, "forward kinematics: model too large for one CTA's shared memory");
+  const size_t n = (size_t)b->n_worlds * std::max(1, nt);
+  int32_t* d_j = nullptr;
+  double* d_v = nullptr;
+  int32_t* d_it = nullptr;
+  double* d_res = nullptr;
+  uint8_t* d_conv = nullptr;
+  KD_CK(cudaMalloc(&d_j, 4 * n));
+  KD_CK(cudaMalloc(&d_v, 8 * n));
+  KD_CK(cudaMalloc(&d_it, 4 * (size_t)b->n_worlds));
+  KD_CK(cudaMalloc(&d_res, 8 * (size_t)b->n_worlds));
+  KD_CK(cudaMalloc(&d_conv, (size_t)b->n_worlds));
+  int rc = KD_OK;
+  if (nt > 0) {
+    KD_CK(cudaMemcpyAsync(d_j, joints, 4 * (size_t)b->n_worlds * nt, cudaMemcpyHostToDevice, b->stream));
+    KD_CK(cudaMemcpyAsync(d_v, values, 8 * (size_t)b->n_worlds * nt, cudaMemcpyHostToDevice, b->stream));
+  }
+  cudaError_t e = launch_fk(b->view, d_j, d_v, nt, tol, max_iters, lm0, d_it, d_res, d_conv, smem, b->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(b->stream);
+  if (e == cudaSuccess && iterations) e = cudaMemcpy(iterations, d_it, 4 * (size_t)b->n_worlds, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && residual_inf)
+    e = cudaMemcpy(residual_inf, d_res, 8 * (size_t)b->n_worlds, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && converged) e = cudaMemcpy(converged, d_conv, (size_t)b->n_worlds, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) rc = fail(KD_ERR_CUDA, std::string("kd_batch_fk: ") + cudaGetErrorString(e));
+  cudaFree(d_j);
+  cudaFree(d_v);
+  cudaFree(d_it);
+  cudaFree(d_res);
+  cudaFree(d_conv);
+  return rc;
+}
+
 int kd_batch_set_state_async(kd_batch* b, const double* poses, const double* twists) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
   if (poses && b->pose_len)

@@ -295,6 +295,30 @@ class WorldBatch:
         _check(lib().kd_batch_stream(self.handle, C.byref(s)))
         return s.value or 0
 
+    def fk(self, joints, values, tolerance=1e-8, max_iters=100, lm_initial=1e-6):
+        """Batched forward kinematics on the device (fk_solve, fk.hpp:33):
+        every active world's poses are moved to satisfy its joints' loop
+        closures plus the targets.  `joints` / `values`: [n_worlds, n_targets]
+        (a 1-D sequence is applied to every world).  Returns (iterations,
+        residual_inf, converged) per world."""
+        self._ensure()
+        j = np.asarray(joints, dtype=np.int32)
+        v = np.asarray(values, dtype=np.float64)
+        if j.ndim == 1:
+            j = np.tile(j, (self.n_worlds, 1))
+        if v.ndim == 1:
+            v = np.tile(v, (self.n_worlds, 1))
+        j, v = np.ascontiguousarray(j), np.ascontiguousarray(v)
+        nt = j.shape[1] if j.ndim == 2 else 0
+        it = np.zeros(max(1, self.n_worlds), np.int32)
+        res = np.zeros(max(1, self.n_worlds))
+        conv = np.zeros(max(1, self.n_worlds), np.uint8)
+        _check(lib().kd_batch_fk(self.handle, _capi.i32ptr(j), _capi.dptr(v), nt, float(tolerance), int(max_iters),
+                                 float(lm_initial), _capi.i32ptr(it), _capi.dptr(res),
+                                 conv.ctypes.data_as(_capi.c_uint8_p)))
+        n = self.n_worlds
+        return it[:n], res[:n], conv[:n].astype(bool)
+
     def device_state(self):
         """Zero-copy views of the device-resident state for PyTorch (RL
         wrappers, PAPER §2 Warp<->PyTorch interop): (poses [pose_len],

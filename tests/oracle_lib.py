@@ -39,6 +39,9 @@ def lib():
             "batch_get_history": (C.c_int, [C.c_void_p, C.c_int32, _capi.c_double_p]),
             "batch_energy": (C.c_int, [C.c_void_p, C.c_int32, _capi.c_double_p, _capi.c_double_p]),
             "fd_check": (C.c_double, [C.c_void_p, _capi.c_double_p, C.c_double]),
+            "fk_solve": (C.c_int, [C.c_void_p, _capi.c_int32_p, _capi.c_double_p, C.c_int32, _capi.c_double_p,
+                                   C.c_double, C.c_int32, C.c_double, _capi.c_double_p, _capi.c_int32_p,
+                                   _capi.c_int32_p]),
         })
     return _lib
 
@@ -82,6 +85,16 @@ class OracleModel:
         p = np.ascontiguousarray(poses7, dtype=np.float64)
         _check(lib().or_joint_coordinate(self.handle, joint, _capi.dptr(p), C.byref(out)))
         return out.value
+
+    def fk(self, joints, values, poses7, tolerance=1e-8, max_iters=100, lm_initial=1e-6):
+        """fk_solve (fk.cpp) on one world; returns (poses7, iterations, residual_inf, converged)."""
+        j = np.ascontiguousarray(joints, dtype=np.int32)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        p = np.array(poses7, dtype=np.float64).reshape(-1)
+        res, it, conv = C.c_double(), C.c_int32(), C.c_int32()
+        _check(lib().or_fk_solve(self.handle, _capi.i32ptr(j), _capi.dptr(v), len(j), _capi.dptr(p), tolerance,
+                                 max_iters, lm_initial, C.byref(res), C.byref(it), C.byref(conv)))
+        return p, it.value, res.value, bool(conv.value)
 
     def fd_check(self, poses7, step=1e-5):
         p = np.ascontiguousarray(poses7, dtype=np.float64)
