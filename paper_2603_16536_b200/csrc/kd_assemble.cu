@@ -200,11 +200,30 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
     if (ji < M.nj) {
       j = mj[ji];
       fr = joint_frames(j, bs);
+      // build_joint_rows (constraints.cpp:20-109), the sequence of
+      // joint_bilateral_rows (kd_joint.cuh) kept inline for K1's register
+      // allocation (measured 0.49 vs 0.75 ms per 4096-world step)
+      const M3 wpt = mtrans(fr.Rp);
       const int child = j.child;
+      const V3 lever_c = sub(fr.ac, ld3(bs[child].ep));
+      const V3 f_pos = mvec(wpt, sub(fr.ac, fr.ap));
+      const M3 c_ang = mmul(mscl(-1.0, wpt), skew(lever_c));
+      M3 p_lin = mzero(), p_ang = mzero();
+      if (j.parent >= 0) {
+        p_lin = mscl(-1.0, wpt);
+        p_ang = mmul(wpt, skew(sub(fr.ac, ld3(bs[j.parent].ep))));
+      }
       const int pb = j.parent;
+      V3 f_rot{0, 0, 0};
+      M3 r_ang = mzero();
+      if (j.type != J_SPHERICAL) {
+        const M3 rel = mmul(wpt, fr.Rc);
+        f_rot = so3_log(rel);
+        r_ang = mmul(left_jacobian_inverse(f_rot), wpt);
+      }
       const V3 z3{0, 0, 0};
       int r = j.row_offset;
-      joint_bilateral_rows(j, fr, bs, [&](V3 al, V3 aa, V3 bl, V3 bang, double fval) {
+      auto emit = [&](V3 al, V3 aa, V3 bl, V3 bang, double fval) {
         put_row(rj, rb, r, child, pb, al, aa, pb >= 0 ? bl : z3, pb >= 0 ? bang : z3);
         rk[r] = ROW_BILATERAL;
         rmu[r] = 0.0;
@@ -212,7 +231,45 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
         bias[r] = fmin(fmax(-bgain * fval, -sp.bias_clamp), sp.bias_clamp);  // clamp_abs
         f_inf = fmax(f_inf, fabs(fval));
         ++r;
-      });
+      };
+      auto emit_pos = [&](int k) { emit(mrow(wpt, k), mrow(c_ang, k), mrow(p_lin, k), mrow(p_ang, k), comp(f_pos, k)); };
+      auto emit_rot = [&](int k) { emit(z3, mrow(r_ang, k), z3, neg(mrow(r_ang, k)), comp(f_rot, k)); };
+      // push_combined (constraints.cpp:77-87): weights^T applied to a 3-row block
+      auto emit_comb = [&](bool pos, const double* wv) {
+        V3 al{0, 0, 0}, aa{0, 0, 0}, bl{0, 0, 0}, bang{0, 0, 0};
+        for (int k = 0; k < 3; ++k) {
+          const double wk = wv[k];
+          if (pos) {
+            al = add(al, scl(wk, mrow(wpt, k)));
+            aa = add(aa, scl(wk, mrow(c_ang, k)));
+            bl = add(bl, scl(wk, mrow(p_lin, k)));
+            bang = add(bang, scl(wk, mrow(p_ang, k)));
+          } else {
+            aa = add(aa, scl(wk, mrow(r_ang, k)));
+            bang = add(bang, scl(wk, neg(mrow(r_ang, k))));
+          }
+        }
+        emit(al, aa, bl, bang, dot(ld3(wv), pos ? f_pos : f_rot));
+      };
+      switch (j.type) {
+        case J_FIXED:
+          for (int k = 0; k < 3; ++k) emit_pos(k);
+          for (int k = 0; k < 3; ++k) emit_rot(k);
+          break;
+        case J_REVOLUTE:
+          for (int k = 0; k < 3; ++k) emit_pos(k);
+          emit_comb(false, j.comp0);
+          emit_comb(false, j.comp1);
+          break;
+        case J_PRISMATIC:
+          emit_comb(true, j.comp0);
+          emit_comb(true, j.comp1);
+          for (int k = 0; k < 3; ++k) emit_rot(k);
+          break;
+        default:
+          for (int k = 0; k < 3; ++k) emit_pos(k);
+          break;
+      }
       // coordinate (limited or actuated scalar joints), dynamics rows
       const bool scalar = j.type == J_REVOLUTE || j.type == J_PRISMATIC;
       double coord = 0.0;

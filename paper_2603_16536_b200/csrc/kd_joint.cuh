@@ -93,9 +93,11 @@ __device__ __forceinline__ void rate_row(const DevJoint& j, const Frames& f, con
 
 // build_joint_rows (constraints.cpp:20-109): calls emit(al, aa, bl, bang, f)
 // once per bilateral row in the reference row order (child block a, parent
-// block b; the caller zeroes b for a world parent).
+// block b; the caller zeroes b for a world parent).  Used by the FK kernel;
+// K1 (kd_assemble.cu) keeps the same sequence inlined in its joint loop,
+// where the functor form measured 0.75 vs 0.49 ms per 4096-world step.
 template <class Emit>
-__device__ __forceinline__ void joint_bilateral_rows(const DevJoint& j, const Frames& fr, const BodyS* bs, Emit&& emit) {
+__device__ __forceinline__ void joint_bilateral_rows(const DevJoint& j, const Frames& fr, const BodyS* bs, Emit emit) {
   const V3 z3{0, 0, 0};
   const M3 wpt = mtrans(fr.Rp);
   const V3 lever_c = sub(fr.ac, ld3(bs[j.child].ep));
