@@ -109,10 +109,25 @@ struct kd_batch {
   size_t ev_used = 0, ev_done = 0;
   double ms[4] = {0, 0, 0, 0};
   int64_t launches = 0;
+  // one step captured as a CUDA graph and replayed for multi-step calls
+  // (launch-bound small batches); re-captured when the step parameters or
+  // the batch view change
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  StepParams graph_sp{};
+  int graph_backend = -1, graph_launches = 0;
+  bool graphs = true;
+  void drop_graph() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (graph) cudaGraphDestroy(graph);
+    graph_exec = nullptr;
+    graph = nullptr;
+  }
   ~kd_batch() {
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+    drop_graph();
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -304,6 +319,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     const char* e = getenv("KD_SPARSE");
     b->sparse_mode = e ? (e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1)) : 1;
     b->sparse = b->sparse_mode != 0;
+    const char* g = getenv("KD_GRAPHS");  // KD_GRAPHS=0: launch every kernel directly
+    b->graphs = !(g && g[0] == '0');
   }
   b->n_worlds = n_worlds;
   // model tables
@@ -669,6 +686,7 @@ int kd_batch_set_active(kd_batch* b, const uint8_t* active) {
 }
 
 int kd_batch_set_history_capacity(kd_batch* b, int32_t cap) {
+  if (b) b->drop_graph();  // the captured kernels hold the old history pointer
   if (!b || cap < 0) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
   KD_CK(cudaSetDevice(b->device));
   double* h = nullptr;
@@ -723,7 +741,7 @@ int kd_batch_get_timing(kd_batch* b, double* ms4, int64_t* launches) {
   return KD_OK;
 }
 
-static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
+static StepParams step_params(const kd_batch* b, const kd_step_config* c) {
   StepParams sp{};
   sp.dt = c->dt;
   sp.eta = c->eta;
@@ -744,12 +762,17 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
   sp.moreau = c->integrator == KD_INTEGRATOR_MOREAU_JEAN;
   sp.backend = c->backend;
   sp.sparse = b->sparse ? 1 : 0;
+  return sp;
+}
+
+// One step's launches: K1 -> K2s bins -> K2 bins -> K2g -> K2b -> K3.
+static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& sp) {
   const BatchView& v = b->view;
   cudaStream_t s = b->stream;
   auto mark = [&](int i) {
     if (b->timing) cudaEventRecord(b->evpool[b->ev_used + i], s);
   };
-  for (int k = 0; k < n_steps; ++k) {
+  {
     if (b->timing) {
       while (b->evpool.size() < b->ev_used + 5) {
         cudaEvent_t e;
@@ -788,6 +811,45 @@ static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) 
     ++b->launches;
     mark(4);
     if (b->timing) b->ev_used += 5;  // per-family device time, resolved lazily
+  }
+  return KD_OK;
+}
+
+static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
+  const StepParams sp = step_params(b, c);
+  if (!b->graphs || b->timing || n_steps < 2) {
+    for (int k = 0; k < n_steps; ++k) {
+      const int rc = enqueue_one(b, c, sp);
+      if (rc != KD_OK) return rc;
+    }
+    return KD_OK;
+  }
+  if (!b->graph_exec || std::memcmp(&b->graph_sp, &sp, sizeof(sp)) != 0 || b->graph_backend != c->backend) {
+    b->drop_graph();
+    const int64_t l0 = b->launches;
+    int rc = enqueue_one(b, c, sp);  // direct first step (also sets the kernels' smem attributes)
+    if (rc != KD_OK) return rc;
+    --n_steps;
+    const int64_t l1 = b->launches;
+    KD_CK(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_one(b, c, sp);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(b->stream, &g);
+    if (rc != KD_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    KD_CK(e);
+    b->graph = g;
+    KD_CK(cudaGraphInstantiate(&b->graph_exec, g, 0));
+    b->launches = l1;  // the captured step has not run yet
+    b->graph_launches = (int)(l1 - l0);
+    b->graph_sp = sp;
+    b->graph_backend = c->backend;
+  }
+  for (int k = 0; k < n_steps; ++k) {
+    KD_CK(cudaGraphLaunch(b->graph_exec, b->stream));
+    b->launches += b->graph_launches;
   }
   return KD_OK;
 }
