@@ -283,11 +283,13 @@ int kd_batch_get_phase_cycles(kd_batch* batch, int64_t* out);
 /* Diagnostics: which device kernel solved each world's last step:
  * KD_KERNEL_NONE (inactive / no rows), KD_KERNEL_DENSE (fused dense LLT, shared
  * or global factor), KD_KERNEL_SUPERNODAL (sparse LLT with the model's plan),
+ * KD_KERNEL_SUPERNODAL_DENSE (the plan's sparse factor, then the dense kernel),
  * KD_KERNEL_CR (matrix-free Conjugate Residual). */
 #define KD_KERNEL_NONE 0
 #define KD_KERNEL_DENSE 1
 #define KD_KERNEL_SUPERNODAL 2
 #define KD_KERNEL_CR 3
+#define KD_KERNEL_SUPERNODAL_DENSE 4 /* supernodal factor handed to the dense kernel's L^{-1} + solves */
 int kd_batch_get_kernels(kd_batch* batch, int32_t* out);
 
 /* Supernodal sparse-LLT plan of a model (the factorization the device uses for

@@ -35,8 +35,8 @@ KD_INTEGRATOR_MOREAU_JEAN = 1
 KD_BACKEND_DENSE = 0
 KD_BACKEND_MATRIX_FREE = 1
 KD_BACKEND_AUTO = 2
-KD_KERNEL_NONE, KD_KERNEL_DENSE, KD_KERNEL_SUPERNODAL, KD_KERNEL_CR = 0, 1, 2, 3
-KERNEL_NAMES = {0: 'none', 1: 'dense', 2: 'supernodal', 3: 'cr'}
+KD_KERNEL_NONE, KD_KERNEL_DENSE, KD_KERNEL_SUPERNODAL, KD_KERNEL_CR, KD_KERNEL_SUPERNODAL_DENSE = 0, 1, 2, 3, 4
+KERNEL_NAMES = {0: 'none', 1: 'dense', 2: 'supernodal', 3: 'cr', 4: 'supernodal+dense'}
 
 
 class kd_body_desc(C.Structure):

@@ -543,8 +543,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
       const bool dense = sp.backend == 0 /*KD_BACKEND_DENSE*/ || (sp.backend == 2 /*AUTO*/ && n <= 300);
       be = dense ? (n <= W.smem_cap ? BE_DENSE_SMEM : BE_DENSE_GLOBAL) : BE_MATRIX_FREE;
       // the dense LLT is factored by the supernodal kernel when the model has a
-      // plan and every active contact lies in a planned slot (kd_snplan.h)
-      if (dense && sn_ok && !overflow) be = BE_SPARSE;
+      // plan and every active contact lies in a planned slot (kd_snplan.h);
+      // for larger plans the factor is handed to the dense kernel (BE_DENSE_SN)
+      if (dense && sn_ok && !overflow) be = M.sn == 2 ? BE_DENSE_SN : BE_SPARSE;
       if (be == BE_DENSE_GLOBAL && n > W.slab_cap) overflow = true;
     }
     if (overflow) {

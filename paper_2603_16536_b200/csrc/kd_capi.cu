@@ -97,6 +97,8 @@ struct kd_batch {
   std::vector<SnBin> sn_bins;
   bool sparse = true;
   int sparse_mode = 1;
+  bool sn_handoff = true;
+  int64_t total_snlv = 0, total_snr2p = 0;
   int hist_cap = 0;
   double* d_hist = nullptr;
   int32_t* d_err = nullptr;
@@ -319,6 +321,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     const char* e = getenv("KD_SPARSE");
     b->sparse_mode = e ? (e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1)) : 1;
     b->sparse = b->sparse_mode != 0;
+    const char* h = getenv("KD_SN_HANDOFF");
+    b->sn_handoff = !(h && h[0] == '0');
     const char* g = getenv("KD_GRAPHS");  // KD_GRAPHS=0: launch every kernel directly
     b->graphs = !(g && g[0] == '0');
   }
@@ -354,9 +358,17 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     // wins on small systems (measured 2.1x on fourbar, 1.9x on double_fourbar);
     // on larger ones (serial_chain_10, DR-Legs) the fused dense kernel's
     // parallel explicit-inverse solves win (tests/kernel_ab.py).
-    d.sn = (b->sparse && m.sn && (b->sparse_mode == 2 || m.sn->S <= kSnAutoMaxSlots) &&
-            (size_t)m.sn->smem_doubles * 8 + (((size_t)m.sn->prog.size() * 4 + 15) & ~(size_t)15) <= kSnMaxSmem)
-               ? 1 : 0;
+    // Larger planned models (S <= the dense kernel's shared-memory rows) use
+    // the hand-off: the supernodal kernel factors D in the plan's order (38k
+    // FMA instead of 1.8M for DR-Legs, several worlds per SM) and the dense
+    // kernel forms L^-1 and runs the PADMM solves (KD_SN_HANDOFF=0 disables).
+    const bool sn_fits =
+        m.sn && (size_t)m.sn->smem_doubles * 8 + (((size_t)m.sn->prog.size() * 4 + 15) & ~(size_t)15) <= kSnMaxSmem;
+    d.sn = 0;
+    if (b->sparse && sn_fits) {
+      if (b->sparse_mode == 2 || m.sn->S <= kSnAutoMaxSlots) d.sn = 1;
+      else if (b->sn_handoff && m.sn->S <= kSmemMaxRows) d.sn = 2;
+    }
     for (int k = 0; k < 3; ++k) d.gravity[k] = m.gravity[k];
     bodies.insert(bodies.end(), m.bodies.begin(), m.bodies.end());
     joints.insert(joints.end(), m.joints.begin(), m.joints.end());
@@ -398,6 +410,14 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     class_worlds[cls].push_back(w);
     W.slab_cap = 0;
     W.lslab_off = -1;
+    W.snlv_off = -1;
+    W.snr2p_off = -1;
+    if (dm[mi].sn == 2) {
+      W.snlv_off = b->total_snlv;
+      b->total_snlv += (m.sn->nLv + 1) & ~1;
+      W.snr2p_off = b->total_snr2p;
+      b->total_snr2p += m.sn->S;
+    }
     if (rc > kSmemMaxRows) {
       W.slab_cap = std::min(rc, kDenseGlobalMaxRows);
       W.lslab_off = b->total_lslab;
@@ -437,8 +457,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     if (!dm[i].sn) continue;
     kd_batch::SnBin sbn;
     sbn.model = i;
-    sbn.per_warp = b->models[i].sn->smem_doubles;
-    sbn.prog_words = (int)b->models[i].sn->prog.size();
+    const bool hand = dm[i].sn == 2;  // factor only: no solve program, smaller per-warp layout
+    sbn.per_warp = hand ? b->models[i].sn->smem_doubles_h : b->models[i].sn->smem_doubles;
+    sbn.prog_words = hand ? 0 : (int)b->models[i].sn->prog.size();
     const size_t prog_bytes = ((size_t)sbn.prog_words * 4 + 15) & ~(size_t)15;
     sbn.wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (kSnMaxSmem - prog_bytes) / (8 * (size_t)sbn.per_warp)));
     for (int w = 0; w < n_worlds; ++w)
@@ -516,6 +537,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
   KD_CK(mem.alloc(v.ls_z, b->total_lslots));
   KD_CK(mem.alloc(v.ls_valid, b->total_lslots));
   KD_CK(mem.alloc(v.lslab, b->total_lslab));
+  KD_CK(mem.alloc(v.sn_lv, b->total_snlv));
+  KD_CK(mem.alloc(v.sn_r2p, b->total_snr2p));
   KD_CK(mem.alloc(b->d_hist, 1));
   KD_CK(mem.alloc(b->d_err, 4));
   v.hist = b->d_hist;
@@ -544,6 +567,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     std::vector<DevSnPlan> dp(n_models);
     std::vector<SnGram> gram;
     std::vector<SnSuper> sups;
+    std::vector<int32_t> prow;
     std::vector<SnGBody> gbody;
     std::vector<uint32_t> tmap, prog, gslot, gpair;
     std::vector<int32_t> pslot;
@@ -559,6 +583,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       d.lim_base = p.lim_base;
       d.smem_doubles = p.smem_doubles;
       d.max_slots = p.max_slots;
+      d.vreg_h = p.vreg_h;
       d.n_sph = p.n_sph;
       d.gram_off = (int)gram.size();
       d.n_gram = (int)p.gram.size();
@@ -583,11 +608,13 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       }
       d.sup_off = (int)sups.size();
       d.n_sup = (int)p.sup.size();
-      const int to = (int)tmap.size();
+      const int to = (int)tmap.size(), po = (int)prow.size();
       for (SnSuper u : p.sup) {
         u.tmap_off += to;
+        u.prow_off += po;
         sups.push_back(u);
       }
+      prow.insert(prow.end(), p.prow.begin(), p.prow.end());
       tmap.insert(tmap.end(), p.tmap.begin(), p.tmap.end());
       while (prog.size() & 3) prog.push_back(0);  // 16-byte aligned blobs
       d.prog_off = (int)prog.size();
@@ -612,6 +639,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     KD_CK(up(v.sn_prog, prog));
     KD_CK(up(v.sn_pair_slot, pslot));
     KD_CK(up(v.sn_slot_pos, spos));
+    KD_CK(up(v.sn_prow, prow));
   }
   for (cudaEvent_t& e : b->ev) KD_CK(cudaEventCreate(&e));
   KD_CK(cudaDeviceSynchronize());
@@ -762,6 +790,7 @@ static StepParams step_params(const kd_batch* b, const kd_step_config* c) {
   sp.moreau = c->integrator == KD_INTEGRATOR_MOREAU_JEAN;
   sp.backend = c->backend;
   sp.sparse = b->sparse ? 1 : 0;
+  sp.sn_handoff = b->sn_handoff ? 1 : 0;
   return sp;
 }
 
@@ -1006,7 +1035,7 @@ int kd_batch_get_phase_cycles(kd_batch* b, int64_t* out) {
   if (b->n_worlds)
     KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
   for (int w = 0; w < b->n_worlds; ++w)
-    for (int k = 0; k < 8; ++k) out[8 * w + k] = (ws[w].backend == BE_DENSE_SMEM || ws[w].backend == BE_SPARSE) ? ws[w].phase_cycles[k] : 0;
+    for (int k = 0; k < 8; ++k) out[8 * w + k] = (ws[w].backend == BE_DENSE_SMEM || ws[w].backend == BE_SPARSE || ws[w].backend == BE_DENSE_SN) ? ws[w].phase_cycles[k] : 0;
   return KD_OK;
 }
 
@@ -1020,6 +1049,7 @@ int kd_batch_get_kernels(kd_batch* b, int32_t* out) {
     const int be = ws[w].backend;
     out[w] = be == BE_SPARSE ? KD_KERNEL_SUPERNODAL
              : (be == BE_DENSE_SMEM || be == BE_DENSE_GLOBAL) ? KD_KERNEL_DENSE
+             : be == BE_DENSE_SN ? KD_KERNEL_SUPERNODAL_DENSE
              : be == BE_MATRIX_FREE ? KD_KERNEL_CR : KD_KERNEL_NONE;
   }
   return KD_OK;

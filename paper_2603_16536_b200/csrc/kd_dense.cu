@@ -135,6 +135,39 @@ __device__ __noinline__ void diag_factor_invert(double* T, int rk, int lane, int
   __syncwarp();
 }
 
+// Overwrite a packed lower diagonal tile that holds L_rc (c < r) and 1/L_rr on
+// its diagonal (the supernodal factor's hand-off format) with L_kk^{-1}; the
+// same column-parallel substitution as the second half of diag_factor_invert.
+__device__ __noinline__ void diag_invert_rinv(double* T, int rk, int lane) {
+  const double my_rinv = lane < rk ? T[tri(lane) + lane] : 1.0;
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const double rr = __shfl_sync(FULL, my_rinv, r);
+    if (r < rk) {
+      double s0 = (lane == r) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      const double* row = T + tri(r);
+#pragma unroll
+      for (int k = 0; k + 3 < r; k += 4) {
+        s0 -= row[k] * a[k];
+        s1 -= row[k + 1] * a[k + 1];
+        s2 -= row[k + 2] * a[k + 2];
+        s3 -= row[k + 3] * a[k + 3];
+      }
+#pragma unroll
+      for (int k = r & ~3; k < r; ++k) s0 -= row[k] * a[k];
+      a[r] = (lane <= r) ? ((s0 + s1) + (s2 + s3)) * rr : 0.0;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 32; ++r)
+    if (r < rk && lane <= r) T[tri(r) + lane] = a[r];
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------- DMMA tile products
 // One warp computes a 32x32 tile product with FP64 tensor-core MMAs
 // (mma.sync m8n8k4 f64: 256 FMA per instruction; tcgen05 has no fp64 kind).
@@ -385,11 +418,14 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   extern __shared__ __align__(16) double smem[];
   const int w = bin_worlds[blockIdx.x];
   WorldStep& ws = bv.wstep[w];
-  if (ws.backend != (GLOBAL_L ? BE_DENSE_GLOBAL : BE_DENSE_SMEM)) return;
+  // BE_DENSE_SN: the supernodal kernel already factored D in its plan's order
+  // (kd_sparse.cu); this CTA forms L^-1 in that order and runs the solves
+  const bool handoff = !GLOBAL_L && ws.backend == BE_DENSE_SN;
+  if (!handoff && ws.backend != (GLOBAL_L ? BE_DENSE_GLOBAL : BE_DENSE_SMEM)) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = NT / 32;
   const DevWorld W = bv.worlds[w];
-  const int n = ws.n_rows;
+  const int n = handoff ? bv.snplan[W.model].S : ws.n_rows;  // hand-off: every planned slot
   const int T = (n + 31) >> 5;
   const int nlen = tile_row_base(T - 1) + (T - 1) * LDT * tile_rows(T - 1, n) + tri(tile_rows(T - 1, n));
   const int npad = 32 * T;
@@ -416,13 +452,40 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     }
   };
   if (tid == 0) fail = 0;
-  for (int r = tid; r < n; r += NT) {
-    P[r] = bv.scale[R0 + r];
-    rbs[2 * r] = rb[2 * r];
-    rbs[2 * r + 1] = rb[2 * r + 1];
+  if (handoff) {  // rbs holds the row -> plan position map; b is zero at unused positions
+    for (int r = tid; r < ws.n_rows; r += NT) rbs[r] = bv.sn_r2p[W.snr2p_off + r];
+    for (int r = tid; r < npad; r += NT) xv[r] = 0.0;
+  } else {
+    for (int r = tid; r < n; r += NT) {
+      P[r] = bv.scale[R0 + r];
+      rbs[2 * r] = rb[2 * r];
+      rbs[2 * r + 1] = rb[2 * r + 1];
+    }
   }
   for (int e = tid; e < nlen; e += NT) L[e] = 0.0;
   __syncthreads();
+  if (handoff) {
+    // scatter the supernode panels (rows in panel order, columns c0..c0+w-1)
+    // into the tile layout, then invert the diagonal tiles
+    const DevSnPlan SP = bv.snplan[W.model];
+    const SnSuper* sup = bv.sn_sup + SP.sup_off;
+    const double* lv = bv.sn_lv + W.snlv_off;
+    for (int k = 0; k < SP.n_sup; ++k) {
+      const SnSuper u = sup[k];
+      const int32_t* prow = bv.sn_prow + u.prow_off;
+      const int rows = u.w + u.m;
+      for (int e = tid; e < rows * u.w; e += NT) {
+        const int c = e / rows, q = e - c * rows;
+        if (q < c) continue;
+        L[lidx(prow[q], u.c0 + c, n)] = lv[u.pb + c * u.ld + q];
+      }
+    }
+    __syncthreads();
+    for (int k = wid; k < T; k += NW) diag_invert_rinv(L + diag_tile(k, n), tile_rows(k, n), lane);
+    __syncthreads();
+    stamp(0);
+    stamp(2);
+  } else {
 
   // ---- 1. D = P (J M^-1 J^T + R) P + (eta+rho) I  (assemble_dense, delassus.cpp:67-104)
   // One warp per body b walks the Gram block of the rows touching b
@@ -547,6 +610,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     }
   }
   stamp(2);
+  }  // !handoff
   // ---- 2b. X = L^{-1}: every PADMM solve becomes two parallel mat-vecs
   tri_inverse<NT>(L, n, T);
   stamp(3);
@@ -560,6 +624,12 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   const int kind = !has_unit ? ROW_BILATERAL : (tid < n_jd ? ROW_BILATERAL : (tid < first_contact ? ROW_LIMIT : ROW_CONTACT));
   const int nr = !has_unit ? 0 : (kind == ROW_CONTACT ? 3 : 1);
   const double mu = has_unit ? bv.rmu[R0 + row0] : 0.0;
+  int pos[3] = {row0, row0 + 1, row0 + 2};  // the unit's rows in the solve's order
+  if (handoff) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (d < nr) pos[d] = rbs[row0 + d];
+  }
   const double inv_1pmu2 = 1.0 / (1.0 + mu * mu);
   const double eta = sp.eta, rho = sp.rho;
   const double inv_rho = 1.0 / rho;  // w = x - z_hat / rho as x - z_hat * (1/rho): no division in the loop
@@ -591,7 +661,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     const double s0 = kind == ROW_CONTACT ? mu * fast_sqrt(zh[1] * zh[1] + zh[2] * zh[2]) : 0.0;  // desaxce_shift (padmm.cpp:44-52)
 #pragma unroll
     for (int d = 0; d < 3; ++d)
-      if (d < nr) xv[row0 + d] = -((((v[d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * yh[d]) - zh[d]);
+      if (d < nr) xv[pos[d]] = -((((v[d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * yh[d]) - zh[d]);
   };
   write_rhs();
   for (it = 1; it <= sp.max_iters; ++it) {
@@ -600,7 +670,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     double yp[3], zp[3], wv[3], yn[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      if (d < nr) x[d] = xv[row0 + d];
+      if (d < nr) x[d] = xv[pos[d]];
       wv[d] = x[d] - zh[d] * inv_rho;
       yp[d] = y[d];
       zp[d] = z[d];

@@ -26,7 +26,16 @@ enum GeomShape : int32_t { G_SPHERE = 0, G_PLANE = 1, G_BOX = 2 };
 // `a` is always the moving geom (ContactPoint::geom_a), `b` the other one.
 enum PairKind : int32_t { P_SPHERE_SPHERE = 0, P_SPHERE_PLANE = 1, P_BOX_PLANE = 2 };
 enum RowKind : int32_t { ROW_BILATERAL = 0, ROW_LIMIT = 1, ROW_CONTACT = 2 };
-enum Backend : int32_t { BE_NONE = -1, BE_DENSE_SMEM = 0, BE_DENSE_GLOBAL = 1, BE_MATRIX_FREE = 2, BE_SPARSE = 3 };
+// BE_DENSE_SN: the supernodal kernel factors (plan order) and hands L to the
+// dense kernel, which forms L^-1 and runs the PADMM solves
+enum Backend : int32_t {
+  BE_NONE = -1,
+  BE_DENSE_SMEM = 0,
+  BE_DENSE_GLOBAL = 1,
+  BE_MATRIX_FREE = 2,
+  BE_SPARSE = 3,
+  BE_DENSE_SN = 4,
+};
 
 enum JointFlags : int32_t {
   JF_PD = 1,
@@ -63,7 +72,7 @@ struct DevModel {
   int32_t nb, nj, ng, npairs;
   int32_t n_bil, n_dyn, n_limited, max_contacts;
   int32_t row_cap, body_off, joint_off, geom_off;
-  int32_t pair_off, sn, pad1, pad2;  // sn: model has a supernodal plan (DevSnPlan)
+  int32_t pair_off, sn, pad1, pad2;  // sn: 1 supernodal kernel, 2 supernodal factor + dense solve
   double gravity[3];
   double pad3;
 };
@@ -100,6 +109,7 @@ struct SnGBody {
 struct SnSuper {
   int32_t c0, w, m, ld;
   int32_t pb, xb, ws, tmap_off;
+  int32_t prow_off, pad0, pad1, pad2;  // w + m panel-row positions at sn_prow[prow_off..]
 };
 // Solve program (one u32 blob per model, copied to shared memory per CTA):
 //   phase (4 words): rec0 (word offset of its records), nsteps, mode, split
@@ -114,7 +124,7 @@ struct DevSnPlan {
   int32_t S, nLv, n_jd, lim_base;
   int32_t gram_off, n_gram, pair_off, slotpos_off;
   int32_t sup_off, n_sup, prog_off, prog_words;
-  int32_t n_sph, max_slots, smem_doubles, pad0;  // smem_doubles: per-warp footprint
+  int32_t n_sph, max_slots, smem_doubles, vreg_h;  // smem_doubles: per-warp footprint; vreg_h: hand-off layout
   int32_t gbody_off, n_gbody, kmax, vreg;  // vreg: per-warp vector region (doubles)
 };
 
@@ -131,6 +141,8 @@ struct DevWorld {
   int32_t contact_cap;  // contacts this world can hold (overflow is reported, never silent)
   int32_t slab_cap;     // rows the dense-global slab can hold (0 if none)
   int64_t lslab_off;    // dense-global factor slab (doubles), -1 if none
+  int64_t snlv_off;     // supernodal factor hand-off slab (doubles), -1 if none
+  int64_t snr2p_off;    // row -> plan position hand-off (int32), -1 if none
 };
 
 // Per-row Jacobian blocks: J = [block_a | block_b], JM = J M^-1 folded
@@ -231,6 +243,9 @@ struct BatchView {
   const uint32_t* sn_prog;
   const int32_t* sn_pair_slot;
   const uint16_t* sn_slot_pos;
+  const int32_t* sn_prow;  // panel-row positions of every supernode
+  double* sn_lv;           // BE_DENSE_SN hand-off: the factor array per world
+  int32_t* sn_r2p;         // BE_DENSE_SN hand-off: compact row -> position per world
 };
 
 struct StepParams {
@@ -238,7 +253,7 @@ struct StepParams {
   double beta, contact_margin, impact_thr, bias_clamp, lim_margin_ang, lim_margin_lin;
   int32_t max_iters, acceleration, restart, fixed_mode;
   int32_t cr_iters, warm_start, moreau, backend;  // backend: KD_BACKEND_*
-  int32_t sparse, pad0;                            // supernodal path enabled for planned models
+  int32_t sparse, sn_handoff;                      // supernodal path enabled / factor hand-off enabled
 };
 
 }  // namespace kd

@@ -237,6 +237,9 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
     u.ld = (u.w + u.m) | 1;
     u.pb = nLv;
     nLv += u.ld * u.w;
+    u.prow_off = (int)p.prow.size();
+    for (int q = 0; q < u.w; ++q) p.prow.push_back(c0 + q);
+    p.prow.insert(p.prow.end(), R.begin(), R.end());
     if (u.m > 255 || u.w > 32) {
       why = "supernode too large";
       return false;
@@ -501,6 +504,8 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
   {  // per-warp shared memory of kd_sparse.cu: Lv | v t + 5 PADMM vectors (or Gram staging) | partials | 2 int16 maps
     const int Sp = (S + 1) & ~1;
     p.smem_doubles = ((nLv + 1) & ~1) + p.vreg + p.max_slots + (Sp + 1) / 2 + 1;
+    p.vreg_h = 12 * p.kmax + Sp;
+    p.smem_doubles_h = ((nLv + 1) & ~1) + p.vreg_h + (Sp + 1) / 2 + 1;
   }
   return true;
 }

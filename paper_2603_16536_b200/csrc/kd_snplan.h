@@ -46,6 +46,8 @@ struct SnPlanHost {
   int n_sph = 0;         // solve phases
   int kmax = 0;          // most rows touching one body
   int vreg = 0;          // per-warp vector region (doubles)
+  int vreg_h = 0;        // hand-off layout (factor only): Gram staging + P
+  int smem_doubles_h = 0;  // per-warp footprint of the factor-only (hand-off) kernel
   std::vector<int32_t> pair_slot;   // per collision pair: first contact slot, -1 if unplanned
   std::vector<uint16_t> slot_pos;   // slot -> elimination position
   std::vector<int32_t> slot_body;   // 2 per slot: (body a, body b or -1)
@@ -55,6 +57,7 @@ struct SnPlanHost {
   std::vector<uint32_t> gpair;      // Lv index | local row i << 16 | local row j << 24
   std::vector<SnSuper> sup;
   std::vector<uint32_t> tmap;
+  std::vector<int32_t> prow;        // per supernode: its w + m panel-row positions
   std::vector<uint32_t> prog;       // solve program blob (see kd_layout.h)
   // statistics
   int nnzL = 0, s_levels = 0;

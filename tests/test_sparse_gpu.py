@@ -41,7 +41,7 @@ def test_auto_kernel_choice():
     small.step(K.config_for(oracle_lib.bundled_scene("fourbar")), 2)
     large.step(K.config_for(dr_legs()), 2)
     assert small.kernels() == ["supernodal"] * 4
-    assert large.kernels() == ["dense"] * 4
+    assert large.kernels() == ["supernodal+dense"] * 4  # plan factor handed to the dense kernel
 
 
 def test_dr_legs_runs_supernodal_kernel(force_supernodal):
@@ -107,6 +107,32 @@ def test_supernodal_dr_legs_trajectory_vs_oracle(force_supernodal):
     assert np.abs(tg - to).max() < 1e-6
 
 
+def test_handoff_matches_dense_kernel_from_identical_states(monkeypatch):
+    """The supernodal factor handed to the dense kernel (default for DR-Legs)
+    against the dense kernel's own blocked Cholesky (KD_SN_HANDOFF=0)."""
+    sc = dr_legs()
+    cfg = K.config_for(sc)
+    ho = _batch(sc, 16)
+    monkeypatch.setenv("KD_SN_HANDOFF", "0")
+    de = _batch(sc, 16)
+    monkeypatch.delenv("KD_SN_HANDOFF")
+    worst, same, total = 0.0, 0, 0
+    for _ in range(40):
+        p, t, tm = ho.get_state()
+        de.set_state(p, t, tm)
+        ho.step(cfg)
+        de.step(cfg)
+        assert ho.kernels() == ["supernodal+dense"] * 16 and de.kernels() == ["dense"] * 16
+        a, d = ho.impulses(), de.impulses()
+        worst = max(worst, float(np.abs(a - d).max() / max(1.0, np.abs(d).max())))
+        for gh, gd in zip(ho.diagnostics(), de.diagnostics()):
+            assert gh.n_rows == gd.n_rows and gh.contact_count == gd.contact_count
+            same += gh.iterations == gd.iterations
+            total += 1
+    assert worst < 1e-8
+    assert same >= 0.98 * total
+
+
 def test_dense_kernel_dr_legs_trajectory_vs_oracle(monkeypatch):
     monkeypatch.setenv("KD_SPARSE", "0")
     sc = dr_legs()
@@ -164,8 +190,8 @@ def test_unplanned_contact_falls_back_to_dense_kernel(force_supernodal):
 
 def test_heterogeneous_batch_kernels():
     """Config 3 mix: four-bar, DR-Legs and serial chain worlds in one batch
-    under Auto: the four-bars take the supernodal kernel, the rest the dense
-    kernel, all in one step."""
+    under Auto: the four-bars take the supernodal kernel, the larger models the
+    supernodal factor + dense solve hand-off, all in one step."""
     scs = [oracle_lib.bundled_scene("fourbar"), dr_legs(), oracle_lib.bundled_scene("serial_chain_10")]
     ms = [K.build_model(s) for s in scs]
     oms = [oracle_lib.OracleModel(s) for s in scs]
@@ -181,7 +207,7 @@ def test_heterogeneous_batch_kernels():
         for dg, do in zip(gb.diagnostics(), ob.diagnostics()):
             assert (dg.n_rows, dg.iterations) == (do.n_rows, do.iterations)
     kinds = gb.kernels()
-    assert all(kinds[w] == ("supernodal" if wm[w] == 0 else "dense") for w in range(12))
+    assert all(kinds[w] == ("supernodal" if wm[w] == 0 else "supernodal+dense") for w in range(12))
     pg, _, _ = gb.get_state()
     po, _, _ = ob.get_state()
     assert np.abs(pg - po).max() < 1e-9
