@@ -367,7 +367,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     d.sn = 0;
     if (b->sparse && sn_fits) {
       if (b->sparse_mode == 2 || m.sn->S <= kSnAutoMaxSlots) d.sn = 1;
-      else if (b->sn_handoff && m.sn->S <= kSmemMaxRows) d.sn = 2;
+      else if (b->sn_handoff && m.sn->S <= kSmemMaxRows && !m.sn->scat.empty()) d.sn = 2;
     }
     for (int k = 0; k < 3; ++k) d.gravity[k] = m.gravity[k];
     bodies.insert(bodies.end(), m.bodies.begin(), m.bodies.end());
@@ -568,6 +568,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     std::vector<SnGram> gram;
     std::vector<SnSuper> sups;
     std::vector<int32_t> prow;
+    std::vector<uint32_t> scat;
     std::vector<SnGBody> gbody;
     std::vector<uint32_t> tmap, prog, gslot, gpair;
     std::vector<int32_t> pslot;
@@ -584,6 +585,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       d.smem_doubles = p.smem_doubles;
       d.max_slots = p.max_slots;
       d.vreg_h = p.vreg_h;
+      d.lmask_lo = (int32_t)(uint32_t)(p.lmask & 0xffffffffull);
+      d.lmask_hi = (int32_t)(uint32_t)(p.lmask >> 32);
       d.n_sph = p.n_sph;
       d.gram_off = (int)gram.size();
       d.n_gram = (int)p.gram.size();
@@ -615,6 +618,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
         sups.push_back(u);
       }
       prow.insert(prow.end(), p.prow.begin(), p.prow.end());
+      d.scat_off = (int)scat.size();
+      d.n_scat = (int)p.scat.size();
+      scat.insert(scat.end(), p.scat.begin(), p.scat.end());
       tmap.insert(tmap.end(), p.tmap.begin(), p.tmap.end());
       while (prog.size() & 3) prog.push_back(0);  // 16-byte aligned blobs
       d.prog_off = (int)prog.size();
@@ -640,6 +646,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     KD_CK(up(v.sn_pair_slot, pslot));
     KD_CK(up(v.sn_slot_pos, spos));
     KD_CK(up(v.sn_prow, prow));
+    KD_CK(up(v.sn_scat, scat));
   }
   for (cudaEvent_t& e : b->ev) KD_CK(cudaEventCreate(&e));
   KD_CK(cudaDeviceSynchronize());

@@ -313,8 +313,14 @@ __device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, 
 
 // Overwrite the Cholesky factor (diag tiles already inverted) with X = L^{-1}
 // by right-looking block forward substitution on L X = I.
+// lmask: bit ti(ti+1)/2 + tj set for every tile of L that can be nonzero
+// (all ones unless the factor came from a supernodal plan); a zero tile
+// L_i,kk contributes nothing to phases 2 and 3 and stays zero.
+__device__ __forceinline__ bool ltile(unsigned long long lmask, int ti, int tj) {
+  return (lmask >> (ti * (ti + 1) / 2 + tj)) & 1ull;
+}
 template <int NT>
-__device__ void tri_inverse(double* L, int n, int T) {
+__device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = 1; k < T; ++k) {
@@ -324,12 +330,21 @@ __device__ void tri_inverse(double* L, int n, int T) {
     // phase 1 (step kk): X_kk,j = Linv_kk B_kk,j for j < kk
     for (int u = wid; u < kk; u += NW) trmm_left(L, kk, u, n, lane);
     __syncthreads();
+    // rows i > kk whose tile L_i,kk is nonzero
+    unsigned rows = 0;
+    for (int i = kk + 1; i < T; ++i)
+      if (ltile(lmask, i, kk)) rows |= 1u << i;
+    const int below = __popc(rows);
+    auto row_at = [&](int q) {  // q-th set bit
+      unsigned r = rows;
+      for (int t = 0; t < q; ++t) r &= r - 1;
+      return __ffs(r) - 1;
+    };
     // phase 2 (step kk): B_ij -= L_i,kk X_kk,j for i > kk, j < kk
-    const int below = T - kk - 1;
-    for (int u = wid; u < below * kk; u += NW) gemm_sub(L, kk + 1 + u / kk, u % kk, kk, n, lane);
+    for (int u = wid; u < below * kk; u += NW) gemm_sub(L, row_at(u / kk), u % kk, kk, n, lane);
     __syncthreads();
     // phase 3 (step kk): B_i,kk = -L_i,kk Linv_kk for i > kk
-    for (int u = wid; u < below; u += NW) trmm_right_neg(L, kk + 1 + u, kk, n, lane);
+    for (int u = wid; u < below; u += NW) trmm_right_neg(L, row_at(u), kk, n, lane);
     __syncthreads();
   }
   // final step T-1: X_T-1,j = Linv B for j < T-1
@@ -465,20 +480,14 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   for (int e = tid; e < nlen; e += NT) L[e] = 0.0;
   __syncthreads();
   if (handoff) {
-    // scatter the supernode panels (rows in panel order, columns c0..c0+w-1)
-    // into the tile layout, then invert the diagonal tiles
+    // scatter the supernode panels into the tile layout (the plan's flat list
+    // of (Lv index, tile index) pairs), then invert the diagonal tiles
     const DevSnPlan SP = bv.snplan[W.model];
-    const SnSuper* sup = bv.sn_sup + SP.sup_off;
     const double* lv = bv.sn_lv + W.snlv_off;
-    for (int k = 0; k < SP.n_sup; ++k) {
-      const SnSuper u = sup[k];
-      const int32_t* prow = bv.sn_prow + u.prow_off;
-      const int rows = u.w + u.m;
-      for (int e = tid; e < rows * u.w; e += NT) {
-        const int c = e / rows, q = e - c * rows;
-        if (q < c) continue;
-        L[lidx(prow[q], u.c0 + c, n)] = lv[u.pb + c * u.ld + q];
-      }
+    const uint32_t* sc = bv.sn_scat + SP.scat_off;
+    for (int e = tid; e < SP.n_scat; e += NT) {
+      const uint32_t q = sc[e];
+      L[q >> 16] = lv[q & 0xffff];
     }
     __syncthreads();
     for (int k = wid; k < T; k += NW) diag_invert_rinv(L + diag_tile(k, n), tile_rows(k, n), lane);
@@ -612,7 +621,9 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   stamp(2);
   }  // !handoff
   // ---- 2b. X = L^{-1}: every PADMM solve becomes two parallel mat-vecs
-  tri_inverse<NT>(L, n, T);
+  tri_inverse<NT>(L, n, T, handoff ? ((unsigned long long)(uint32_t)bv.snplan[W.model].lmask_hi << 32) |
+                                          (uint32_t)bv.snplan[W.model].lmask_lo
+                                    : ~0ull);
   stamp(3);
 
   // ---- 3. PADMM (padmm.cpp:87-159), one cone unit per thread

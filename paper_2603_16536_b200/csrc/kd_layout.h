@@ -126,6 +126,7 @@ struct DevSnPlan {
   int32_t sup_off, n_sup, prog_off, prog_words;
   int32_t n_sph, max_slots, smem_doubles, vreg_h;  // smem_doubles: per-warp footprint; vreg_h: hand-off layout
   int32_t gbody_off, n_gbody, kmax, vreg;  // vreg: per-warp vector region (doubles)
+  int32_t lmask_lo, lmask_hi, scat_off, n_scat;  // nonzero 32x32 tiles of L in plan order; hand-off scatter list
 };
 
 // Per-world indexing (prefix sums over model capacities).
@@ -244,6 +245,7 @@ struct BatchView {
   const int32_t* sn_pair_slot;
   const uint16_t* sn_slot_pos;
   const int32_t* sn_prow;  // panel-row positions of every supernode
+  const uint32_t* sn_scat; // hand-off scatter lists (Lv index | tile index << 16)
   double* sn_lv;           // BE_DENSE_SN hand-off: the factor array per world
   int32_t* sn_r2p;         // BE_DENSE_SN hand-off: compact row -> position per world
 };

@@ -217,6 +217,16 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
   std::vector<int> snid(S);
   for (int k = 0; k < K; ++k)
     for (int j = sn_start[k]; j < sn_start[k + 1]; ++j) snid[j] = k;
+  // nonzero tiles of L (the hand-off's L^-1 skips the zero ones)
+  if (S <= 256) {
+    p.lmask = 0;
+    for (int j = 0; j < S; ++j) {
+      p.lmask |= 1ull << ((j / 32) * (j / 32 + 1) / 2 + j / 32);
+      for (int i : cs[j]) p.lmask |= 1ull << ((i / 32) * (i / 32 + 1) / 2 + j / 32);
+    }
+  } else {
+    p.lmask = ~0ull;
+  }
   // row patterns
   std::vector<std::vector<int>> rp(S);
   for (int j = 0; j < S; ++j)
@@ -269,6 +279,28 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
     const SnSuper& u = p.sup[snid[j]];
     return u.xb + (i - u.c0) * u.ws + (j - u.c0);
   };
+  // ---- hand-off scatter list: panel (lower) entries -> kd_dense.cu's tile
+  // layout for n = S (tiles of 32, off-diagonal row stride 33, packed
+  // diagonal tiles)
+  {
+    auto rows_of = [&](int ti) { return std::min(32, S - 32 * ti); };
+    auto lidx = [&](int i, int j) {
+      const int ti = i >> 5, tj = j >> 5, r = i & 31, c = j & 31;
+      const int base = 528 * ti * ti;
+      if (ti == tj) return base + ti * 33 * rows_of(ti) + ((r * (r + 1)) >> 1) + c;
+      return base + tj * 33 * rows_of(ti) + r * 33 + c;
+    };
+    for (const SnSuper& u : p.sup)
+      for (int c = 0; c < u.w; ++c)
+        for (int q = c; q < u.w + u.m; ++q) {
+          const int li = lidx(p.prow[u.prow_off + q], u.c0 + c);
+          if (li >= 65536) {
+            p.scat.clear();
+            break;
+          }
+          p.scat.push_back((uint32_t)(u.pb + c * u.ld + q) | ((uint32_t)li << 16));
+        }
+  }
   // ---- ancestor-update target maps
   for (int k = 0; k < K; ++k) {
     SnSuper& u = p.sup[k];

@@ -48,6 +48,7 @@ struct SnPlanHost {
   int vreg = 0;          // per-warp vector region (doubles)
   int vreg_h = 0;        // hand-off layout (factor only): Gram staging + P
   int smem_doubles_h = 0;  // per-warp footprint of the factor-only (hand-off) kernel
+  uint64_t lmask = 0;      // nonzero 32x32 tiles of L (tile ti(ti+1)/2 + tj), for S <= 256
   std::vector<int32_t> pair_slot;   // per collision pair: first contact slot, -1 if unplanned
   std::vector<uint16_t> slot_pos;   // slot -> elimination position
   std::vector<int32_t> slot_body;   // 2 per slot: (body a, body b or -1)
@@ -58,6 +59,7 @@ struct SnPlanHost {
   std::vector<SnSuper> sup;
   std::vector<uint32_t> tmap;
   std::vector<int32_t> prow;        // per supernode: its w + m panel-row positions
+  std::vector<uint32_t> scat;       // hand-off scatter: Lv index | dense tile index (n = S) << 16
   std::vector<uint32_t> prog;       // solve program blob (see kd_layout.h)
   // statistics
   int nnzL = 0, s_levels = 0;
