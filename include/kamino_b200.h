@@ -298,9 +298,10 @@ int kd_batch_get_kernels(kd_batch* batch, int32_t* out);
  * nnz(L), per-world fp64 array length, supernodes, solve levels, solve
  * program words, factor FMAs, solve FMA terms per PADMM iteration, dense-LLT
  * FMAs S^3/6, per-world shared-memory doubles, solve critical path (terms on
- * the busiest lane, summed over phases), solve phases.
+ * the busiest lane, summed over phases), solve phases, and the 64-bit masks of
+ * the nonzero 32x32 tiles of L and of L^-1 (bit ti(ti+1)/2 + tj).
  * Returns KD_ERR_INVALID_ARGUMENT with the reason if the model has no plan. */
-int kd_model_sparse_plan_info(const kd_model* model, int64_t* stats12);
+int kd_model_sparse_plan_info(const kd_model* model, int64_t* stats14);
 /* Host self-test of the plan (no device): a random SPD system with the plan's
  * pattern and a random active-slot mask, solved by the plan's factor and solve
  * programs and by a dense Cholesky; writes the max relative difference. */

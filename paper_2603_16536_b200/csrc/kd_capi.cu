@@ -101,6 +101,8 @@ struct kd_batch {
   int64_t total_snlv = 0, total_snr2p = 0;
   int hist_cap = 0;
   double* d_hist = nullptr;
+  double* d_nest = nullptr;  // Nesterov beta table (StepParams::nest_beta)
+  int nest_cap = 0;
   int32_t* d_err = nullptr;
   bool timing = false;
   cudaEvent_t ev[6] = {};
@@ -189,9 +191,10 @@ int kd_model_sparse_plan_info(const kd_model* mp, int64_t* st) {
   if (!mp || !st) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   if (!mp->m.sn) return fail(KD_ERR_INVALID_ARGUMENT, "model has no sparse plan: " + mp->m.sn_why);
   const SnPlanHost& p = *mp->m.sn;
-  const int64_t v[12] = {p.S, p.nnzL, p.nLv, (int64_t)p.sup.size(), p.s_levels, (int64_t)p.prog.size(),
-                         p.factor_fma, p.solve_terms, p.dense_factor_fma, p.smem_doubles, p.solve_crit, p.n_sph};
-  for (int k = 0; k < 12; ++k) st[k] = v[k];
+  const int64_t v[14] = {p.S, p.nnzL, p.nLv, (int64_t)p.sup.size(), p.s_levels, (int64_t)p.prog.size(),
+                         p.factor_fma, p.solve_terms, p.dense_factor_fma, p.smem_doubles, p.solve_crit, p.n_sph,
+                         (int64_t)p.lmask, (int64_t)p.xmask};
+  for (int k = 0; k < 14; ++k) st[k] = v[k];
   return KD_OK;
 }
 
@@ -798,6 +801,7 @@ static StepParams step_params(const kd_batch* b, const kd_step_config* c) {
   sp.backend = c->backend;
   sp.sparse = b->sparse ? 1 : 0;
   sp.sn_handoff = b->sn_handoff ? 1 : 0;
+  sp.nest_beta = b->d_nest;
   return sp;
 }
 
@@ -851,7 +855,33 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
   return KD_OK;
 }
 
+// Nesterov coefficients (nesterov_next_coefficient / nesterov_update,
+// padmm.cpp:54-71): a_0 = 1, a_{m+1} = (1 + sqrt(1 + 4 a_m^2)) / 2 and
+// beta_m = (a_m - 1) / a_{m+1}.  The sequence restarts from a_0, so a PADMM
+// loop only needs m (updates since the last restart); the host computes the
+// table once in IEEE double, as the reference does.
+static int ensure_nest_table(kd_batch* b, int max_iters) {
+  if (max_iters <= b->nest_cap) return KD_OK;
+  const int cap = std::max(256, max_iters);
+  std::vector<double> t(cap);
+  double a = 1.0;
+  for (int m = 0; m < cap; ++m) {
+    volatile double q = 4.0 * a * a;  // rounded product, never fused into the sum
+    const double a_next = 0.5 * (1.0 + std::sqrt(1.0 + q));
+    t[m] = (a - 1.0) / a_next;
+    a = a_next;
+  }
+  double* d = nullptr;
+  KD_CK(b->mem.alloc(d, cap));
+  KD_CK(cudaMemcpy(d, t.data(), 8 * (size_t)cap, cudaMemcpyHostToDevice));
+  b->d_nest = d;
+  b->nest_cap = cap;
+  return KD_OK;
+}
+
 static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
+  const int nrc = ensure_nest_table(b, c->max_iters);
+  if (nrc != KD_OK) return nrc;
   const StepParams sp = step_params(b, c);
   if (!b->graphs || b->timing || n_steps < 2) {
     for (int k = 0; k < n_steps; ++k) {

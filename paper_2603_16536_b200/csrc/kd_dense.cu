@@ -68,6 +68,24 @@ __device__ __forceinline__ void block_max3(double& a, double& b, double& c, doub
   }
 }
 
+// Block maximum of one non-negative value per thread (one barrier).
+template <int NT>
+__device__ __forceinline__ double block_max_nonneg(double v, double* red) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_max_nonneg(v);
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double m[NW];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) m[k] = red[k];
+#pragma unroll
+  for (int s = 1; s < NW; s *= 2)
+#pragma unroll
+    for (int k = 0; k + s < NW; k += 2 * s) m[k] = fmax(m[k], m[k + s]);
+  return m[0];
+}
+
 // ---------------------------------------------------------------- Cholesky pieces
 // Factor the packed diagonal tile in place and overwrite it with L_kk^{-1}.
 // One warp; lane r owns row r in registers (fully unrolled so every register
@@ -358,9 +376,12 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask) {
 // Padded tiles give both walks constant offsets and no bank conflicts; the
 // broadcast vector operand is read as double2 (one wavefront per two entries).
 template <int NT>
-__device__ void inv_solve(const double* X, double* b, double* w, int n, int T) {
+__device__ void inv_solve(const double* X, double* b, double* w, int n, int T, long long* prof = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __syncthreads();
+#ifdef KD_PROF_PADMM
+  long long q0 = clock64();
+#endif
   for (int i = wid; i < T; i += NT / 32) {
     const int ri = tile_rows(i, n), r = lane;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -389,6 +410,10 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T) {
     }
   }
   __syncthreads();
+#ifdef KD_PROF_PADMM
+  long long q1 = clock64();
+  prof[0] += q1 - q0;
+#endif
   for (int j = wid; j < T; j += NT / 32) {
     const int c = lane, rj = tile_rows(j, n);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -423,6 +448,9 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T) {
     }
   }
   __syncthreads();
+#ifdef KD_PROF_PADMM
+  prof[1] += clock64() - q1;
+#endif
 }
 
 
@@ -662,9 +690,9 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     yh[d] = y[d];
     zh[d] = z[d];
   }
-  double a = 1.0, prev = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-  double r_p = 0, r_d = 0, r_c = 0;
-  int restarts = 0, it = 1;
+  double prev = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  double rp = 0.0, dmax = 0.0, rc = 0.0;  // this thread's last-iteration residual terms
+  int restarts = 0, it = 1, m = 0;          // m: Nesterov updates since the last restart (a = a_m)
   bool converged = false;
   const int hcap = bv.hist_cap;
   // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
@@ -675,9 +703,17 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
       if (d < nr) xv[pos[d]] = -((((v[d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * yh[d]) - zh[d]);
   };
   write_rhs();
+  long long prof[4] = {0, 0, 0, 0};
   for (it = 1; it <= sp.max_iters; ++it) {
-    inv_solve<NT>(L, xv, wv_s, n, T);
-    double rp = 0.0, dmax = 0.0, rc = 0.0;
+#ifdef KD_PROF_PADMM
+    const long long p0 = clock64();
+#endif
+    inv_solve<NT>(L, xv, wv_s, n, T, prof);
+#ifdef KD_PROF_PADMM
+    const long long p1 = clock64();
+#endif
+    // beta_m of the Nesterov sequence (host table), fetched before the reduction
+    const double beta = sp.acceleration ? sp.nest_beta[m] : 0.0;
     double yp[3], zp[3], wv[3], yn[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -692,6 +728,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
       yn[1] = yn[2] = 0.0;
     }
     double ymax = 0.0, zmax = 0.0;
+    rp = dmax = rc = 0.0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       if (d < nr) {
@@ -705,11 +742,14 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
       }
     }
     if (kind != ROW_BILATERAL) rc = fmin(ymax, zmax);
-    block_max3<NT>(rp, dmax, rc, red);
-    r_p = rp;
-    r_d = rho * dmax;
-    r_c = rc;
-    const double combined = fmax(r_p, fmax(r_d, r_c));
+    // max(r_p, r_d, r_c) (padmm.cpp:128-131) in one reduction: rho > 0, so
+    // max(rho * dmax_i) = rho * max(dmax_i) exactly
+    const double combined = block_max_nonneg<NT>(fmax(rp, fmax(rho * dmax, rc)), red);
+#ifdef KD_PROF_PADMM
+    const long long p2 = clock64();
+    prof[2] += p2 - p1;
+    prof[3] += p1 - p0;  // whole solve incl. entry barrier
+#endif
     if (tid == 0 && it <= hcap) bv.hist[(int64_t)w * hcap + it - 1] = combined;
     if (!sp.fixed_mode && combined < sp.eps) {
       converged = true;
@@ -718,7 +758,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     if (sp.acceleration) {  // nesterov_update (padmm.cpp:58-71)
       const bool restart = sp.restart && combined > prev;
       if (restart) {
-        a = 1.0;
+        m = 0;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           yh[d] = y[d];
@@ -726,14 +766,12 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
         }
         ++restarts;
       } else {
-        const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));
-        const double beta = (a - 1.0) / an;
+        ++m;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           yh[d] = y[d] + beta * (y[d] - yp[d]);
           zh[d] = z[d] + beta * (z[d] - zp[d]);
         }
-        a = an;
       }
     } else {
 #pragma unroll
@@ -745,7 +783,19 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
     prev = combined;
     write_rhs();
   }
+  // the last iteration's r_p, r_d, r_c (padmm.cpp:147-157)
+  __syncthreads();  // red is still being read by the last reduction
+  block_max3<NT>(rp, dmax, rc, red);
+  const double r_p = rp, r_d = rho * dmax, r_c = rc;
   stamp(4);
+#ifdef KD_PROF_PADMM
+  if (tid == 0) {
+    ws.phase_cycles[5] = prof[0];
+    ws.phase_cycles[6] = prof[1];
+    ws.phase_cycles[7] = prof[2];
+    ws.phase_cycles[1] = prof[3];
+  }
+#endif
   // outputs (padmm.cpp:147-157)
 #pragma unroll
   for (int d = 0; d < 3; ++d) {

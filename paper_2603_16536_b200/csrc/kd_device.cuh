@@ -26,6 +26,18 @@ __device__ __forceinline__ void stm(double* p, const M3& m) {
   for (int i = 0; i < 9; ++i) p[i] = m.m[i];
 }
 
+// Exact warp maximum of non-negative doubles.  With the sign bit cleared,
+// IEEE bit patterns of non-negative doubles order like their values, so two
+// 32-bit REDUX reductions (high words, then the low words of the lanes that
+// hold the maximal high word) give the maximum without a shuffle tree.
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull;
+  const unsigned hi = (unsigned)(u >> 32), lo = (unsigned)u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
+
 // Warp exclusive prefix sum; returns the warp total.
 __device__ __forceinline__ int warp_exclusive_sum(int v, int lane, int& excl) {
   int incl = v;

@@ -256,6 +256,7 @@ struct StepParams {
   int32_t max_iters, acceleration, restart, fixed_mode;
   int32_t cr_iters, warm_start, moreau, backend;  // backend: KD_BACKEND_*
   int32_t sparse, sn_handoff;                      // supernodal path enabled / factor hand-off enabled
+  const double* nest_beta;  // Nesterov beta_m = (a_m - 1) / a_{m+1}, a_0 = 1, m < max_iters (padmm.cpp:54-71)
 };
 
 }  // namespace kd

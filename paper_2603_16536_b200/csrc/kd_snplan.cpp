@@ -1,3 +1,6 @@
+#include <set>
+#include <cstdio>
+#include <cstdlib>
 // kd_snplan.cpp — host construction of the supernodal sparse LLT plan
 // (see kd_snplan.h) and a CPU interpreter used only by the self-test.
 //
@@ -224,8 +227,23 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       p.lmask |= 1ull << ((j / 32) * (j / 32 + 1) / 2 + j / 32);
       for (int i : cs[j]) p.lmask |= 1ull << ((i / 32) * (i / 32 + 1) / 2 + j / 32);
     }
+    // X = L^-1: X_ij != 0 only if i is j or an elimination-tree ancestor of j
+    if (getenv("KD_DBG_X")) {
+      long nx = 0;
+      std::set<std::pair<int,int>> t16, t8;
+      for (int j = 0; j < S; ++j)
+        for (int i = j;; i = cs[i][0]) { ++nx; t16.insert({i/16,j/16}); t8.insert({i/8,j/8}); if (cs[i].empty()) break; }
+      fprintf(stderr, "S=%d nnzX=%ld dense=%d tiles16=%zu (%d) tiles8=%zu (%d)\n", S, nx, S*(S+1)/2, t16.size(), ((S+15)/16)*((S+15)/16+1)/2, t8.size(), ((S+7)/8)*((S+7)/8+1)/2);
+      for (int i = 0; i < S; i += 8) { for (int j = 0; j <= i; j += 8) fputc(t8.count({i/8,j/8}) ? '#' : '.', stderr); fputc('\n', stderr); }
+    }
+    p.xmask = 0;
+    for (int j = 0; j < S; ++j)
+      for (int i = j;; i = cs[i][0]) {
+        p.xmask |= 1ull << ((i / 32) * (i / 32 + 1) / 2 + j / 32);
+        if (cs[i].empty()) break;
+      }
   } else {
-    p.lmask = ~0ull;
+    p.lmask = p.xmask = ~0ull;
   }
   // row patterns
   std::vector<std::vector<int>> rp(S);

@@ -102,12 +102,12 @@ class Model:
 
     SPARSE_PLAN_FIELDS = ("slots", "nnz_L", "lv_len", "supernodes", "solve_levels", "program_words",
                           "factor_fma", "solve_terms", "dense_factor_fma", "smem_doubles_per_world", "solve_crit",
-                          "solve_phases")
+                          "solve_phases", "l_tile_mask", "x_tile_mask")
 
     def sparse_plan_info(self) -> Optional[dict]:
         """Statistics of the supernodal sparse-LLT plan (kd_snplan.h), or None
         if the model has none (its dense worlds then use the dense kernel)."""
-        st = np.zeros(12, np.int64)
+        st = np.zeros(14, np.int64)
         if lib().kd_model_sparse_plan_info(self.handle, _capi.i64ptr(st)) != 0:
             return None
         return dict(zip(self.SPARSE_PLAN_FIELDS, (int(x) for x in st)))
