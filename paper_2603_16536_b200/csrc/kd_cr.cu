@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
     yh[r] = yv[r];
     zh[r] = zv[r];
   }
-  double a = 1.0, prev = __longlong_as_double(0x7ff0000000000000ll);
+  double prev = __longlong_as_double(0x7ff0000000000000ll);
+  int m = 0;  // Nesterov updates since the last restart (a = a_m)
   double r_p = 0, r_d = 0, r_c = 0;
   int restarts = 0, it;
   bool converged = false;
@@ -335,20 +336,18 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
     if (sp.acceleration) {
       const bool restart = sp.restart && combined > prev;
       if (restart) {
-        a = 1.0;
+        m = 0;
         ++restarts;
         for (int r = tid; r < n; r += NT) {
           yh[r] = yv[r];
           zh[r] = zv[r];
         }
       } else {
-        const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));
-        const double beta = (a - 1.0) / an;
+        const double beta = sp.nest_beta[m++];  // (a_m - 1) / a_{m+1}, host table
         for (int r = tid; r < n; r += NT) {
           yh[r] = yv[r] + beta * (yv[r] - yh[r]);
           zh[r] = zv[r] + beta * (zv[r] - zh[r]);
         }
-        a = an;
       }
     } else {
       for (int r = tid; r < n; r += NT) {

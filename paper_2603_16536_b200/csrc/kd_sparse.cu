@@ -291,7 +291,9 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
       }
   }
   __syncwarp();
-  double a = 1.0, prev = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  double prev = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  int m = 0;  // Nesterov updates since the last restart (a = a_m)
+  double rp = 0.0, dmax = 0.0, rc = 0.0;
   double r_p = 0, r_d = 0, r_c = 0;
   int restarts = 0, it = 1;
   bool converged = false;
@@ -343,9 +345,8 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
       __syncwarp();
     }
     // projection, dual update, residual partials; candidate extrapolation
-    const double an = 0.5 * (1.0 + sqrt(1.0 + 4.0 * a * a));  // nesterov_next_coefficient
-    const double beta = (a - 1.0) / an;
-    double rp = 0.0, dmax = 0.0, rc = 0.0;
+    const double beta = sp.acceleration ? sp.nest_beta[m] : 0.0;  // (a_m - 1) / a_{m+1}, host table
+    rp = dmax = rc = 0.0;
     for (int u = lane; u < n_units; u += 32) {
       const bool con = u >= first_contact;
       const int r0 = con ? first_contact + 3 * (u - first_contact) : u;
@@ -376,10 +377,8 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
         }
       if (u >= n_jd) rc = fmax(rc, fmin(ymax, zmax));
     }
-    r_p = warp_max(rp);
-    r_d = rho * warp_max(dmax);
-    r_c = warp_max(rc);
-    const double combined = fmax(r_p, fmax(r_d, r_c));
+    // max(r_p, r_d, r_c) in one reduction (rho > 0: max(rho dmax_i) = rho max(dmax_i))
+    const double combined = warp_max_nonneg(fmax(rp, fmax(rho * dmax, rc)));
     if (lane == 0 && it <= hcap) bv.hist[(int64_t)w * hcap + it - 1] = combined;
     if (!sp.fixed_mode && combined < sp.eps) {
       converged = true;
@@ -388,10 +387,10 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
     // nesterov_update (padmm.cpp:58-71)
     const bool restart = sp.acceleration && sp.restart && combined > prev;
     if (restart) {
-      a = 1.0;
+      m = 0;
       ++restarts;
     } else if (sp.acceleration) {
-      a = an;
+      ++m;
     }
     for (int u = lane; u < n_units; u += 32) {
       const bool con = u >= first_contact;
@@ -419,7 +418,11 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
     __syncwarp();
   }
   stamp(4);
-  // outputs (padmm.cpp:147-157)
+  // the last iteration's r_p, r_d, r_c (padmm.cpp:147-157)
+  r_p = warp_max(rp);
+  r_d = rho * warp_max(dmax);
+  r_c = warp_max(rc);
+  // outputs
   for (int r = lane; r < n; r += 32) {
     bv.lam[R0 + r] = y_s[r];
     bv.zo[R0 + r] = z_s[r];
