@@ -92,6 +92,8 @@ struct kd_batch {
   // supernodal sparse-LLT bins: one per planned model (worlds of one model per CTA)
   struct SnBin {
     int model = 0, per_warp = 0, wpc = 1, prog_words = 0;
+    bool hand = false;  // hand-off model: K2f (factor only, CTA per world)
+    size_t hand_smem = 0;
     Bin bin;
   };
   std::vector<SnBin> sn_bins;
@@ -460,9 +462,10 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     if (!dm[i].sn) continue;
     kd_batch::SnBin sbn;
     sbn.model = i;
-    const bool hand = dm[i].sn == 2;  // factor only: no solve program, smaller per-warp layout
-    sbn.per_warp = hand ? b->models[i].sn->smem_doubles_h : b->models[i].sn->smem_doubles;
-    sbn.prog_words = hand ? 0 : (int)b->models[i].sn->prog.size();
+    sbn.hand = dm[i].sn == 2;  // hand-off: the factor kernel K2f, then the dense kernel
+    sbn.hand_smem = snfactor_smem_bytes(b->models[i].sn->nLv, b->models[i].sn->S);
+    sbn.per_warp = b->models[i].sn->smem_doubles;
+    sbn.prog_words = (int)b->models[i].sn->prog.size();
     const size_t prog_bytes = ((size_t)sbn.prog_words * 4 + 15) & ~(size_t)15;
     sbn.wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (kSnMaxSmem - prog_bytes) / (8 * (size_t)sbn.per_warp)));
     for (int w = 0; w < n_worlds; ++w)
@@ -587,7 +590,6 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       d.lim_base = p.lim_base;
       d.smem_doubles = p.smem_doubles;
       d.max_slots = p.max_slots;
-      d.vreg_h = p.vreg_h;
       d.lmask_lo = (int32_t)(uint32_t)(p.lmask & 0xffffffffull);
       d.lmask_hi = (int32_t)(uint32_t)(p.lmask >> 32);
       d.n_sph = p.n_sph;
@@ -827,7 +829,8 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
     mark(1);
     if (c->backend != KD_BACKEND_MATRIX_FREE) {
       for (const auto& sbn : b->sn_bins) {
-        KD_CK(launch_sparse(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.per_warp, sbn.wpc, sbn.prog_words, s));
+        if (sbn.hand) KD_CK(launch_snfactor(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.hand_smem, s));
+        else KD_CK(launch_sparse(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.per_warp, sbn.wpc, sbn.prog_words, s));
         ++b->launches;
       }
       for (const Bin& bin : b->dense_bins) {

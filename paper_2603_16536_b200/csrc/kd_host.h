@@ -41,6 +41,9 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
                int nt, cudaStream_t s);
 cudaError_t launch_sparse(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int per_warp,
                           int wpc, int prog_words, cudaStream_t s);
+cudaError_t launch_snfactor(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, size_t smem,
+                            cudaStream_t s);
+size_t snfactor_smem_bytes(int nLv, int S);
 cudaError_t launch_fk(const BatchView& bv, const int32_t* tj, const double* tv, int nt, double tol, int max_iters,
                       double lm0, int32_t* iters, double* res, uint8_t* conv, size_t smem, cudaStream_t s);
 size_t fk_smem_bytes(int nb, int nr);

@@ -124,7 +124,7 @@ struct DevSnPlan {
   int32_t S, nLv, n_jd, lim_base;
   int32_t gram_off, n_gram, pair_off, slotpos_off;
   int32_t sup_off, n_sup, prog_off, prog_words;
-  int32_t n_sph, max_slots, smem_doubles, vreg_h;  // smem_doubles: per-warp footprint; vreg_h: hand-off layout
+  int32_t n_sph, max_slots, smem_doubles, pad0;  // smem_doubles: per-warp footprint of K2s
   int32_t gbody_off, n_gbody, kmax, vreg;  // vreg: per-warp vector region (doubles)
   int32_t lmask_lo, lmask_hi, scat_off, n_scat;  // nonzero 32x32 tiles of L in plan order; hand-off scatter list
 };

@@ -297,6 +297,14 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
     const SnSuper& u = p.sup[snid[j]];
     return u.xb + (i - u.c0) * u.ws + (j - u.c0);
   };
+  if (getenv("KD_DBG_X")) {
+    for (size_t k = 0; k < p.sup.size(); ++k) {
+      const SnSuper& u = p.sup[k];
+      int par = -1;
+      if (u.m > 0) { const int r = p.prow[u.prow_off + u.w]; for (size_t q = 0; q < p.sup.size(); ++q) if (r >= p.sup[q].c0 && r < p.sup[q].c0 + p.sup[q].w) par = (int)q; }
+      fprintf(stderr, "sn %zu c0=%d w=%d m=%d parent=%d\n", k, u.c0, u.w, u.m, par);
+    }
+  }
   // ---- hand-off scatter list: panel (lower) entries -> kd_dense.cu's tile
   // layout for n = S (tiles of 32, off-diagonal row stride 33, packed
   // diagonal tiles)
@@ -554,8 +562,6 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
   {  // per-warp shared memory of kd_sparse.cu: Lv | v t + 5 PADMM vectors (or Gram staging) | partials | 2 int16 maps
     const int Sp = (S + 1) & ~1;
     p.smem_doubles = ((nLv + 1) & ~1) + p.vreg + p.max_slots + (Sp + 1) / 2 + 1;
-    p.vreg_h = 12 * p.kmax + Sp;
-    p.smem_doubles_h = ((nLv + 1) & ~1) + p.vreg_h + (Sp + 1) / 2 + 1;
   }
   return true;
 }

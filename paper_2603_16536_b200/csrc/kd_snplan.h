@@ -46,8 +46,6 @@ struct SnPlanHost {
   int n_sph = 0;         // solve phases
   int kmax = 0;          // most rows touching one body
   int vreg = 0;          // per-warp vector region (doubles)
-  int vreg_h = 0;        // hand-off layout (factor only): Gram staging + P
-  int smem_doubles_h = 0;  // per-warp footprint of the factor-only (hand-off) kernel
   uint64_t lmask = 0;      // nonzero 32x32 tiles of L (tile ti(ti+1)/2 + tj), for S <= 256
   uint64_t xmask = 0;      // nonzero 32x32 tiles of X = L^-1 (same numbering)
   std::vector<int32_t> pair_slot;   // per collision pair: first contact slot, -1 if unplanned

@@ -48,8 +48,7 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   if (slot_idx >= count) return;
   const int w = worlds[slot_idx];
   WorldStep& ws = bv.wstep[w];
-  if (ws.backend != BE_SPARSE && ws.backend != BE_DENSE_SN) return;
-  const bool handoff = ws.backend == BE_DENSE_SN;  // factor only; the dense kernel solves
+  if (ws.backend != BE_SPARSE) return;
   const DevWorld W = bv.worlds[w];
   const DevSnPlan P = bv.snplan[W.model];
   const DevModel M = bv.models[W.model];
@@ -62,12 +61,9 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
   double* z_s = y_s + Sp;
   double* yh_s = z_s + Sp;
   double* zh_s = yh_s + Sp;
-  // factor-only CTAs (a hand-off model's bin) use a smaller layout: no PADMM
-  // vectors or partials, no solve program, so more worlds fit per SM
-  const bool hlay = prog_words == 0;
-  const int vreg = hlay ? P.vreg_h : P.vreg;
+  const int vreg = P.vreg;
   double* part = v + vreg;
-  int16_t* row2pos = reinterpret_cast<int16_t*>(part + (hlay ? 0 : P.max_slots));
+  int16_t* row2pos = reinterpret_cast<int16_t*>(part + P.max_slots);
   int16_t* slot2row = row2pos + Sp;
 
   const int64_t R0 = W.row_off;
@@ -211,7 +207,7 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
         __syncwarp();
       }
       // X = L_SS^-1, lane j owns column j (X_ij = -(sum_{q=j}^{i-1} L_iq X_qj) / L_ii)
-      if (!handoff && lane < u.w) {
+      if (lane < u.w) {
         const int j = lane;
         for (int i = j + 1; i < u.w; ++i) {
           double s0 = 0.0, s1 = 0.0;
@@ -248,12 +244,6 @@ __global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams
     }
   }
   stamp(2);
-  if (handoff) {  // the factor (panels, 1/L_jj on their diagonals) and the row map go to the dense kernel
-    double* dst = bv.sn_lv + W.snlv_off;
-    for (int e = lane; e < P.nLv; e += 32) dst[e] = Lv[e];
-    for (int r = lane; r < n; r += 32) bv.sn_r2p[W.snr2p_off + r] = row2pos[r];
-    return;
-  }
 
   // ---- 3. PADMM (padmm.cpp:87-159); units = bilateral/limit rows and contact triples.
   // The solve result x stays in v (at the row's position) until the same lane
