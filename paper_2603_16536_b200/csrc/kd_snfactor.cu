@@ -28,6 +28,39 @@ namespace {
 constexpr int kFactorThreads = 128;
 constexpr int kFactorMinBlocks = 5;
 __host__ __device__ __forceinline__ int pad2(int x) { return (x + 1) & ~1; }
+
+// Panel factor with the panel in registers (rows <= 32, width <= WMAX <= 24): lane q
+// holds row q.  Column c: the pivot comes from lane c, rows below it scale by
+// 1/L_cc, then row q's columns j in (c, w) take -= L_qc L_jc with L_jc from
+// lane j.  Same operations, operands and order as the shared-memory version
+// (one fused multiply-add per update), so the factor is bit-identical.
+template <int WMAX>
+__device__ __forceinline__ bool panel_factor_reg(double* Pn, int w, int rows, int ld, int lane) {
+  bool bad = false;
+  double row[WMAX];
+#pragma unroll
+  for (int c = 0; c < WMAX; ++c) row[c] = (c < w && lane < rows) ? Pn[c * ld + lane] : 0.0;
+#pragma unroll
+  for (int c = 0; c < WMAX; ++c) {
+    if (c < w) {  // warp-uniform
+      const double d = __shfl_sync(0xffffffffu, row[c], c);
+      if (!(d > 0.0)) bad = true;
+      const double r = fast_rsqrt(d);
+      row[c] = lane > c ? row[c] * r : (lane == c ? r : row[c]);  // the diagonal keeps 1/L_cc
+      // L_jc from lane j: unconditional shuffles (no divergent region), predicated updates
+#pragma unroll
+      for (int j = c + 1; j < WMAX; ++j) {
+        const double ljc = __shfl_sync(0xffffffffu, row[c], j);
+        if (j < w && lane >= j) row[j] -= row[c] * ljc;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < WMAX; ++c)
+    if (c < w && lane >= c && lane < rows) Pn[c * ld + lane] = row[c];
+  return bad;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
@@ -54,6 +87,7 @@ __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
   const int first_contact = n_jd + ws.n_limits;
   const uint16_t* slot_pos = bv.sn_slot_pos + P.slotpos_off;
 
+  long long t0 = clock64(), c_panel = 0, c_upd = 0, c_fn = 0;
   // ---- 0. zero the factor, map compact rows <-> planned slots
   for (int e = tid; e < P.nLv; e += NT) Lv[e] = 0.0;
   for (int s = tid; s < S; s += NT) slot2row[s] = s < n_jd ? (int16_t)s : (int16_t)-1;
@@ -91,13 +125,13 @@ __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
     const double* reg = bv.reg + R0;
     const double eta_rho = sp.eta + sp.rho;
     const SnGram* gl = bv.sn_gram + P.gram_off;
-    for (int e = tid; e < P.n_gram; e += NT) {
-      const SnGram g = gl[e];
+    // two entries per thread and pass, so their descriptor and J loads overlap
+    auto entry = [&](const SnGram g) {
       const int rs = slot2row[g.s], rt = slot2row[g.t];
       const bool diag = g.flags & SG_DIAG;
       if (rs < 0 || rt < 0) {
         if (diag) Lv[g.dst] = 1.0;
-        continue;
+        return;
       }
       const double* a = rj[rs].JM + ((g.flags & SG_S1) ? 6 : 0);
       const double* c = rj[rt].J + ((g.flags & SG_T1) ? 6 : 0);
@@ -116,18 +150,43 @@ __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
       double d = (Ps[rs] * s) * Ps[rt];
       if (diag) d += eta_rho;
       Lv[g.dst] = d;
+    };
+    for (int e = tid; e < P.n_gram; e += 2 * NT) {
+      const SnGram g0 = gl[e];
+      const bool two = e + NT < P.n_gram;
+      const SnGram g1 = two ? gl[e + NT] : g0;
+      entry(g0);
+      if (two) entry(g1);
     }
   }
   __syncthreads();
 
   // ---- 2. supernodal right-looking Cholesky in postorder
+  const long long t1 = clock64();
   bool bad = false;
   const SnSuper* sup = bv.sn_sup + P.sup_off;
+  SnSuper un = sup[0];
   for (int k = 0; k < P.n_sup; ++k) {
-    const SnSuper u = sup[k];
+    const long long q0 = clock64();
+    const SnSuper u = un;
+    if (k + 1 < P.n_sup) un = sup[k + 1];  // next descriptor in flight during this supernode
     double* Pn = Lv + u.pb;
     const int rows = u.w + u.m;
-    if (wid == 0) {
+    // this thread's first target-map words, loaded while warp 0 factors the panel
+    const int T = u.m * (u.m + 1) / 2;
+    const uint32_t* tm = bv.sn_tmap + u.tmap_off;
+    constexpr int kTE = 4;
+    uint32_t tep[kTE];
+#pragma unroll
+    for (int i = 0; i < kTE; ++i) tep[i] = tid + i * NT < T ? tm[tid + i * NT] : 0u;
+    if (wid == 0 && rows <= 32 && u.w <= 16) {
+      const long long f0 = clock64();
+      const bool b = u.w <= 8 ? panel_factor_reg<8>(Pn, u.w, rows, u.ld, lane)
+                              : panel_factor_reg<16>(Pn, u.w, rows, u.ld, lane);
+      bad = bad || b;
+      __syncwarp();
+      c_fn += clock64() - f0;
+    } else if (wid == 0) {
       for (int c = 0; c < u.w; ++c) {
         double* col = Pn + c * u.ld;
         const double d = col[c];
@@ -156,12 +215,15 @@ __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
       }
     }
     __syncthreads();
+    const long long q1 = clock64();
     // ancestors: A_ij -= sum_c L_ic L_jc for i >= j in the row structure
-    const int T = u.m * (u.m + 1) / 2;
     if (T > 0) {
-      const uint32_t* tm = bv.sn_tmap + u.tmap_off;
-      for (int e = tid; e < T; e += NT) {
-        const uint32_t te = tm[e];
+      for (int e = tid, i = 0; e < T; e += NT, ++i) {
+        uint32_t te = tep[0];
+#pragma unroll
+        for (int q = 1; q < kTE; ++q)
+          if (i == q) te = tep[q];
+        if (i >= kTE) te = tm[e];
         const double* a = Pn + u.w + ((te >> 16) & 0xff);
         const double* b = Pn + u.w + (te >> 24);
         double s0 = 0.0, s1 = 0.0;
@@ -175,6 +237,14 @@ __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
       }
       __syncthreads();
     }
+    c_panel += q1 - q0;
+    c_upd += clock64() - q1;
+  }
+  if (tid == 0) {
+    ws.phase_cycles[5] = t1 - t0;
+    ws.phase_cycles[6] = c_panel;
+    ws.phase_cycles[7] = c_upd;
+    ws.phase_cycles[1] = c_fn;
   }
   if (__syncthreads_or(bad) && tid == 0) {
     ws.fail = 1;
