@@ -1,6 +1,3 @@
-#include <set>
-#include <cstdio>
-#include <cstdlib>
 // kd_snplan.cpp — host construction of the supernodal sparse LLT plan
 // (see kd_snplan.h) and a CPU interpreter used only by the self-test.
 //
@@ -228,14 +225,6 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       for (int i : cs[j]) p.lmask |= 1ull << ((i / 32) * (i / 32 + 1) / 2 + j / 32);
     }
     // X = L^-1: X_ij != 0 only if i is j or an elimination-tree ancestor of j
-    if (getenv("KD_DBG_X")) {
-      long nx = 0;
-      std::set<std::pair<int,int>> t16, t8;
-      for (int j = 0; j < S; ++j)
-        for (int i = j;; i = cs[i][0]) { ++nx; t16.insert({i/16,j/16}); t8.insert({i/8,j/8}); if (cs[i].empty()) break; }
-      fprintf(stderr, "S=%d nnzX=%ld dense=%d tiles16=%zu (%d) tiles8=%zu (%d)\n", S, nx, S*(S+1)/2, t16.size(), ((S+15)/16)*((S+15)/16+1)/2, t8.size(), ((S+7)/8)*((S+7)/8+1)/2);
-      for (int i = 0; i < S; i += 8) { for (int j = 0; j <= i; j += 8) fputc(t8.count({i/8,j/8}) ? '#' : '.', stderr); fputc('\n', stderr); }
-    }
     p.xmask = 0;
     for (int j = 0; j < S; ++j)
       for (int i = j;; i = cs[i][0]) {
@@ -297,14 +286,6 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
     const SnSuper& u = p.sup[snid[j]];
     return u.xb + (i - u.c0) * u.ws + (j - u.c0);
   };
-  if (getenv("KD_DBG_X")) {
-    for (size_t k = 0; k < p.sup.size(); ++k) {
-      const SnSuper& u = p.sup[k];
-      int par = -1;
-      if (u.m > 0) { const int r = p.prow[u.prow_off + u.w]; for (size_t q = 0; q < p.sup.size(); ++q) if (r >= p.sup[q].c0 && r < p.sup[q].c0 + p.sup[q].w) par = (int)q; }
-      fprintf(stderr, "sn %zu c0=%d w=%d m=%d parent=%d\n", k, u.c0, u.w, u.m, par);
-    }
-  }
   // ---- hand-off scatter list: panel (lower) entries -> kd_dense.cu's tile
   // layout for n = S (tiles of 32, off-diagonal row stride 33, packed
   // diagonal tiles)

@@ -63,6 +63,9 @@ b.step(cfg, 1)
 pc = b.phase_cycles()
 its = np.array([x.iterations for x in b.diagnostics()[:148]])
 names = ["gram_scaled", "unused", "cholesky", "inverse", "padmm", "chol_panel", "chol_syrk", "chol_diag"]
+if b.kernels()[0] == "supernodal+dense":  # slots 1, 5-7 come from the hand-off factor kernel (kd_snfactor.cu)
+    names = ["scatter_diag_inverse", "k2f_panel_factor", "unused", "inverse", "padmm", "k2f_gram", "k2f_panels",
+             "k2f_updates"]
 print(json.dumps({"kernel": b.kernels()[0], "phase_cycles_mean": {names[k]: float(pc[:, k].mean()) for k in range(8)},
                   "iters_mean": float(its.mean()),
                   "padmm_cycles_per_iter": float((pc[:, 4] / np.maximum(its, 1)).mean())}), flush=True)
