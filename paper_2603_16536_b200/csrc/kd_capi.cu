@@ -592,6 +592,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       d.max_slots = p.max_slots;
       d.lmask_lo = (int32_t)(uint32_t)(p.lmask & 0xffffffffull);
       d.lmask_hi = (int32_t)(uint32_t)(p.lmask >> 32);
+      d.xmask_lo = (int32_t)(uint32_t)(p.xmask & 0xffffffffull);
+      d.xmask_hi = (int32_t)(uint32_t)(p.xmask >> 32);
       d.n_sph = p.n_sph;
       d.gram_off = (int)gram.size();
       d.n_gram = (int)p.gram.size();

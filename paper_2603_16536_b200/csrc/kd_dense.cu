@@ -331,42 +331,44 @@ __device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, 
 
 // Overwrite the Cholesky factor (diag tiles already inverted) with X = L^{-1}
 // by right-looking block forward substitution on L X = I.
-// lmask: bit ti(ti+1)/2 + tj set for every tile of L that can be nonzero
-// (all ones unless the factor came from a supernodal plan); a zero tile
-// L_i,kk contributes nothing to phases 2 and 3 and stays zero.
-__device__ __forceinline__ bool ltile(unsigned long long lmask, int ti, int tj) {
-  return (lmask >> (ti * (ti + 1) / 2 + tj)) & 1ull;
+// lmask / xmask: bit ti(ti+1)/2 + tj set for every tile of L / of X that can
+// be nonzero (all ones unless the factor came from a supernodal plan).  A zero
+// tile L_i,kk contributes nothing to phases 2 and 3; a structurally zero tile
+// X_kk,j is never formed (phase 1) nor used (phase 2).
+__device__ __forceinline__ bool mtile(unsigned long long mask, int ti, int tj) {
+  return (mask >> (ti * (ti + 1) / 2 + tj)) & 1ull;
 }
 template <int NT>
-__device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask) {
+__device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, unsigned long long xmask) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto nth_bit = [](unsigned m, int q) {  // position of the q-th set bit
+    for (int t = 0; t < q; ++t) m &= m - 1;
+    return __ffs(m) - 1;
+  };
   for (int k = 1; k < T; ++k) {
     // the column-(k-1) contributions B_i,k-1 = -L_i,k-1 Linv_k-1 (phase 3 of step k-1)
     // and B_ij -= L_i,k-1 X_k-1,j (phase 2) are applied below, in order.
     const int kk = k - 1;
-    // phase 1 (step kk): X_kk,j = Linv_kk B_kk,j for j < kk
-    for (int u = wid; u < kk; u += NW) trmm_left(L, kk, u, n, lane);
-    __syncthreads();
-    // rows i > kk whose tile L_i,kk is nonzero
-    unsigned rows = 0;
+    unsigned rows = 0, cols = 0;  // rows i > kk with L_i,kk != 0; columns j < kk with X_kk,j != 0
     for (int i = kk + 1; i < T; ++i)
-      if (ltile(lmask, i, kk)) rows |= 1u << i;
-    const int below = __popc(rows);
-    auto row_at = [&](int q) {  // q-th set bit
-      unsigned r = rows;
-      for (int t = 0; t < q; ++t) r &= r - 1;
-      return __ffs(r) - 1;
-    };
+      if (mtile(lmask, i, kk)) rows |= 1u << i;
+    for (int j = 0; j < kk; ++j)
+      if (mtile(xmask, kk, j)) cols |= 1u << j;
+    const int below = __popc(rows), nc = __popc(cols);
+    // phase 1 (step kk): X_kk,j = Linv_kk B_kk,j for j < kk
+    for (int u = wid; u < nc; u += NW) trmm_left(L, kk, nth_bit(cols, u), n, lane);
+    __syncthreads();
     // phase 2 (step kk): B_ij -= L_i,kk X_kk,j for i > kk, j < kk
-    for (int u = wid; u < below * kk; u += NW) gemm_sub(L, row_at(u / kk), u % kk, kk, n, lane);
+    for (int u = wid; u < below * nc; u += NW) gemm_sub(L, nth_bit(rows, u / nc), nth_bit(cols, u % nc), kk, n, lane);
     __syncthreads();
     // phase 3 (step kk): B_i,kk = -L_i,kk Linv_kk for i > kk
-    for (int u = wid; u < below; u += NW) trmm_right_neg(L, row_at(u), kk, n, lane);
+    for (int u = wid; u < below; u += NW) trmm_right_neg(L, nth_bit(rows, u), kk, n, lane);
     __syncthreads();
   }
   // final step T-1: X_T-1,j = Linv B for j < T-1
-  for (int u = wid; u < T - 1; u += NW) trmm_left(L, T - 1, u, n, lane);
+  for (int u = wid; u < T - 1; u += NW)
+    if (mtile(xmask, T - 1, u)) trmm_left(L, T - 1, u, n, lane);
   __syncthreads();
 }
 
@@ -376,7 +378,8 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask) {
 // Padded tiles give both walks constant offsets and no bank conflicts; the
 // broadcast vector operand is read as double2 (one wavefront per two entries).
 template <int NT>
-__device__ void inv_solve(const double* X, double* b, double* w, int n, int T, long long* prof = nullptr) {
+__device__ void inv_solve(const double* X, double* b, double* w, int n, int T, unsigned long long xmask,
+                          long long* prof = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __syncthreads();
 #ifdef KD_PROF_PADMM
@@ -387,6 +390,7 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, l
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (r < ri) {
       for (int j = 0; j < i; ++j) {
+        if (!mtile(xmask, i, j)) continue;  // structurally zero tile of L^-1
         const double* row = X + off_tile(i, j, n) + r * LDT;
         const double2* bj = reinterpret_cast<const double2*>(b + 32 * j);
 #pragma unroll
@@ -427,6 +431,7 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, l
         if (r + 1 >= c && r + 1 < rj) a1 += D[tri(r + 1) + c] * ww.y;
       }
       for (int i = j + 1; i < T; ++i) {
+        if (!mtile(xmask, i, j)) continue;
         const int ri = tile_rows(i, n);
         const double* A = X + off_tile(i, j, n) + c;
         const double2* wi = reinterpret_cast<const double2*>(w + 32 * i);
@@ -649,9 +654,16 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
   stamp(2);
   }  // !handoff
   // ---- 2b. X = L^{-1}: every PADMM solve becomes two parallel mat-vecs
-  tri_inverse<NT>(L, n, T, handoff ? ((unsigned long long)(uint32_t)bv.snplan[W.model].lmask_hi << 32) |
-                                          (uint32_t)bv.snplan[W.model].lmask_lo
-                                    : ~0ull);
+  unsigned long long xm = ~0ull;
+  {
+    unsigned long long lm = ~0ull;
+    if (handoff) {
+      const DevSnPlan& SP = bv.snplan[W.model];
+      lm = ((unsigned long long)(uint32_t)SP.lmask_hi << 32) | (uint32_t)SP.lmask_lo;
+      xm = ((unsigned long long)(uint32_t)SP.xmask_hi << 32) | (uint32_t)SP.xmask_lo;
+    }
+    tri_inverse<NT>(L, n, T, lm, xm);
+  }
   stamp(3);
 
   // ---- 3. PADMM (padmm.cpp:87-159), one cone unit per thread
@@ -708,7 +720,7 @@ __global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams s
 #ifdef KD_PROF_PADMM
     const long long p0 = clock64();
 #endif
-    inv_solve<NT>(L, xv, wv_s, n, T, prof);
+    inv_solve<NT>(L, xv, wv_s, n, T, xm, prof);
 #ifdef KD_PROF_PADMM
     const long long p1 = clock64();
 #endif

@@ -127,6 +127,7 @@ struct DevSnPlan {
   int32_t n_sph, max_slots, smem_doubles, pad0;  // smem_doubles: per-warp footprint of K2s
   int32_t gbody_off, n_gbody, kmax, vreg;  // vreg: per-warp vector region (doubles)
   int32_t lmask_lo, lmask_hi, scat_off, n_scat;  // nonzero 32x32 tiles of L in plan order; hand-off scatter list
+  int32_t xmask_lo, xmask_hi, pad1, pad2;        // nonzero 32x32 tiles of L^-1
 };
 
 // Per-world indexing (prefix sums over model capacities).
