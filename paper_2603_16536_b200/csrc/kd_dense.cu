@@ -444,9 +444,15 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, u
             a2 += A[(r + 2) * LDT] * w23.x;
             a3 += A[(r + 3) * LDT] * w23.y;
           }
-        } else {
-          const double* wr = w + 32 * i;
-          for (int r = 0; r < ri; ++r) a0 += A[r * LDT] * wr[r];
+        } else {  // the last tile row: same walk, rows >= ri predicated off
+#pragma unroll
+          for (int r = 0; r < 32; r += 4) {
+            const double2 w01 = wi[r / 2], w23 = wi[r / 2 + 1];
+            if (r < ri) a0 += A[r * LDT] * w01.x;
+            if (r + 1 < ri) a1 += A[(r + 1) * LDT] * w01.y;
+            if (r + 2 < ri) a2 += A[(r + 2) * LDT] * w23.x;
+            if (r + 3 < ri) a3 += A[(r + 3) * LDT] * w23.y;
+          }
         }
       }
       b[32 * j + c] = (a0 + a1) + (a2 + a3);
