@@ -370,8 +370,8 @@ def main():
         fam, fam_ms, fam_bytes = "dense", dense_ms, bytes_dense / rsteps
         nd, nh, ns = (kern_count.get(k, 0) for k in ("dense", "supernodal+dense", "supernodal"))
         if nh >= max(nd, ns):
-            kname = ("dense_kernel (K2 after the K2s supernodal factor hand-off: L^-1 + explicit-inverse PADMM, "
-                     "smem-resident; the family time includes the factor kernel)")
+            kname = ("dense_kernel (K2 after the K2f supernodal factor kernel: L^-1 + explicit-inverse PADMM, "
+                     "smem-resident; the family time includes K2f)")
         elif nd >= ns:
             kname = "dense_kernel (K2: Delassus assembly + Cholesky + explicit-inverse PADMM, smem-resident)"
         else:

@@ -13,6 +13,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:dens
   -o gpurun_out/${TAG}_dense python tests/ncu_target.py 148 62 > gpurun_out/${TAG}_ncu_dense.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cr_kernel -s 10 -c 1 \
   -o gpurun_out/${TAG}_cr python tests/ncu_target_cr.py 296 12 > gpurun_out/${TAG}_ncu_cr.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:snfactor_kernel -s 60 -c 1 \
+  -o gpurun_out/${TAG}_snfactor python tests/ncu_target.py 4096 62 > gpurun_out/${TAG}_ncu_snfactor.log 2>&1
 KD_SPARSE=2 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_kernel -s 60 -c 1 \
   -o gpurun_out/${TAG}_sparse python tests/ncu_target.py 444 62 > gpurun_out/${TAG}_ncu_sparse.log 2>&1
 tail -2 gpurun_out/${TAG}_smoke.txt; tail -3 gpurun_out/${TAG}_pytest_gpu.txt
