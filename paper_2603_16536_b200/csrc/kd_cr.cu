@@ -14,6 +14,7 @@
 #include "kd_device.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace kd {
 
@@ -141,14 +142,15 @@ __device__ void apply_op(const CrCtx& c, const double* v, double* out) {
 
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds,
-                                                  int smem_doubles) {
+                                                  int smem_doubles, int n_reg) {
   extern __shared__ __align__(16) double smem[];
   const int w = bin_worlds[blockIdx.x];
   WorldStep& ws = bv.wstep[w];
   if (ws.backend != BE_MATRIX_FREE) return;
+  const int n = ws.n_rows;
+  if (n <= n_reg) return;  // cr_reg_kernel took it
   const int tid = threadIdx.x;
   const DevWorld W = bv.worlds[w];
-  const int n = ws.n_rows;
   const int nb = W.nb;
   const int64_t R0 = W.row_off;
   // shared layout
@@ -376,6 +378,425 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2b' cr_reg_kernel<NT, RPT>: the same PADMM + warm-started CR, with the CR
+// state held in registers.  Thread t owns rows t, t + NT, ... (at most RPT):
+// its P-scaled Jacobian blocks ja = P J (bake_jacobian, delassus.cpp:139-146),
+// diag_add and the CR vectors x, r, p, Ap stay in registers for the whole
+// step, so an apply moves 12 doubles per row through shared memory instead of
+// re-reading J, M^-1 and index lists per incidence:
+//   A  row owner:  prod[e] = ja_side * v_r, written to the row's slot e of its
+//                  body's ascending incidence list (the CSR K1 builds);
+//   B  body half:  s_b = sum_e prod[e] in ascending row order (the reference
+//                  scatter order, delassus.cpp:108-113), w_b = M_b^-1 s_b;
+//   C  row owner:  out_r = diag_add v_r + ja_a . w_a + ja_b . w_b.
+// ja . (M^-1 s) is the reference's jma . s (jma = fold_inverse_mass(ja),
+// delassus.cpp:12-17, M^-1 symmetric) with the product re-associated.
+// Block reductions use one barrier each (double-buffered partials, every
+// thread sums the warp partials in the same fixed order).  Worlds with
+// n > RPT * NT are left to cr_kernel (runtime check on both sides).
+// ---------------------------------------------------------------------------
+namespace {
+
+template <int NT, int K>
+__device__ __forceinline__ void bsum(double (&v)[K], double* red, int& par) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* buf = red + par * (NW * K);
+  par ^= 1;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) buf[wid * K + k] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = buf[k];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) s += buf[i * K + k];
+    v[k] = s;
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void bmax3(double& a, double& b, double& c, double* red, int& par) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* buf = red + par * (NW * 3);
+  par ^= 1;
+  a = warp_max_nonneg(a);
+  b = warp_max_nonneg(b);
+  c = warp_max_nonneg(c);
+  if (lane == 0) {
+    buf[3 * wid] = a;
+    buf[3 * wid + 1] = b;
+    buf[3 * wid + 2] = c;
+  }
+  __syncthreads();
+  a = buf[0];
+  b = buf[1];
+  c = buf[2];
+#pragma unroll
+  for (int i = 1; i < NW; ++i) {
+    a = fmax(a, buf[3 * i]);
+    b = fmax(b, buf[3 * i + 1]);
+    c = fmax(c, buf[3 * i + 2]);
+  }
+}
+
+template <int NT, int RPT>
+struct RegRows {
+  double ja[RPT][12];
+  double dadd[RPT];
+  int ea[RPT], eb[RPT];  // incidence slots (or -1)
+  int ba[RPT], bb[RPT];  // bodies (or -1)
+};
+
+template <int NT, int RPT>
+__device__ __forceinline__ void apply_reg(const RegRows<NT, RPT>& R, int n, int nb, const double (&v)[RPT],
+                                          double (&out)[RPT], double* prod, double* wv, const double* binv,
+                                          const int32_t* cptr) {
+  const int tid = threadIdx.x;
+  // A: per-incidence products ja^T v_r
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    if (tid + k * NT < n) {
+      if (R.ea[k] >= 0) {
+        double2* d = reinterpret_cast<double2*>(prod + 6 * R.ea[k]);
+        d[0] = make_double2(R.ja[k][0] * v[k], R.ja[k][1] * v[k]);
+        d[1] = make_double2(R.ja[k][2] * v[k], R.ja[k][3] * v[k]);
+        d[2] = make_double2(R.ja[k][4] * v[k], R.ja[k][5] * v[k]);
+      }
+      if (R.eb[k] >= 0) {
+        double2* d = reinterpret_cast<double2*>(prod + 6 * R.eb[k]);
+        d[0] = make_double2(R.ja[k][6] * v[k], R.ja[k][7] * v[k]);
+        d[1] = make_double2(R.ja[k][8] * v[k], R.ja[k][9] * v[k]);
+        d[2] = make_double2(R.ja[k][10] * v[k], R.ja[k][11] * v[k]);
+      }
+    }
+  }
+  __syncthreads();
+  // B: body halves (linear / angular), ascending incidences, then M^-1
+  for (int u = tid; u < 2 * nb; u += NT) {
+    const int b = u >> 1;
+    const int e0 = cptr[b], e1 = cptr[b + 1];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if ((u & 1) == 0) {
+      for (int e = e0; e < e1; ++e) {
+        const double2 a = *reinterpret_cast<const double2*>(prod + 6 * e);
+        s0 += a.x;
+        s1 += a.y;
+        s2 += prod[6 * e + 2];
+      }
+      const double im = binv[10 * b];
+      wv[6 * b] = im * s0;
+      wv[6 * b + 1] = im * s1;
+      wv[6 * b + 2] = im * s2;
+    } else {
+      for (int e = e0; e < e1; ++e) {
+        const double2 a = *reinterpret_cast<const double2*>(prod + 6 * e + 4);
+        s0 += prod[6 * e + 3];
+        s1 += a.x;
+        s2 += a.y;
+      }
+      const double* I = binv + 10 * b + 1;
+      wv[6 * b + 3] = (I[0] * s0 + I[1] * s1) + I[2] * s2;
+      wv[6 * b + 4] = (I[3] * s0 + I[4] * s1) + I[5] * s2;
+      wv[6 * b + 5] = (I[6] * s0 + I[7] * s1) + I[8] * s2;
+    }
+  }
+  __syncthreads();
+  // C: gather
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    double s = R.dadd[k] * v[k];
+    if (R.ba[k] >= 0) {
+      const double2* w = reinterpret_cast<const double2*>(wv + 6 * R.ba[k]);
+      const double2 w0 = w[0], w1 = w[1], w2 = w[2];
+      s += ((R.ja[k][0] * w0.x + R.ja[k][1] * w0.y) + (R.ja[k][2] * w1.x + R.ja[k][3] * w1.y)) +
+           (R.ja[k][4] * w2.x + R.ja[k][5] * w2.y);
+    }
+    if (R.bb[k] >= 0) {
+      const double2* w = reinterpret_cast<const double2*>(wv + 6 * R.bb[k]);
+      const double2 w0 = w[0], w1 = w[1], w2 = w[2];
+      s += ((R.ja[k][6] * w0.x + R.ja[k][7] * w0.y) + (R.ja[k][8] * w1.x + R.ja[k][9] * w1.y)) +
+           (R.ja[k][10] * w2.x + R.ja[k][11] * w2.y);
+    }
+    out[k] = s;
+  }
+}
+
+}  // namespace
+
+// shared memory (doubles) of cr_reg_kernel for n rows / nb bodies:
+// 6 n vectors | prod 12 n | w 6 nb | binv 10 nb | red | int: cptr nb+1, slot 2n
+static size_t cr_reg_smem_bytes(int n, int nb, int nt) {
+  return 8 * ((size_t)18 * n + 16 * (size_t)nb + 2 * 3 * (nt / 32) + 8) + 4 * ((size_t)nb + 1 + 2 * n) + 16;
+}
+
+template <int NT, int RPT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
+  extern __shared__ __align__(16) double smem[];
+  const int w = bin_worlds[blockIdx.x];
+  WorldStep& ws = bv.wstep[w];
+  if (ws.backend != BE_MATRIX_FREE) return;
+  const int n = ws.n_rows;
+  if (n > RPT * NT) return;  // cr_kernel takes it
+  const int tid = threadIdx.x;
+  const DevWorld W = bv.worlds[w];
+  const int nb = W.nb;
+  const int64_t R0 = W.row_off;
+  double* yv = smem;
+  double* zv = yv + n;
+  double* yh = zv + n;
+  double* zh = yh + n;
+  double* vf = zh + n;
+  double* xs = vf + n;
+  double* prod = xs + n;           // 6 per incidence (<= 2n incidences)
+  double* wv = prod + 12 * n;      // 6 nb
+  double* binv = wv + 6 * nb;      // 10 nb
+  double* red = binv + 10 * nb;    // 2 buffers x 3 x NW
+  int32_t* cptr = reinterpret_cast<int32_t*>(red + 2 * 3 * (NT / 32));
+  int32_t* slot = cptr + nb + 1;   // code (2 r + side) -> incidence index
+
+  const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
+  const double inv_rho = 1.0 / rho;
+  const int32_t* cptr_g = bv.csr_ptr + W.body_off + w;
+  const int32_t* cl_g = bv.csr + 2 * R0;
+  for (int b = tid; b <= nb; b += NT) cptr[b] = cptr_g[b];
+  for (int e = tid; e < 2 * n; e += NT) slot[e] = -1;
+  for (int b = tid; b < nb; b += NT) {
+    const BodyS& B = bv.bs[W.body_off + b];
+    binv[10 * b] = B.inv_mass;
+    for (int k = 0; k < 9; ++k) binv[10 * b + 1 + k] = B.Iwinv[k];
+  }
+  __syncthreads();
+  const int ninc = cptr[nb];
+  for (int e = tid; e < ninc; e += NT) slot[cl_g[e]] = e;
+  RegRows<NT, RPT> R;
+  double x[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int r = tid + k * NT;
+    x[k] = 0.0;
+    R.dadd[k] = 0.0;
+    R.ba[k] = R.bb[k] = -1;
+#pragma unroll
+    for (int i = 0; i < 12; ++i) R.ja[k][i] = 0.0;
+    if (r < n) {
+      const double p = bv.scale[R0 + r];
+      R.dadd[k] = p * p * bv.reg[R0 + r] + eta_rho;
+      const double* J = bv.rowj[R0 + r].J;
+#pragma unroll
+      for (int i = 0; i < 12; ++i) R.ja[k][i] = p * J[i];  // bake_jacobian: ja = P J
+      R.ba[k] = bv.rbody[2 * (R0 + r)];
+      R.bb[k] = bv.rbody[2 * (R0 + r) + 1];
+      x[k] = bv.x0[R0 + r];
+      xs[r] = x[k];
+      vf[r] = bv.vf[R0 + r];
+      zv[r] = bv.z0[R0 + r];
+    }
+  }
+  __syncthreads();  // slot
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int r = tid + k * NT;
+    R.ea[k] = (r < n && R.ba[k] >= 0) ? slot[2 * r] : -1;
+    R.eb[k] = (r < n && R.bb[k] >= 0) ? slot[2 * r + 1] : -1;
+  }
+  const int n_jd = n - ws.n_limits - 3 * ws.n_contacts;
+  const int first_contact = n_jd + ws.n_limits;
+  const int n_units = first_contact + ws.n_contacts;
+  const double* rmu = bv.rmu + R0;
+
+  // y = Pi_K(x0); hats
+  for (int u = tid; u < n_units; u += NT) {
+    if (u < n_jd) {
+      yv[u] = xs[u];
+    } else if (u < first_contact) {
+      yv[u] = fmax(0.0, xs[u]);
+    } else {
+      const int r = first_contact + 3 * (u - first_contact);
+      double wv3[3] = {xs[r], xs[r + 1], xs[r + 2]}, yn[3];
+      project_soc(wv3, rmu[r], 1.0 / (1.0 + rmu[r] * rmu[r]), yn);
+      for (int d = 0; d < 3; ++d) yv[r + d] = yn[d];
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < n; r += NT) {
+    yh[r] = yv[r];
+    zh[r] = zv[r];
+  }
+  __syncthreads();
+  int par = 0;
+  double prev = __longlong_as_double(0x7ff0000000000000ll);
+  int m = 0;
+  double r_p = 0, r_d = 0, r_c = 0;
+  int restarts = 0, it;
+  bool converged = false;
+  long long cr_total = 0;
+  bool cr_break = false;
+  const int hcap = bv.hist_cap;
+  for (it = 1; it <= sp.max_iters; ++it) {
+    // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
+    double rhs[RPT], rr[RPT], pp[RPT], ap[RPT], ar[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * NT;
+      rhs[k] = 0.0;
+      if (r < n) {
+        double s = 0.0;
+        if (r >= first_contact && ((r - first_contact) % 3) == 0)
+          s = rmu[r] * fast_sqrt(zh[r + 1] * zh[r + 1] + zh[r + 2] * zh[r + 2]);
+        rhs[k] = -((((vf[r] + s) - eta * x[k]) - rho * yh[r]) - zh[r]);
+      }
+    }
+    // ---- cr_solve(op, rhs, x, budget)   (delassus.cpp:156-187)
+    apply_reg<NT, RPT>(R, n, nb, x, ar, prod, wv, binv, cptr);
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) rr[k] = rhs[k] - ar[k];
+    apply_reg<NT, RPT>(R, n, nb, rr, ar, prod, wv, binv, cptr);
+    double d3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      pp[k] = rr[k];
+      ap[k] = ar[k];
+      d3[0] += rr[k] * ar[k];
+      d3[1] += rhs[k] * rhs[k];
+      d3[2] += ar[k] * ar[k];
+    }
+    bsum<NT, 3>(d3, red, par);
+    double rar = d3[0];
+    const double rhs2 = d3[1];
+    double apap = d3[2];
+    const double beps = 1e-30 * fmax(1.0, rhs2);
+    int iters = 0;
+    bool brk = false;
+    for (int kk = 0; kk < sp.cr_iters; ++kk) {
+      if (kk > 0) {
+        double a1[1] = {0.0};
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) a1[0] += ap[k] * ap[k];
+        bsum<NT, 1>(a1, red, par);
+        apap = a1[0];
+      }
+      if (!(rar > beps) || !(apap > beps)) {
+        brk = true;
+        break;
+      }
+      const double alpha = fast_div(rar, apap);
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        x[k] += alpha * pp[k];
+        rr[k] -= alpha * ap[k];
+      }
+      apply_reg<NT, RPT>(R, n, nb, rr, ar, prod, wv, binv, cptr);
+      double a1[1] = {0.0};
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) a1[0] += rr[k] * ar[k];
+      bsum<NT, 1>(a1, red, par);
+      const double beta = fast_div(a1[0], rar);
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        pp[k] = rr[k] + beta * pp[k];
+        ap[k] = ar[k] + beta * ap[k];
+      }
+      rar = a1[0];
+      ++iters;
+    }
+    cr_total += iters;
+    if (brk) {
+      double a1[1] = {0.0};
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) a1[0] += rr[k] * rr[k];
+      bsum<NT, 1>(a1, red, par);
+      if (sqrt(a1[0]) > 1e-9 * fmax(1.0, sqrt(rhs2))) cr_break = true;
+    }
+#pragma unroll
+    for (int k = 0; k < RPT; ++k)
+      if (tid + k * NT < n) xs[tid + k * NT] = x[k];
+    __syncthreads();
+    // ---- projection, dual update, residuals (padmm.cpp:120-123)
+    double rp = 0.0, dmax = 0.0, rc = 0.0;
+    for (int u = tid; u < n_units; u += NT) {
+      const int r = u < first_contact ? u : first_contact + 3 * (u - first_contact);
+      const int nr = u < first_contact ? 1 : 3;
+      double wv3[3], yn[3];
+      for (int d = 0; d < nr; ++d) wv3[d] = xs[r + d] - zh[r + d] * inv_rho;
+      if (u >= first_contact) project_soc(wv3, rmu[r], fast_rcp(1.0 + rmu[r] * rmu[r]), yn);
+      else if (u >= n_jd) yn[0] = fmax(0.0, wv3[0]);
+      else yn[0] = wv3[0];
+      double ymax = 0.0, zmax = 0.0;
+      for (int d = 0; d < nr; ++d) {
+        const double zn = zh[r + d] - rho * (xs[r + d] - yn[d]);
+        rp = fmax(rp, fabs(xs[r + d] - yn[d]));
+        dmax = fmax(dmax, fabs(yn[d] - yv[r + d]));
+        ymax = fmax(ymax, fabs(yn[d]));
+        zmax = fmax(zmax, fabs(zn));
+        yh[r + d] = yv[r + d];  // y_prev, z_prev until the Nesterov step
+        zh[r + d] = zv[r + d];
+        yv[r + d] = yn[d];
+        zv[r + d] = zn;
+      }
+      if (u >= n_jd) rc = fmax(rc, fmin(ymax, zmax));
+    }
+    bmax3<NT>(rp, dmax, rc, red, par);
+    r_p = rp;
+    r_d = rho * dmax;
+    r_c = rc;
+    const double combined = fmax(r_p, fmax(r_d, r_c));
+    if (tid == 0 && it <= hcap) bv.hist[(int64_t)w * hcap + it - 1] = combined;
+    if (!sp.fixed_mode && combined < sp.eps) {
+      converged = true;
+      break;
+    }
+    // Nesterov step on the rows of this thread's own units (no barrier needed
+    // between the projection and this update)
+    const bool restart = sp.acceleration && sp.restart && combined > prev;
+    if (restart) {
+      m = 0;
+      ++restarts;
+    }
+    const bool nest = sp.acceleration && !restart;
+    const double beta = nest ? sp.nest_beta[m] : 0.0;  // (a_m - 1) / a_{m+1}, host table
+    if (nest) ++m;
+    for (int u = tid; u < n_units; u += NT) {
+      const int r = u < first_contact ? u : first_contact + 3 * (u - first_contact);
+      const int nr = u < first_contact ? 1 : 3;
+      for (int d = 0; d < nr; ++d) {
+        if (nest) {
+          yh[r + d] = yv[r + d] + beta * (yv[r + d] - yh[r + d]);
+          zh[r + d] = zv[r + d] + beta * (zv[r + d] - zh[r + d]);
+        } else {
+          yh[r + d] = yv[r + d];
+          zh[r + d] = zv[r + d];
+        }
+      }
+    }
+    prev = combined;
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int r = tid; r < n; r += NT) {
+    bv.lam[R0 + r] = yv[r];
+    bv.zo[R0 + r] = zv[r];
+  }
+  if (tid == 0) {
+    const int done = min(it, sp.max_iters);
+    ws.iterations = done;
+    ws.r_p = r_p;
+    ws.r_d = r_d;
+    ws.r_c = r_c;
+    ws.restarts = restarts;
+    ws.converged = (converged || fmax(r_p, fmax(r_d, r_c)) < sp.eps) ? 1 : 0;
+    ws.cr_iterations = cr_total;
+    ws.cr_breakdown = cr_break ? 1 : 0;
+    for (int i = done; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
+  }
+}
+
 size_t cr_smem_bytes(int n, int nb, int nt) { return 8 * ((size_t)13 * n + 16 * (size_t)nb + 3 * (nt / 32) + 8); }
 // with the optional per-step staging of P J and the index lists
 static size_t cr_staged_bytes(int n, int nb, int nt) {
@@ -384,7 +805,7 @@ static size_t cr_staged_bytes(int n, int nb, int nt) {
 
 template <int NT, int MINB>
 static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap,
-                               int nbcap, cudaStream_t s) {
+                               int nbcap, int n_reg, cudaStream_t s) {
   const size_t smem = std::max(cr_smem_bytes(ncap, nbcap, NT),
                                std::min<size_t>(232448 / MINB, cr_staged_bytes(ncap, nbcap, NT)));
   static size_t configured = 0;
@@ -393,22 +814,65 @@ static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const 
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  cr_kernel<NT, MINB><<<count, NT, smem, s>>>(bv, sp, worlds, (int)(smem / 8));
+  cr_kernel<NT, MINB><<<count, NT, smem, s>>>(bv, sp, worlds, (int)(smem / 8), n_reg);
   return cudaGetLastError();
+}
+
+template <int NT, int RPT, int MINB>
+static cudaError_t launch_cr_reg_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
+                                   int ncap, int nbcap, cudaStream_t s) {
+  const size_t smem = cr_reg_smem_bytes(std::min(ncap, RPT * NT), nbcap, NT);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(cr_reg_kernel<NT, RPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cr_reg_kernel<NT, RPT, MINB><<<count, NT, smem, s>>>(bv, sp, worlds);
+  return cudaGetLastError();
+}
+
+static int cr_reg_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("KD_CR_REG");
+    m = e ? atoi(e) : 1;
+  }
+  return m;
 }
 
 cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
                       int nt, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
+  // register-resident CR for worlds with n <= 2 NT rows (runtime n), the
+  // shared-memory kernel for the rest (both launched over the bin; each skips
+  // the other's worlds)
+  int n_reg = 0;
+  if (cr_reg_mode() && cr_reg_smem_bytes(std::min(ncap, 1024), nbcap, 512) <= 232448) {
+    cudaError_t e;
+    if (ncap <= 256) {
+      n_reg = 256;
+      e = launch_cr_reg_t<128, 2, 4>(bv, sp, worlds, count, ncap, nbcap, s);
+    } else if (ncap <= 512) {
+      n_reg = 512;
+      e = launch_cr_reg_t<256, 2, 2>(bv, sp, worlds, count, ncap, nbcap, s);
+    } else {
+      n_reg = 1024;
+      e = launch_cr_reg_t<512, 2, 1>(bv, sp, worlds, count, ncap, nbcap, s);
+    }
+    if (e != cudaSuccess) return e;
+    if (ncap <= n_reg) return cudaSuccess;
+  }
   // two resident CTAs per SM whenever their (staged) shared memory fits: the
   // kernel is synchronisation/latency bound, so a second world hides it
   if (cr_staged_bytes(ncap, nbcap, 256) <= 232448 / 2) {
-    if (nt <= 128) return launch_cr_t<128, 2>(bv, sp, worlds, count, ncap, nbcap, s);
-    return launch_cr_t<256, 2>(bv, sp, worlds, count, ncap, nbcap, s);
+    if (nt <= 128) return launch_cr_t<128, 2>(bv, sp, worlds, count, ncap, nbcap, n_reg, s);
+    return launch_cr_t<256, 2>(bv, sp, worlds, count, ncap, nbcap, n_reg, s);
   }
-  if (nt <= 128) return launch_cr_t<128, 1>(bv, sp, worlds, count, ncap, nbcap, s);
-  if (nt <= 256) return launch_cr_t<256, 1>(bv, sp, worlds, count, ncap, nbcap, s);
-  return launch_cr_t<512, 1>(bv, sp, worlds, count, ncap, nbcap, s);
+  if (nt <= 128) return launch_cr_t<128, 1>(bv, sp, worlds, count, ncap, nbcap, n_reg, s);
+  if (nt <= 256) return launch_cr_t<256, 1>(bv, sp, worlds, count, ncap, nbcap, n_reg, s);
+  return launch_cr_t<512, 1>(bv, sp, worlds, count, ncap, nbcap, n_reg, s);
 }
 
 }  // namespace kd

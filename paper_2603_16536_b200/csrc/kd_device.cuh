@@ -91,6 +91,13 @@ __device__ __forceinline__ double fast_rcp(double x) {
   const double e = fma(-x, y, 1.0);
   return fma(y, fma(e, e, e), y);
 }
+// y / x from the estimate above plus one residual correction (q + r (y - x q)):
+// the correctly rounded quotient except in rare last-bit cases.
+__device__ __forceinline__ double fast_div(double y, double x) {
+  const double r = fast_rcp(x);
+  const double q = y * r;
+  return fma(fma(-x, q, y), r, q);
+}
 __device__ __forceinline__ double fast_sqrt(double x) {
   if (!(x > 1e-30 && x < 1e30)) return sqrt(x);
   return x * fast_rsqrt(x);

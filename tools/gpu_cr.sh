@@ -1,0 +1,11 @@
+#!/bin/bash
+# CR-path pass: GPU tests, closed-chain and sphere-pile bench lines (new and old CR kernel).
+TAG=${1:-x}
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/${TAG}_pytest_gpu.txt 2>&1
+for wl in closed_chain sphere_pile; do
+  timeout 600 python bench.py --workload $wl --steps 10 --warmup 3 --settle 10 --no-cpu > gpurun_out/${TAG}_bench_$wl.json 2> gpurun_out/${TAG}_bench_$wl.err
+done
+KD_CR_REG=0 timeout 600 python bench.py --workload closed_chain --steps 10 --warmup 3 --settle 10 --no-cpu --no-e2e > gpurun_out/${TAG}_bench_closed_chain_old.json 2>&1
+tail -3 gpurun_out/${TAG}_pytest_gpu.txt
+for f in gpurun_out/${TAG}_bench_*.json; do echo "$f: $(cut -c1-180 $f)"; done
