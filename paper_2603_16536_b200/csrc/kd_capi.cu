@@ -1077,7 +1077,7 @@ int kd_batch_get_phase_cycles(kd_batch* b, int64_t* out) {
   if (b->n_worlds)
     KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
   for (int w = 0; w < b->n_worlds; ++w)
-    for (int k = 0; k < 8; ++k) out[8 * w + k] = (ws[w].backend == BE_DENSE_SMEM || ws[w].backend == BE_SPARSE || ws[w].backend == BE_DENSE_SN) ? ws[w].phase_cycles[k] : 0;
+    for (int k = 0; k < 8; ++k) out[8 * w + k] = (ws[w].backend == BE_DENSE_SMEM || ws[w].backend == BE_SPARSE || ws[w].backend == BE_DENSE_SN || ws[w].backend == BE_MATRIX_FREE) ? ws[w].phase_cycles[k] : 0;
   return KD_OK;
 }
 

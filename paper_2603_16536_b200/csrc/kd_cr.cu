@@ -383,12 +383,13 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
 // state held in registers.  Thread t owns rows t, t + NT, ... (at most RPT):
 // its P-scaled Jacobian blocks ja = P J (bake_jacobian, delassus.cpp:139-146),
 // diag_add and the CR vectors x, r, p, Ap stay in registers for the whole
-// step, so an apply moves 12 doubles per row through shared memory instead of
-// re-reading J, M^-1 and index lists per incidence:
-//   A  row owner:  prod[e] = ja_side * v_r, written to the row's slot e of its
-//                  body's ascending incidence list (the CSR K1 builds);
-//   B  body half:  s_b = sum_e prod[e] in ascending row order (the reference
-//                  scatter order, delassus.cpp:108-113), w_b = M_b^-1 s_b;
+// step.  ja is also staged once per step incidence-major: slot e of a body's
+// ascending incidence list (the CSR K1 builds) holds that row side's 6 values.
+// An apply is then three shared-memory passes:
+//   A  row owner:  v_r -> both incidence slots of row r;
+//   B  body half:  s_b = sum_e ja_e^T v_{r(e)} in ascending row order (the
+//                  reference scatter order, delassus.cpp:108-113),
+//                  w_b = M_b^-1 s_b;
 //   C  row owner:  out_r = diag_add v_r + ja_a . w_a + ja_b . w_b.
 // ja . (M^-1 s) is the reference's jma . s (jma = fold_inverse_mass(ja),
 // delassus.cpp:12-17, M^-1 symmetric) with the product re-associated.
@@ -454,60 +455,68 @@ struct RegRows {
   int ba[RPT], bb[RPT];  // bodies (or -1)
 };
 
-template <int NT, int RPT>
+// phase clock of thread 0 (KD_CR_PROF=1 diagnostics build of the launch)
+template <bool PROF>
+__device__ __forceinline__ void pstamp(long long* acc, int k, long long& t) {
+  if (PROF && threadIdx.x == 0) {
+    const long long c = clock64();
+    acc[k] += c - t;
+    t = c;
+  }
+}
+
+template <int NT, int RPT, bool PROF>
 __device__ __forceinline__ void apply_reg(const RegRows<NT, RPT>& R, int n, int nb, const double (&v)[RPT],
-                                          double (&out)[RPT], double* prod, double* wv, const double* binv,
-                                          const int32_t* cptr) {
+                                          double (&out)[RPT], double* vsh, const double* jinc, double* wv, const double* binv, const int32_t* pseg,
+                                          long long* acc, long long& tclk) {
   const int tid = threadIdx.x;
-  // A: per-incidence products ja^T v_r
+  pstamp<PROF>(acc, 5, tclk);
+  // A: publish v_r into both of the row's incidence slots
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    if (tid + k * NT < n) {
-      if (R.ea[k] >= 0) {
-        double2* d = reinterpret_cast<double2*>(prod + 6 * R.ea[k]);
-        d[0] = make_double2(R.ja[k][0] * v[k], R.ja[k][1] * v[k]);
-        d[1] = make_double2(R.ja[k][2] * v[k], R.ja[k][3] * v[k]);
-        d[2] = make_double2(R.ja[k][4] * v[k], R.ja[k][5] * v[k]);
-      }
-      if (R.eb[k] >= 0) {
-        double2* d = reinterpret_cast<double2*>(prod + 6 * R.eb[k]);
-        d[0] = make_double2(R.ja[k][6] * v[k], R.ja[k][7] * v[k]);
-        d[1] = make_double2(R.ja[k][8] * v[k], R.ja[k][9] * v[k]);
-        d[2] = make_double2(R.ja[k][10] * v[k], R.ja[k][11] * v[k]);
-      }
-    }
+    if (R.ea[k] >= 0) vsh[R.ea[k]] = v[k];
+    if (R.eb[k] >= 0) vsh[R.eb[k]] = v[k];
   }
   __syncthreads();
-  // B: body halves (linear / angular), ascending incidences, then M^-1
+  pstamp<PROF>(acc, 0, tclk);
+  // B: body halves (linear / angular): s_b = sum over the body's incidences in
+  // ascending row order of ja^T v_r (ja staged incidence-major), then M^-1.
+  // Body segments start at residues of 8 (kBodyRes) that keep the lanes of a
+  // warp on distinct shared-memory banks while they walk their lists in step;
+  // both halves run the same instructions (half h reads the 16-byte pair at
+  // +4h and the single word at +2+h).
   for (int u = tid; u < 2 * nb; u += NT) {
-    const int b = u >> 1;
-    const int e0 = cptr[b], e1 = cptr[b + 1];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    if ((u & 1) == 0) {
-      for (int e = e0; e < e1; ++e) {
-        const double2 a = *reinterpret_cast<const double2*>(prod + 6 * e);
-        s0 += a.x;
-        s1 += a.y;
-        s2 += prod[6 * e + 2];
-      }
-      const double im = binv[10 * b];
-      wv[6 * b] = im * s0;
-      wv[6 * b + 1] = im * s1;
-      wv[6 * b + 2] = im * s2;
+    const int b = u >> 1, h = u & 1;
+    const int2 se = *reinterpret_cast<const int2*>(pseg + 2 * b);
+    double sp = 0.0, sq = 0.0, sc = 0.0;  // pair .x, pair .y, single
+    const double* pr = jinc + 4 * h;
+    const double* pc = jinc + 2 + h;
+#pragma unroll 4
+    for (int e = se.x; e < se.y; ++e) {
+      const double vr = vsh[e];
+      const double2 a = *reinterpret_cast<const double2*>(pr + 6 * e);
+      const double c = pc[6 * e];
+      sp += a.x * vr;
+      sq += a.y * vr;
+      sc += c * vr;
+    }
+    // s = (s0, s1, s2) of this half: linear (sp, sq, sc), angular (sc, sp, sq)
+    const double s0 = h ? sc : sp, s1 = h ? sp : sq, s2 = h ? sq : sc;
+    const double* I = binv + 10 * b + 1;
+    const double im = binv[10 * b];
+    double* wo = wv + 6 * b + 3 * h;
+    if (h == 0) {
+      wo[0] = im * s0;
+      wo[1] = im * s1;
+      wo[2] = im * s2;
     } else {
-      for (int e = e0; e < e1; ++e) {
-        const double2 a = *reinterpret_cast<const double2*>(prod + 6 * e + 4);
-        s0 += prod[6 * e + 3];
-        s1 += a.x;
-        s2 += a.y;
-      }
-      const double* I = binv + 10 * b + 1;
-      wv[6 * b + 3] = (I[0] * s0 + I[1] * s1) + I[2] * s2;
-      wv[6 * b + 4] = (I[3] * s0 + I[4] * s1) + I[5] * s2;
-      wv[6 * b + 5] = (I[6] * s0 + I[7] * s1) + I[8] * s2;
+      wo[0] = (I[0] * s0 + I[1] * s1) + I[2] * s2;
+      wo[1] = (I[3] * s0 + I[4] * s1) + I[5] * s2;
+      wo[2] = (I[6] * s0 + I[7] * s1) + I[8] * s2;
     }
   }
   __syncthreads();
+  pstamp<PROF>(acc, 1, tclk);
   // C: gather
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
@@ -526,17 +535,23 @@ __device__ __forceinline__ void apply_reg(const RegRows<NT, RPT>& R, int n, int 
     }
     out[k] = s;
   }
+  pstamp<PROF>(acc, 2, tclk);
 }
 
 }  // namespace
 
 // shared memory (doubles) of cr_reg_kernel for n rows / nb bodies:
-// 6 n vectors | prod 12 n | w 6 nb | binv 10 nb | red | int: cptr nb+1, slot 2n
+// 6 n vectors | jinc 6 S | vinc S | w 6 nb | binv 10 nb | red | int: cptr nb+1,
+// pseg 2 nb, slot 2n  (S = 2n + 7 nb + 8 incidence slots)
 static size_t cr_reg_smem_bytes(int n, int nb, int nt) {
-  return 8 * ((size_t)18 * n + 16 * (size_t)nb + 2 * 3 * (nt / 32) + 8) + 4 * ((size_t)nb + 1 + 2 * n) + 16;
+  return 8 * ((size_t)20 * n + 65 * (size_t)nb + 64 + 2 * 3 * (nt / 32) + 8) + 4 * ((size_t)3 * nb + 2 + 2 * n) + 16;
 }
+// start residue (mod 8 incidences of 48 B) of body b's segment, by b mod 8:
+// 16-byte slots {3r, 3r+2} mod 8 are distinct within each group of four
+// bodies and the 8-byte slots 6r mod 16 within each group of eight
+__constant__ int kBodyRes[8] = {0, 3, 4, 7, 6, 1, 2, 5};
 
-template <int NT, int RPT, int MINB>
+template <int NT, int RPT, int MINB, bool PROF>
 __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
   extern __shared__ __align__(16) double smem[];
   const int w = bin_worlds[blockIdx.x];
@@ -554,12 +569,15 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
   double* zh = yh + n;
   double* vf = zh + n;
   double* xs = vf + n;
-  double* prod = xs + n;           // 6 per incidence (<= 2n incidences)
-  double* wv = prod + 12 * n;      // 6 nb
+  const int nslot = (2 * n + 7 * nb + 9) & ~1;  // <= 2n incidences + residue padding (even: keeps w 16-byte aligned)
+  double* jinc = xs + n;           // P-scaled J block of every incidence slot (6 doubles)
+  double* vinc = jinc + 6 * nslot; // apply input v_r at both incidence slots of row r
+  double* wv = vinc + nslot;       // 6 nb
   double* binv = wv + 6 * nb;      // 10 nb
   double* red = binv + 10 * nb;    // 2 buffers x 3 x NW
   int32_t* cptr = reinterpret_cast<int32_t*>(red + 2 * 3 * (NT / 32));
-  int32_t* slot = cptr + nb + 1;   // code (2 r + side) -> incidence index
+  int32_t* pseg = cptr + ((nb + 2) & ~1);  // padded [begin, end) of every body's segment (8-byte aligned)
+  int32_t* slot = pseg + 2 * nb;   // code (2 r + side) -> padded incidence slot
 
   const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
   const double inv_rho = 1.0 / rho;
@@ -573,8 +591,20 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
     for (int k = 0; k < 9; ++k) binv[10 * b + 1 + k] = B.Iwinv[k];
   }
   __syncthreads();
-  const int ninc = cptr[nb];
-  for (int e = tid; e < ninc; e += NT) slot[cl_g[e]] = e;
+  if (tid == 0) {
+    int p = 0;
+    for (int b = 0; b < nb; ++b) {
+      p += (kBodyRes[b & 7] - p) & 7;
+      pseg[2 * b] = p;
+      p += cptr[b + 1] - cptr[b];
+      pseg[2 * b + 1] = p;
+    }
+  }
+  __syncthreads();
+  for (int b = tid; b < nb; b += NT) {
+    const int c0 = cptr[b], c1 = cptr[b + 1], p0 = pseg[2 * b];
+    for (int e = c0; e < c1; ++e) slot[cl_g[e]] = p0 + (e - c0);
+  }
   RegRows<NT, RPT> R;
   double x[RPT];
 #pragma unroll
@@ -600,12 +630,18 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
     }
   }
   __syncthreads();  // slot
+  // stage ja incidence-major (read-only for the step) and slot -> row
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     const int r = tid + k * NT;
     R.ea[k] = (r < n && R.ba[k] >= 0) ? slot[2 * r] : -1;
     R.eb[k] = (r < n && R.bb[k] >= 0) ? slot[2 * r + 1] : -1;
+    if (R.ea[k] >= 0)
+      for (int i = 0; i < 6; ++i) jinc[6 * R.ea[k] + i] = R.ja[k][i];
+    if (R.eb[k] >= 0)
+      for (int i = 0; i < 6; ++i) jinc[6 * R.eb[k] + i] = R.ja[k][6 + i];
   }
+  __syncthreads();
   const int n_jd = n - ws.n_limits - 3 * ws.n_contacts;
   const int first_contact = n_jd + ws.n_limits;
   const int n_units = first_contact + ws.n_contacts;
@@ -639,6 +675,9 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
   long long cr_total = 0;
   bool cr_break = false;
   const int hcap = bv.hist_cap;
+  long long acc[6] = {0, 0, 0, 0, 0, 0};
+  long long tclk = PROF ? clock64() : 0;
+  const long long t_start = tclk;
   for (it = 1; it <= sp.max_iters; ++it) {
     // rhs = -(v_f + s - eta x - rho y_hat - z_hat)   (padmm.cpp:116-117)
     double rhs[RPT], rr[RPT], pp[RPT], ap[RPT], ar[RPT];
@@ -654,10 +693,10 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
       }
     }
     // ---- cr_solve(op, rhs, x, budget)   (delassus.cpp:156-187)
-    apply_reg<NT, RPT>(R, n, nb, x, ar, prod, wv, binv, cptr);
+    apply_reg<NT, RPT, PROF>(R, n, nb, x, ar, vinc, jinc, wv, binv, pseg, acc, tclk);
 #pragma unroll
     for (int k = 0; k < RPT; ++k) rr[k] = rhs[k] - ar[k];
-    apply_reg<NT, RPT>(R, n, nb, rr, ar, prod, wv, binv, cptr);
+    apply_reg<NT, RPT, PROF>(R, n, nb, rr, ar, vinc, jinc, wv, binv, pseg, acc, tclk);
     double d3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
@@ -667,7 +706,9 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
       d3[1] += rhs[k] * rhs[k];
       d3[2] += ar[k] * ar[k];
     }
+    pstamp<PROF>(acc, 5, tclk);
     bsum<NT, 3>(d3, red, par);
+    pstamp<PROF>(acc, 3, tclk);
     double rar = d3[0];
     const double rhs2 = d3[1];
     double apap = d3[2];
@@ -679,7 +720,9 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
         double a1[1] = {0.0};
 #pragma unroll
         for (int k = 0; k < RPT; ++k) a1[0] += ap[k] * ap[k];
+        pstamp<PROF>(acc, 5, tclk);
         bsum<NT, 1>(a1, red, par);
+        pstamp<PROF>(acc, 3, tclk);
         apap = a1[0];
       }
       if (!(rar > beps) || !(apap > beps)) {
@@ -692,11 +735,13 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
         x[k] += alpha * pp[k];
         rr[k] -= alpha * ap[k];
       }
-      apply_reg<NT, RPT>(R, n, nb, rr, ar, prod, wv, binv, cptr);
+      apply_reg<NT, RPT, PROF>(R, n, nb, rr, ar, vinc, jinc, wv, binv, pseg, acc, tclk);
       double a1[1] = {0.0};
 #pragma unroll
       for (int k = 0; k < RPT; ++k) a1[0] += rr[k] * ar[k];
+      pstamp<PROF>(acc, 5, tclk);
       bsum<NT, 1>(a1, red, par);
+      pstamp<PROF>(acc, 3, tclk);
       const double beta = fast_div(a1[0], rar);
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
@@ -742,7 +787,9 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
       }
       if (u >= n_jd) rc = fmax(rc, fmin(ymax, zmax));
     }
+    pstamp<PROF>(acc, 5, tclk);
     bmax3<NT>(rp, dmax, rc, red, par);
+    pstamp<PROF>(acc, 4, tclk);
     r_p = rp;
     r_d = rho * dmax;
     r_c = rc;
@@ -794,6 +841,12 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
     ws.cr_iterations = cr_total;
     ws.cr_breakdown = cr_break ? 1 : 0;
     for (int i = done; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
+    if (PROF) {
+      // [0] publish v + barrier, [1] body sums + barrier, [2] gather, [3] CR
+      // reductions, [4] PADMM residual reduction, [5] the rest, [6] total
+      for (int k = 0; k < 6; ++k) ws.phase_cycles[k] = acc[k];
+      ws.phase_cycles[6] = clock64() - t_start;
+    }
   }
 }
 
@@ -818,19 +871,28 @@ static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const 
   return cudaGetLastError();
 }
 
-template <int NT, int RPT, int MINB>
-static cudaError_t launch_cr_reg_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
+template <int NT, int RPT, int MINB, bool PROF>
+static cudaError_t launch_cr_reg_p(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
                                    int ncap, int nbcap, cudaStream_t s) {
   const size_t smem = cr_reg_smem_bytes(std::min(ncap, RPT * NT), nbcap, NT);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     const cudaError_t e =
-        cudaFuncSetAttribute(cr_reg_kernel<NT, RPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(cr_reg_kernel<NT, RPT, MINB, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  cr_reg_kernel<NT, RPT, MINB><<<count, NT, smem, s>>>(bv, sp, worlds);
+  cr_reg_kernel<NT, RPT, MINB, PROF><<<count, NT, smem, s>>>(bv, sp, worlds);
   return cudaGetLastError();
+}
+
+static int cr_reg_mode();
+
+template <int NT, int RPT, int MINB>
+static cudaError_t launch_cr_reg_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
+                                   int ncap, int nbcap, cudaStream_t s) {
+  if (cr_reg_mode() == 2) return launch_cr_reg_p<NT, RPT, MINB, true>(bv, sp, worlds, count, ncap, nbcap, s);
+  return launch_cr_reg_p<NT, RPT, MINB, false>(bv, sp, worlds, count, ncap, nbcap, s);
 }
 
 static int cr_reg_mode() {
