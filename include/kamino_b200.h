@@ -292,6 +292,18 @@ int kd_batch_get_phase_cycles(kd_batch* batch, int64_t* out);
 #define KD_KERNEL_SUPERNODAL_DENSE 4 /* supernodal factor handed to the dense kernel's L^{-1} + solves */
 int kd_batch_get_kernels(kd_batch* batch, int32_t* out);
 
+/* Per world, which matrix-free kernel solved the last step (diagnostics; the
+ * three compute the same cr_solve / MatrixFreeDelassus::apply, delassus.cpp:
+ * 106-187): KD_CR_PATH_NONE (not on the matrix-free backend),
+ * KD_CR_PATH_INCIDENCE (incidence-owner lanes keep P J in registers),
+ * KD_CR_PATH_ROWS (row owners keep P J in registers), KD_CR_PATH_SHARED
+ * (P J staged in shared memory or streamed; worlds above 1024 rows). */
+#define KD_CR_PATH_NONE 0
+#define KD_CR_PATH_INCIDENCE 1
+#define KD_CR_PATH_ROWS 2
+#define KD_CR_PATH_SHARED 3
+int kd_batch_get_cr_paths(kd_batch* batch, int32_t* out);
+
 /* Supernodal sparse-LLT plan of a model (the factorization the device uses for
  * the reference's Dense backend, DenseDelassus delassus.cpp:59-65, on models
  * whose static row-capacity pattern admits one).  stats[0..11] = slots S,

@@ -37,6 +37,7 @@ KD_BACKEND_MATRIX_FREE = 1
 KD_BACKEND_AUTO = 2
 KD_KERNEL_NONE, KD_KERNEL_DENSE, KD_KERNEL_SUPERNODAL, KD_KERNEL_CR, KD_KERNEL_SUPERNODAL_DENSE = 0, 1, 2, 3, 4
 KERNEL_NAMES = {0: 'none', 1: 'dense', 2: 'supernodal', 3: 'cr', 4: 'supernodal+dense'}
+CR_PATH_NAMES = {0: 'none', 1: 'incidence', 2: 'rows', 3: 'shared'}
 
 
 class kd_body_desc(C.Structure):
@@ -213,6 +214,7 @@ KD_ONLY = {
     "batch_get_timing": (C.c_int, [_H, c_double_p, c_int64_p]),
     "version": (C.c_char_p, []),
     "batch_get_phase_cycles": (C.c_int, [_H, c_int64_p]),
+    "batch_get_cr_paths": (C.c_int, [_H, c_int32_p]),
     "batch_step_async": (C.c_int, [_H, C.POINTER(kd_step_config), C.c_int32]),
     "batch_sync": (C.c_int, [_H]),
     "batch_stream": (C.c_int, [_H, C.POINTER(C.c_void_p)]),

@@ -1097,6 +1097,17 @@ int kd_batch_get_kernels(kd_batch* b, int32_t* out) {
   return KD_OK;
 }
 
+int kd_batch_get_cr_paths(kd_batch* b, int32_t* out) {
+  if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  KD_CK(cudaSetDevice(b->device));
+  std::vector<WorldStep> ws(b->n_worlds);
+  if (b->n_worlds)
+    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+  for (int w = 0; w < b->n_worlds; ++w)
+    out[w] = ws[w].backend == BE_MATRIX_FREE ? ws[w].cr_path : KD_CR_PATH_NONE;
+  return KD_OK;
+}
+
 int kd_batch_row_offsets(const kd_batch* b, int64_t* ro, int64_t* total) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
   for (int w = 0; w < b->n_worlds; ++w) ro[w] = b->row_off[w];

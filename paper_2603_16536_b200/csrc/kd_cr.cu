@@ -148,8 +148,9 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
   WorldStep& ws = bv.wstep[w];
   if (ws.backend != BE_MATRIX_FREE) return;
   const int n = ws.n_rows;
-  if (n <= n_reg) return;  // cr_reg_kernel took it
+  if (n <= n_reg) return;  // cr_op_kernel took it
   const int tid = threadIdx.x;
+  if (tid == 0) ws.cr_path = 3;  // KD_CR_PATH_SHARED
   const DevWorld W = bv.worlds[w];
   const int nb = W.nb;
   const int64_t R0 = W.row_off;
@@ -447,15 +448,7 @@ __device__ __forceinline__ void bmax3(double& a, double& b, double& c, double* r
   }
 }
 
-template <int NT, int RPT>
-struct RegRows {
-  double ja[RPT][12];
-  double dadd[RPT];
-  int ea[RPT], eb[RPT];  // incidence slots (or -1)
-  int ba[RPT], bb[RPT];  // bodies (or -1)
-};
-
-// phase clock of thread 0 (KD_CR_PROF=1 diagnostics build of the launch)
+// phase clock of thread 0 (KD_CR_REG=2 diagnostics launch)
 template <bool PROF>
 __device__ __forceinline__ void pstamp(long long* acc, int k, long long& t) {
   if (PROF && threadIdx.x == 0) {
@@ -465,101 +458,361 @@ __device__ __forceinline__ void pstamp(long long* acc, int k, long long& t) {
   }
 }
 
-template <int NT, int RPT, bool PROF>
-__device__ __forceinline__ void apply_reg(const RegRows<NT, RPT>& R, int n, int nb, const double (&v)[RPT],
-                                          double (&out)[RPT], double* vsh, const double* jinc, double* wv, const double* binv, const int32_t* pseg,
-                                          long long* acc, long long& tclk) {
-  const int tid = threadIdx.x;
-  pstamp<PROF>(acc, 5, tclk);
-  // A: publish v_r into both of the row's incidence slots
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    if (R.ea[k] >= 0) vsh[R.ea[k]] = v[k];
-    if (R.eb[k] >= 0) vsh[R.eb[k]] = v[k];
-  }
-  __syncthreads();
-  pstamp<PROF>(acc, 0, tclk);
-  // B: body halves (linear / angular): s_b = sum over the body's incidences in
-  // ascending row order of ja^T v_r (ja staged incidence-major), then M^-1.
-  // Body segments start at residues of 8 (kBodyRes) that keep the lanes of a
-  // warp on distinct shared-memory banks while they walk their lists in step;
-  // both halves run the same instructions (half h reads the 16-byte pair at
-  // +4h and the single word at +2+h).
-  for (int u = tid; u < 2 * nb; u += NT) {
-    const int b = u >> 1, h = u & 1;
-    const int2 se = *reinterpret_cast<const int2*>(pseg + 2 * b);
-    double sp = 0.0, sq = 0.0, sc = 0.0;  // pair .x, pair .y, single
-    const double* pr = jinc + 4 * h;
-    const double* pc = jinc + 2 + h;
-#pragma unroll 4
-    for (int e = se.x; e < se.y; ++e) {
-      const double vr = vsh[e];
-      const double2 a = *reinterpret_cast<const double2*>(pr + 6 * e);
-      const double c = pc[6 * e];
-      sp += a.x * vr;
-      sq += a.y * vr;
-      sc += c * vr;
-    }
-    // s = (s0, s1, s2) of this half: linear (sp, sq, sc), angular (sc, sp, sq)
-    const double s0 = h ? sc : sp, s1 = h ? sp : sq, s2 = h ? sq : sc;
-    const double* I = binv + 10 * b + 1;
-    const double im = binv[10 * b];
-    double* wo = wv + 6 * b + 3 * h;
-    if (h == 0) {
-      wo[0] = im * s0;
-      wo[1] = im * s1;
-      wo[2] = im * s2;
-    } else {
-      wo[0] = (I[0] * s0 + I[1] * s1) + I[2] * s2;
-      wo[1] = (I[3] * s0 + I[4] * s1) + I[5] * s2;
-      wo[2] = (I[6] * s0 + I[7] * s1) + I[8] * s2;
-    }
-  }
-  __syncthreads();
-  pstamp<PROF>(acc, 1, tclk);
-  // C: gather
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    double s = R.dadd[k] * v[k];
-    if (R.ba[k] >= 0) {
-      const double2* w = reinterpret_cast<const double2*>(wv + 6 * R.ba[k]);
-      const double2 w0 = w[0], w1 = w[1], w2 = w[2];
-      s += ((R.ja[k][0] * w0.x + R.ja[k][1] * w0.y) + (R.ja[k][2] * w1.x + R.ja[k][3] * w1.y)) +
-           (R.ja[k][4] * w2.x + R.ja[k][5] * w2.y);
-    }
-    if (R.bb[k] >= 0) {
-      const double2* w = reinterpret_cast<const double2*>(wv + 6 * R.bb[k]);
-      const double2 w0 = w[0], w1 = w[1], w2 = w[2];
-      s += ((R.ja[k][6] * w0.x + R.ja[k][7] * w0.y) + (R.ja[k][8] * w1.x + R.ja[k][9] * w1.y)) +
-           (R.ja[k][10] * w2.x + R.ja[k][11] * w2.y);
-    }
-    out[k] = s;
-  }
-  pstamp<PROF>(acc, 2, tclk);
-}
-
-}  // namespace
-
-// shared memory (doubles) of cr_reg_kernel for n rows / nb bodies:
-// 6 n vectors | jinc 6 S | vinc S | w 6 nb | binv 10 nb | red | int: cptr nb+1,
-// pseg 2 nb, slot 2n  (S = 2n + 7 nb + 8 incidence slots)
-static size_t cr_reg_smem_bytes(int n, int nb, int nt) {
-  return 8 * ((size_t)20 * n + 65 * (size_t)nb + 64 + 2 * 3 * (nt / 32) + 8) + 4 * ((size_t)3 * nb + 2 + 2 * n) + 16;
-}
 // start residue (mod 8 incidences of 48 B) of body b's segment, by b mod 8:
 // 16-byte slots {3r, 3r+2} mod 8 are distinct within each group of four
 // bodies and the 8-byte slots 6r mod 16 within each group of eight
 __constant__ int kBodyRes[8] = {0, 3, 4, 7, 6, 1, 2, 5};
 
-template <int NT, int RPT, int MINB, bool PROF>
-__global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
+// ---- operator 1: rows own P J in registers; J also staged incidence-major
+template <int NT, int RPT, bool PROF>
+struct RegOp {
+  double ja[RPT][12];
+  double dadd[RPT];
+  int ea[RPT], eb[RPT];  // incidence slots (or -1)
+  int ba[RPT], bb[RPT];  // bodies (or -1)
+  double *jinc, *vinc, *wv;
+  const double* binv;
+  const int32_t* pseg;
+
+  // op shared memory: jinc 6 S | vinc S | w 6 nb | binv 10 nb | int: cptr nb+1,
+  // pseg 2 nb, slot 2n  (S = 2n + 7 nb + 8 incidence slots, rounded even)
+  static size_t smem_bytes(int n, int nb) {
+    return 8 * ((size_t)14 * n + 65 * (size_t)nb + 64) + 4 * ((size_t)3 * nb + 2 + 2 * n) + 16;
+  }
+
+  __device__ bool setup(const BatchView& bv, const DevWorld& W, int w, int n, int nb, double eta_rho, double* dsm) {
+    const int tid = threadIdx.x;
+    const int64_t R0 = W.row_off;
+    const int nslot = (2 * n + 7 * nb + 9) & ~1;  // even: keeps w 16-byte aligned
+    jinc = dsm;
+    vinc = jinc + 6 * nslot;
+    wv = vinc + nslot;
+    double* binv_w = wv + 6 * nb;
+    binv = binv_w;
+    int32_t* cptr = reinterpret_cast<int32_t*>(binv_w + 10 * nb);
+    int32_t* pseg_w = cptr + ((nb + 2) & ~1);
+    pseg = pseg_w;
+    int32_t* slot = pseg_w + 2 * nb;
+    const int32_t* cptr_g = bv.csr_ptr + W.body_off + w;
+    const int32_t* cl_g = bv.csr + 2 * R0;
+    for (int b = tid; b <= nb; b += NT) cptr[b] = cptr_g[b];
+    for (int b = tid; b < nb; b += NT) {
+      const BodyS& B = bv.bs[W.body_off + b];
+      binv_w[10 * b] = B.inv_mass;
+      for (int k = 0; k < 9; ++k) binv_w[10 * b + 1 + k] = B.Iwinv[k];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int p = 0;
+      for (int b = 0; b < nb; ++b) {
+        p += (kBodyRes[b & 7] - p) & 7;
+        pseg_w[2 * b] = p;
+        p += cptr[b + 1] - cptr[b];
+        pseg_w[2 * b + 1] = p;
+      }
+    }
+    __syncthreads();
+    for (int b = tid; b < nb; b += NT) {
+      const int c0 = cptr[b], c1 = cptr[b + 1], p0 = pseg_w[2 * b];
+      for (int e = c0; e < c1; ++e) slot[cl_g[e]] = p0 + (e - c0);
+    }
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * NT;
+      dadd[k] = 0.0;
+      ba[k] = bb[k] = -1;
+#pragma unroll
+      for (int i = 0; i < 12; ++i) ja[k][i] = 0.0;
+      if (r < n) {
+        const double p = bv.scale[R0 + r];
+        dadd[k] = p * p * bv.reg[R0 + r] + eta_rho;
+        const double* J = bv.rowj[R0 + r].J;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) ja[k][i] = p * J[i];  // bake_jacobian: ja = P J
+        ba[k] = bv.rbody[2 * (R0 + r)];
+        bb[k] = bv.rbody[2 * (R0 + r) + 1];
+      }
+    }
+    __syncthreads();  // slot
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * NT;
+      ea[k] = (r < n && ba[k] >= 0) ? slot[2 * r] : -1;
+      eb[k] = (r < n && bb[k] >= 0) ? slot[2 * r + 1] : -1;
+      if (ea[k] >= 0)
+        for (int i = 0; i < 6; ++i) jinc[6 * ea[k] + i] = ja[k][i];
+      if (eb[k] >= 0)
+        for (int i = 0; i < 6; ++i) jinc[6 * eb[k] + i] = ja[k][6 + i];
+    }
+    return true;
+  }
+
+  __device__ __forceinline__ void apply(int n, int nb, const double (&v)[RPT], double (&out)[RPT], long long* acc,
+                                        long long& tclk) const {
+    const int tid = threadIdx.x;
+    pstamp<PROF>(acc, 5, tclk);
+    // A: publish v_r into both of the row's incidence slots
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      if (ea[k] >= 0) vinc[ea[k]] = v[k];
+      if (eb[k] >= 0) vinc[eb[k]] = v[k];
+    }
+    __syncthreads();
+    pstamp<PROF>(acc, 0, tclk);
+    // B: body halves (linear / angular): s_b = sum over the body's incidences in
+    // ascending row order of ja^T v_r, then M^-1.  Body segments start at
+    // residues of 8 (kBodyRes) that keep the lanes of a warp on distinct banks
+    // while they walk their lists in step; both halves run the same
+    // instructions (half h reads the 16-byte pair at +4h and the word at +2+h).
+    for (int u = tid; u < 2 * nb; u += NT) {
+      const int b = u >> 1, h = u & 1;
+      const int2 se = *reinterpret_cast<const int2*>(pseg + 2 * b);
+      double sp = 0.0, sq = 0.0, sc = 0.0;  // pair .x, pair .y, single
+      const double* pr = jinc + 4 * h;
+      const double* pc = jinc + 2 + h;
+#pragma unroll 4
+      for (int e = se.x; e < se.y; ++e) {
+        const double vr = vinc[e];
+        const double2 a = *reinterpret_cast<const double2*>(pr + 6 * e);
+        const double c = pc[6 * e];
+        sp += a.x * vr;
+        sq += a.y * vr;
+        sc += c * vr;
+      }
+      // s = (s0, s1, s2) of this half: linear (sp, sq, sc), angular (sc, sp, sq)
+      const double s0 = h ? sc : sp, s1 = h ? sp : sq, s2 = h ? sq : sc;
+      const double* I = binv + 10 * b + 1;
+      const double im = binv[10 * b];
+      double* wo = wv + 6 * b + 3 * h;
+      if (h == 0) {
+        wo[0] = im * s0;
+        wo[1] = im * s1;
+        wo[2] = im * s2;
+      } else {
+        wo[0] = (I[0] * s0 + I[1] * s1) + I[2] * s2;
+        wo[1] = (I[3] * s0 + I[4] * s1) + I[5] * s2;
+        wo[2] = (I[6] * s0 + I[7] * s1) + I[8] * s2;
+      }
+    }
+    __syncthreads();
+    pstamp<PROF>(acc, 1, tclk);
+    // C: gather
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      double s = dadd[k] * v[k];
+      if (ba[k] >= 0) {
+        const double2* wp = reinterpret_cast<const double2*>(wv + 6 * ba[k]);
+        const double2 w0 = wp[0], w1 = wp[1], w2 = wp[2];
+        s += ((ja[k][0] * w0.x + ja[k][1] * w0.y) + (ja[k][2] * w1.x + ja[k][3] * w1.y)) +
+             (ja[k][4] * w2.x + ja[k][5] * w2.y);
+      }
+      if (bb[k] >= 0) {
+        const double2* wp = reinterpret_cast<const double2*>(wv + 6 * bb[k]);
+        const double2 w0 = wp[0], w1 = wp[1], w2 = wp[2];
+        s += ((ja[k][6] * w0.x + ja[k][7] * w0.y) + (ja[k][8] * w1.x + ja[k][9] * w1.y)) +
+             (ja[k][10] * w2.x + ja[k][11] * w2.y);
+      }
+      out[k] = s;
+    }
+    pstamp<PROF>(acc, 2, tclk);
+  }
+};
+
+// ---- operator 2: incidence owners.  Lanes own contiguous pieces (<= P
+// incidences) of one body's ascending incidence list and keep those
+// incidences' P J blocks in registers; a body's pieces sit on consecutive
+// lanes of one warp.  Rows only keep diag_add and their two slots.
+//   A  row owner:   v_r -> both incidence slots of row r;
+//   B  piece lane:  partial s = sum ja_e^T v over the piece (ascending), then a
+//                   fixed tree over the body's lanes (shuffles) and w = M^-1 s;
+//   C  piece lane:  q_e = ja_e . w_b per incidence -> slot e;
+//      row owner:   out_r = diag_add v_r + q_a + q_b.
+// Worlds whose bodies do not fit NT lanes (a body needs ceil(deg / P) lanes
+// within one warp) are left to RegOp.
+template <int NT, int RPT, int P, bool PROF>
+struct IncOp {
+  double dadd[RPT];
+  int ea[RPT], eb[RPT];
+  double jp[P][6];
+  int e0, cnt, mb, g0, gq;
+  double *vinc, *qinc;
+  const double* binv;
+
+  // op shared memory: vinc 2n | qinc 2n | binv 10 nb | int: cptr nb+1, slot 2n, lanes 4 NT, flag
+  static size_t smem_bytes(int n, int nb) {
+    return 8 * ((size_t)4 * n + 10 * (size_t)nb + 2) + 4 * ((size_t)nb + 2 + 2 * n + 4 * NT + 2) + 16;
+  }
+
+  __device__ bool setup(const BatchView& bv, const DevWorld& W, int w, int n, int nb, double eta_rho, double* dsm) {
+    const int tid = threadIdx.x;
+    const int64_t R0 = W.row_off;
+    vinc = dsm;
+    qinc = vinc + 2 * n;
+    double* binv_w = qinc + 2 * n;
+    binv = binv_w;
+    int32_t* cptr = reinterpret_cast<int32_t*>(binv_w + 10 * nb);
+    int32_t* slot = cptr + nb + 1;
+    int32_t* lanes = slot + 2 * n;  // per lane: body, e0, cnt, g0 | gq << 16
+    int32_t* okf = lanes + 4 * NT;
+    const int32_t* cptr_g = bv.csr_ptr + W.body_off + w;
+    const int32_t* cl_g = bv.csr + 2 * R0;
+    for (int b = tid; b <= nb; b += NT) cptr[b] = cptr_g[b];
+    for (int b = tid; b < nb; b += NT) {
+      const BodyS& B = bv.bs[W.body_off + b];
+      binv_w[10 * b] = B.inv_mass;
+      for (int k = 0; k < 9; ++k) binv_w[10 * b + 1 + k] = B.Iwinv[k];
+    }
+    lanes[4 * tid] = -1;
+    lanes[4 * tid + 1] = 0;
+    lanes[4 * tid + 2] = 0;
+    lanes[4 * tid + 3] = tid | (1 << 16);
+    __syncthreads();
+    if (tid == 0) {
+      int L = 0, ok = 1;
+      for (int b = 0; b < nb && ok; ++b) {
+        const int c0 = cptr[b], d = cptr[b + 1] - c0;
+        if (d == 0) continue;
+        const int q = (d + P - 1) / P;
+        if (q > 32) {
+          ok = 0;
+          break;
+        }
+        if ((L & 31) + q > 32) L = (L + 31) & ~31;  // a body's lanes stay in one warp
+        if (L + q > NT) {
+          ok = 0;
+          break;
+        }
+        const int pl = (d + q - 1) / q;
+        for (int j = 0; j < q; ++j) {
+          lanes[4 * (L + j)] = b;
+          lanes[4 * (L + j) + 1] = c0 + j * pl;
+          lanes[4 * (L + j) + 2] = max(0, min(pl, d - j * pl));
+          lanes[4 * (L + j) + 3] = L | (q << 16);
+        }
+        L += q;
+      }
+      *okf = ok;
+    }
+    for (int e = tid; e < 2 * n; e += NT) slot[e] = -1;
+    __syncthreads();
+    if (!*okf) return false;
+    const int ninc = cptr[nb];
+    for (int e = tid; e < ninc; e += NT) slot[cl_g[e]] = e;
+    mb = lanes[4 * tid];
+    e0 = lanes[4 * tid + 1];
+    cnt = lanes[4 * tid + 2];
+    g0 = lanes[4 * tid + 3] & 0xffff;
+    gq = lanes[4 * tid + 3] >> 16;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) jp[j][k] = 0.0;
+      if (j < cnt) {
+        const int code = cl_g[e0 + j];
+        const int r = code >> 1;
+        const double p = bv.scale[R0 + r];
+        const double* J = bv.rowj[R0 + r].J + 6 * (code & 1);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) jp[j][k] = p * J[k];  // bake_jacobian: ja = P J
+      }
+    }
+    __syncthreads();  // slot
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * NT;
+      dadd[k] = 0.0;
+      ea[k] = eb[k] = -1;
+      if (r < n) {
+        const double p = bv.scale[R0 + r];
+        dadd[k] = p * p * bv.reg[R0 + r] + eta_rho;
+        if (bv.rbody[2 * (R0 + r)] >= 0) ea[k] = slot[2 * r];
+        if (bv.rbody[2 * (R0 + r) + 1] >= 0) eb[k] = slot[2 * r + 1];
+      }
+    }
+    return true;
+  }
+
+  __device__ __forceinline__ void apply(int n, int nb, const double (&v)[RPT], double (&out)[RPT], long long* acc,
+                                        long long& tclk) const {
+    pstamp<PROF>(acc, 5, tclk);
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      if (ea[k] >= 0) vinc[ea[k]] = v[k];
+      if (eb[k] >= 0) vinc[eb[k]] = v[k];
+    }
+    __syncthreads();
+    pstamp<PROF>(acc, 0, tclk);
+    double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      if (j < cnt) {
+        const double vv = vinc[e0 + j];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s[k] += jp[j][k] * vv;
+      }
+    }
+    // fixed tree over the body's lanes toward its first lane, then broadcast
+    const int lane = threadIdx.x & 31, gl = g0 & 31, qi = lane - gl;
+    const int qmax = __reduce_max_sync(0xffffffffu, gq);
+    for (int o = 1; o < qmax; o <<= 1) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const double t = __shfl_down_sync(0xffffffffu, s[k], o);
+        if ((qi & (2 * o - 1)) == 0 && qi + o < gq) s[k] += t;
+      }
+    }
+    if (qmax > 1) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s[k] = __shfl_sync(0xffffffffu, s[k], gl);
+    }
+    double wv[6];
+    if (mb >= 0) {
+      const double* bi = binv + 10 * mb;
+      const double im = bi[0];
+      const double* I = bi + 1;
+      wv[0] = im * s[0];
+      wv[1] = im * s[1];
+      wv[2] = im * s[2];
+      wv[3] = (I[0] * s[3] + I[1] * s[4]) + I[2] * s[5];
+      wv[4] = (I[3] * s[3] + I[4] * s[4]) + I[5] * s[5];
+      wv[5] = (I[6] * s[3] + I[7] * s[4]) + I[8] * s[5];
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+      if (j < cnt)
+        qinc[e0 + j] = ((jp[j][0] * wv[0] + jp[j][1] * wv[1]) + (jp[j][2] * wv[2] + jp[j][3] * wv[3])) +
+                       (jp[j][4] * wv[4] + jp[j][5] * wv[5]);
+    __syncthreads();
+    pstamp<PROF>(acc, 1, tclk);
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      double t = dadd[k] * v[k];
+      if (ea[k] >= 0) t += qinc[ea[k]];
+      if (eb[k] >= 0) t += qinc[eb[k]];
+      out[k] = t;
+    }
+    pstamp<PROF>(acc, 2, tclk);
+  }
+};
+}  // namespace
+
+// common shared memory of cr_op_kernel: 6 n vectors | 2 x 3 x NW reduction partials
+static size_t cr_common_bytes(int n, int nt) { return 8 * ((size_t)6 * n + 2 * 3 * (nt / 32) + 2); }
+
+template <class Op, int NT, int RPT, int MINB, bool PROF, bool MARK>
+__global__ void __launch_bounds__(NT, MINB) cr_op_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds,
+                                                         int skip_marked) {
   extern __shared__ __align__(16) double smem[];
   const int w = bin_worlds[blockIdx.x];
   WorldStep& ws = bv.wstep[w];
   if (ws.backend != BE_MATRIX_FREE) return;
+  if (skip_marked && ws.cr_path == 1) return;  // the incidence-owner kernel took it
   const int n = ws.n_rows;
-  if (n > RPT * NT) return;  // cr_kernel takes it
   const int tid = threadIdx.x;
+  if (n > RPT * NT) {  // cr_kernel takes it
+    if (MARK && tid == 0) ws.cr_path = 0;
+    return;
+  }
   const DevWorld W = bv.worlds[w];
   const int nb = W.nb;
   const int64_t R0 = W.row_off;
@@ -569,77 +822,26 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
   double* zh = yh + n;
   double* vf = zh + n;
   double* xs = vf + n;
-  const int nslot = (2 * n + 7 * nb + 9) & ~1;  // <= 2n incidences + residue padding (even: keeps w 16-byte aligned)
-  double* jinc = xs + n;           // P-scaled J block of every incidence slot (6 doubles)
-  double* vinc = jinc + 6 * nslot; // apply input v_r at both incidence slots of row r
-  double* wv = vinc + nslot;       // 6 nb
-  double* binv = wv + 6 * nb;      // 10 nb
-  double* red = binv + 10 * nb;    // 2 buffers x 3 x NW
-  int32_t* cptr = reinterpret_cast<int32_t*>(red + 2 * 3 * (NT / 32));
-  int32_t* pseg = cptr + ((nb + 2) & ~1);  // padded [begin, end) of every body's segment (8-byte aligned)
-  int32_t* slot = pseg + 2 * nb;   // code (2 r + side) -> padded incidence slot
-
+  double* red = xs + n;  // 2 buffers x 3 x NW
+  double* opsm = red + ((2 * 3 * (NT / 32) + 1) & ~1);
   const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
   const double inv_rho = 1.0 / rho;
-  const int32_t* cptr_g = bv.csr_ptr + W.body_off + w;
-  const int32_t* cl_g = bv.csr + 2 * R0;
-  for (int b = tid; b <= nb; b += NT) cptr[b] = cptr_g[b];
-  for (int e = tid; e < 2 * n; e += NT) slot[e] = -1;
-  for (int b = tid; b < nb; b += NT) {
-    const BodyS& B = bv.bs[W.body_off + b];
-    binv[10 * b] = B.inv_mass;
-    for (int k = 0; k < 9; ++k) binv[10 * b + 1 + k] = B.Iwinv[k];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int p = 0;
-    for (int b = 0; b < nb; ++b) {
-      p += (kBodyRes[b & 7] - p) & 7;
-      pseg[2 * b] = p;
-      p += cptr[b + 1] - cptr[b];
-      pseg[2 * b + 1] = p;
-    }
-  }
-  __syncthreads();
-  for (int b = tid; b < nb; b += NT) {
-    const int c0 = cptr[b], c1 = cptr[b + 1], p0 = pseg[2 * b];
-    for (int e = c0; e < c1; ++e) slot[cl_g[e]] = p0 + (e - c0);
-  }
-  RegRows<NT, RPT> R;
+  Op op;
+  const bool ok = op.setup(bv, W, w, n, nb, eta_rho, opsm);
+  if (MARK && tid == 0) ws.cr_path = ok ? 1 : 0;  // KD_CR_PATH_INCIDENCE, or left to RegOp
+  if (!ok) return;
+  if (!MARK && tid == 0) ws.cr_path = 2;  // KD_CR_PATH_ROWS
   double x[RPT];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     const int r = tid + k * NT;
     x[k] = 0.0;
-    R.dadd[k] = 0.0;
-    R.ba[k] = R.bb[k] = -1;
-#pragma unroll
-    for (int i = 0; i < 12; ++i) R.ja[k][i] = 0.0;
     if (r < n) {
-      const double p = bv.scale[R0 + r];
-      R.dadd[k] = p * p * bv.reg[R0 + r] + eta_rho;
-      const double* J = bv.rowj[R0 + r].J;
-#pragma unroll
-      for (int i = 0; i < 12; ++i) R.ja[k][i] = p * J[i];  // bake_jacobian: ja = P J
-      R.ba[k] = bv.rbody[2 * (R0 + r)];
-      R.bb[k] = bv.rbody[2 * (R0 + r) + 1];
       x[k] = bv.x0[R0 + r];
       xs[r] = x[k];
       vf[r] = bv.vf[R0 + r];
       zv[r] = bv.z0[R0 + r];
     }
-  }
-  __syncthreads();  // slot
-  // stage ja incidence-major (read-only for the step) and slot -> row
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int r = tid + k * NT;
-    R.ea[k] = (r < n && R.ba[k] >= 0) ? slot[2 * r] : -1;
-    R.eb[k] = (r < n && R.bb[k] >= 0) ? slot[2 * r + 1] : -1;
-    if (R.ea[k] >= 0)
-      for (int i = 0; i < 6; ++i) jinc[6 * R.ea[k] + i] = R.ja[k][i];
-    if (R.eb[k] >= 0)
-      for (int i = 0; i < 6; ++i) jinc[6 * R.eb[k] + i] = R.ja[k][6 + i];
   }
   __syncthreads();
   const int n_jd = n - ws.n_limits - 3 * ws.n_contacts;
@@ -693,10 +895,10 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
       }
     }
     // ---- cr_solve(op, rhs, x, budget)   (delassus.cpp:156-187)
-    apply_reg<NT, RPT, PROF>(R, n, nb, x, ar, vinc, jinc, wv, binv, pseg, acc, tclk);
+    op.apply(n, nb, x, ar, acc, tclk);
 #pragma unroll
     for (int k = 0; k < RPT; ++k) rr[k] = rhs[k] - ar[k];
-    apply_reg<NT, RPT, PROF>(R, n, nb, rr, ar, vinc, jinc, wv, binv, pseg, acc, tclk);
+    op.apply(n, nb, rr, ar, acc, tclk);
     double d3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
@@ -735,7 +937,7 @@ __global__ void __launch_bounds__(NT, MINB) cr_reg_kernel(BatchView bv, StepPara
         x[k] += alpha * pp[k];
         rr[k] -= alpha * ap[k];
       }
-      apply_reg<NT, RPT, PROF>(R, n, nb, rr, ar, vinc, jinc, wv, binv, pseg, acc, tclk);
+      op.apply(n, nb, rr, ar, acc, tclk);
       double a1[1] = {0.0};
 #pragma unroll
       for (int k = 0; k < RPT; ++k) a1[0] += rr[k] * ar[k];
@@ -871,28 +1073,42 @@ static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const 
   return cudaGetLastError();
 }
 
-template <int NT, int RPT, int MINB, bool PROF>
-static cudaError_t launch_cr_reg_p(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
-                                   int ncap, int nbcap, cudaStream_t s) {
-  const size_t smem = cr_reg_smem_bytes(std::min(ncap, RPT * NT), nbcap, NT);
+template <class Op, int NT, int RPT, int MINB, bool PROF, bool MARK>
+static cudaError_t launch_cr_op_p(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
+                                  int ncap, int nbcap, int skip_marked, cudaStream_t s) {
+  const int nc = std::min(ncap, RPT * NT);
+  const size_t smem = cr_common_bytes(nc, NT) + Op::smem_bytes(nc, nbcap);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(cr_reg_kernel<NT, RPT, MINB, PROF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = cudaFuncSetAttribute(cr_op_kernel<Op, NT, RPT, MINB, PROF, MARK>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  cr_reg_kernel<NT, RPT, MINB, PROF><<<count, NT, smem, s>>>(bv, sp, worlds);
+  cr_op_kernel<Op, NT, RPT, MINB, PROF, MARK><<<count, NT, smem, s>>>(bv, sp, worlds, skip_marked);
   return cudaGetLastError();
 }
 
 static int cr_reg_mode();
 
+// KD_CR_REG: 0 = shared-memory kernel only, 1 (default) = incidence-owner then
+// register-row kernels, 2 = the same with phase clocks, 3 = register-row only
 template <int NT, int RPT, int MINB>
 static cudaError_t launch_cr_reg_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
                                    int ncap, int nbcap, cudaStream_t s) {
-  if (cr_reg_mode() == 2) return launch_cr_reg_p<NT, RPT, MINB, true>(bv, sp, worlds, count, ncap, nbcap, s);
-  return launch_cr_reg_p<NT, RPT, MINB, false>(bv, sp, worlds, count, ncap, nbcap, s);
+  const int mode = cr_reg_mode();
+  const bool prof = mode == 2;
+  const bool inc = mode != 3 && cr_common_bytes(std::min(ncap, RPT * NT), NT) +
+                                         IncOp<NT, RPT, 5, false>::smem_bytes(std::min(ncap, RPT * NT), nbcap) <=
+                                     232448 / MINB;
+  cudaError_t e = cudaSuccess;
+  if (inc) {
+    e = prof ? launch_cr_op_p<IncOp<NT, RPT, 5, true>, NT, RPT, MINB, true, true>(bv, sp, worlds, count, ncap, nbcap, 0, s)
+             : launch_cr_op_p<IncOp<NT, RPT, 5, false>, NT, RPT, MINB, false, true>(bv, sp, worlds, count, ncap, nbcap, 0, s);
+    if (e != cudaSuccess) return e;
+  }
+  return prof ? launch_cr_op_p<RegOp<NT, RPT, true>, NT, RPT, MINB, true, false>(bv, sp, worlds, count, ncap, nbcap, inc, s)
+              : launch_cr_op_p<RegOp<NT, RPT, false>, NT, RPT, MINB, false, false>(bv, sp, worlds, count, ncap, nbcap, inc, s);
 }
 
 static int cr_reg_mode() {
@@ -911,7 +1127,7 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
   // shared-memory kernel for the rest (both launched over the bin; each skips
   // the other's worlds)
   int n_reg = 0;
-  if (cr_reg_mode() && cr_reg_smem_bytes(std::min(ncap, 1024), nbcap, 512) <= 232448) {
+  if (cr_reg_mode() && cr_common_bytes(std::min(ncap, 1024), 512) + RegOp<512, 2, false>::smem_bytes(std::min(ncap, 1024), nbcap) <= 232448) {
     cudaError_t e;
     if (ncap <= 256) {
       n_reg = 256;

@@ -185,7 +185,7 @@ struct WorldStep {
   int64_t cr_iterations;
   double r_p, r_d, r_c;
   double f_inf, kkt, bil_vel;
-  int32_t jcache_valid, ccache_count, fail, pad;
+  int32_t jcache_valid, ccache_count, fail, cr_path;  // cr_path: 1 if the incidence-owner CR kernel took the world
   int64_t phase_cycles[8];  // fused-kernel phase stamps (clock64 deltas), diagnostics only
 };
 

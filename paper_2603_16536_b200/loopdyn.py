@@ -387,6 +387,14 @@ class WorldBatch:
         _check(lib().kd_batch_get_kernels(self.handle, _capi.i32ptr(out)))
         return [_capi.KERNEL_NAMES[int(k)] for k in out[: self.n_worlds]]
 
+    def cr_paths(self):
+        """Per world, the matrix-free kernel that solved the last step:
+        'none' | 'incidence' | 'rows' | 'shared' (kd_batch_get_cr_paths)."""
+        self._ensure()
+        out = np.zeros(max(1, self.n_worlds), np.int32)
+        _check(lib().kd_batch_get_cr_paths(self.handle, _capi.i32ptr(out)))
+        return [_capi.CR_PATH_NAMES[int(k)] for k in out[: self.n_worlds]]
+
     def phase_cycles(self):
         """clock64 cycles per fused-kernel phase of the last step, [n_worlds, 8]."""
         self._ensure()

@@ -219,3 +219,66 @@ def test_dense_vs_matrix_free_on_device():
         b = sparse.impulses()[:21]
         worst = max(worst, float(np.abs(a - b).max() / max(1e-9, np.abs(a).max())))
     assert worst <= 1e-6
+
+
+@pytest.mark.parametrize("cells,steps", [(16, 20), (22, 12)])
+def test_cr_kernel_paths_vs_oracle(cells, steps):
+    """Every matrix-free kernel path (incidence owners, row owners; selected by
+    the world's size and body degrees) against the oracle: same row counts and
+    PADMM iterations per step, CR counts within +-2, poses after N steps."""
+    sc = closed_chain(cells)
+    cfg = K.config_for(sc)
+    gb, ob = pair(sc, n_worlds=2, jitter=True)
+    paths = set()
+    for _ in range(steps):
+        gb.step(cfg)
+        ob.step(cfg)
+        paths.update(gb.cr_paths())
+        for dg, do in zip(gb.diagnostics()[:2], ob.diagnostics()[:2]):
+            assert dg.n_rows == do.n_rows > 300
+            assert dg.iterations == do.iterations
+            assert abs(dg.cr_iterations - do.cr_iterations) <= 2
+    assert paths <= {"incidence", "rows"} and paths, paths
+    if cells == 22:  # 440 rows, rails of degree 15 -> 3 lanes of 5: fits 256 lanes
+        assert paths == {"incidence"}
+    pg, tg, _ = gb.get_state()
+    po, to, _ = ob.get_state()
+    assert np.abs(pg - po).max() < 1e-7 and np.abs(tg - to).max() < 1e-5
+
+
+def test_cr_incidence_vs_rows_kernels():
+    """The incidence-owner and row-owner kernels on the same states (the
+    second via KD_CR_REG=3 in a subprocess): impulses within 1e-9 relative."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import paper_2603_16536_b200 as K
+from paper_2603_16536_b200.scenes import closed_chain
+sc = closed_chain(22)
+cfg = K.config_for(sc)
+m = K.build_model(sc)
+b = K.WorldBatch()
+for _ in range(4):
+    b.add_world(m)
+p, t, tm = b.get_state()
+t = K.bench_jitter(t, [m.n_bodies] * 4, seed=3)
+b.set_state(p, t, tm)
+b.step(cfg, 5)
+print(json.dumps({"paths": b.cr_paths(), "imp": b.impulses().tolist(),
+                  "it": [d.iterations for d in b.diagnostics()[:4]]}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("1", "3"):
+        env = dict(os.environ, KD_CR_REG=mode)
+        r = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, check=True)
+        out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert set(out["1"]["paths"]) == {"incidence"} and set(out["3"]["paths"]) == {"rows"}
+    assert out["1"]["it"] == out["3"]["it"]
+    a, b = np.array(out["1"]["imp"]), np.array(out["3"]["imp"])
+    assert np.abs(a - b).max() <= 1e-9 * max(1.0, np.abs(b).max())
