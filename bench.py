@@ -393,9 +393,11 @@ def main():
     peak, peak_kind = measured_peaks()
     if cr_ms > dense_ms:
         fam, fam_ms, fam_bytes = "cr", cr_ms, bytes_cr / rsteps
-        kname = "cr_kernel (K2b: matrix-free Delassus apply + warm-started Conjugate Residual + PADMM)"
-        note = ("SURVEY.md §8d matrix-free model with the applies executed; J rows stream from L2/HBM every "
-                "apply, the n-vectors stay in shared memory")
+        kname = ("cr_op_kernel (K2b: PADMM + warm-started Conjugate Residual over the matrix-free Delassus "
+                 "operator, P J register-resident)")
+        note = ("SURVEY.md §8d matrix-free model with the applies executed (the reference re-reads the baked "
+                "rows every apply); the device keeps P J in registers and the n-vectors in shared memory, so "
+                "HBM is not the binding roof (see DESIGN.md)")
     else:
         fam, fam_ms, fam_bytes = "dense", dense_ms, bytes_dense / rsteps
         nd, nh, ns = (kern_count.get(k, 0) for k in ("dense", "supernodal+dense", "supernodal"))
