@@ -11,7 +11,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 3 --settle 0 --no-e2e --no-cpu > gpurun_out/${TAG}_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_kernel -s 60 -c 1 \
   -o gpurun_out/${TAG}_dense python tests/ncu_target.py 148 62 > gpurun_out/${TAG}_ncu_dense.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:cr_kernel -s 10 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cr_op_kernel -s 10 -c 1 \
   -o gpurun_out/${TAG}_cr python tests/ncu_target_cr.py 296 12 > gpurun_out/${TAG}_ncu_cr.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:snfactor_kernel -s 60 -c 1 \
   -o gpurun_out/${TAG}_snfactor python tests/ncu_target.py 4096 62 > gpurun_out/${TAG}_ncu_snfactor.log 2>&1
