@@ -190,3 +190,39 @@ def test_dr_legs_kkt_and_convergence_at_scale():
     assert max(d[w].kkt_momentum_inf for w in range(256)) < 1e-5
     assert np.mean([d[w].converged for w in range(256)]) > 0.9
     assert max(d[w].f_inf for w in range(256)) < 1e-3
+
+
+@pytest.mark.parametrize("workload,nw,steps", [("dr_legs", 4096, 3), ("closed_chain", 1024, 3)])
+def test_full_size_batch_equals_sampled_solo_runs(workload, nw, steps):
+    """BASELINE sizes (4096 DR-Legs worlds on the dense path, 1024 closed-chain
+    worlds on the matrix-free path): every sampled world of the full batch is
+    bitwise equal to the same world stepped in a small batch (no cross-world
+    interaction, no dependence on batch size or launch shape), and the momentum
+    balance (KKT) holds in every world."""
+    from paper_2603_16536_b200.scenes import closed_chain
+    sc = dr_legs() if workload == "dr_legs" else closed_chain(22)
+    m = K.build_model(sc)
+    cfg = K.config_for(sc)
+    b = K.WorldBatch()
+    for _ in range(nw):
+        b.add_world(m)
+    p, t, tm = b.get_state()
+    t = K.bench_jitter(t, [m.n_bodies] * nw, seed=1)
+    b.set_state(p, t, tm)
+    sample = [0, nw // 3, nw // 2 + 7, nw - 1]
+    s = K.WorldBatch()
+    for _ in sample:
+        s.add_world(m)
+    np_, nt_ = 7 * m.n_bodies, 6 * m.n_bodies
+    s.set_state(np.concatenate([p[w * np_:(w + 1) * np_] for w in sample]),
+                np.concatenate([t[w * nt_:(w + 1) * nt_] for w in sample]), tm[sample])
+    b.step(cfg, steps)
+    s.step(cfg, steps)
+    pb, tb, _ = b.get_state()
+    ps, ts, _ = s.get_state()
+    for k, w in enumerate(sample):
+        assert (pb[w * np_:(w + 1) * np_] == ps[k * np_:(k + 1) * np_]).all()
+        assert (tb[w * nt_:(w + 1) * nt_] == ts[k * nt_:(k + 1) * nt_]).all()
+    d = b.diagnostics()
+    assert max(d[w].kkt_momentum_inf for w in range(nw)) < 1e-5
+    assert len(set(b.kernels())) == 1
