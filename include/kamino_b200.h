@@ -169,6 +169,14 @@ typedef struct kd_model_info {
  * counts loops, resolves default PD targets.  On error returns the ModelError
  * code (KD_ERR_MODEL_*) and kd_last_error() holds the reference message. */
 int kd_model_build(const kd_scene_desc* scene, kd_model** out);
+
+/* Opt-in extensions beyond the reference (no reference counterpart; parity
+ * unpinned).  KD_EXT_BOX_BOX: box-box geom pairs collide (SAT + face clipping,
+ * up to 4 contacts per pair) instead of failing with
+ * KD_ERR_MODEL_UNSUPPORTED_COLLISION_PAIR (model.cpp:56-62).
+ * kd_model_build(scene, out) == kd_model_build_ex(scene, 0, out). */
+#define KD_EXT_BOX_BOX 1u
+int kd_model_build_ex(const kd_scene_desc* scene, uint32_t extensions, kd_model** out);
 void kd_model_destroy(kd_model* model);
 int kd_model_get_info(const kd_model* model, kd_model_info* out);
 /* JointLayout (model.hpp:63-74): per joint row_offset,row_count,dyn_offset,dyn_count */

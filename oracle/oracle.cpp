@@ -313,6 +313,7 @@ MechanismModel build_model(const SceneDescription& scene) {
   MechanismModel m;
   m.name = scene.name;
   m.gravity = scene.gravity;
+  m.box_box = scene.box_box;  // extension flag (see box_box in the contacts section)
   std::map<std::string, int> body_ids;
   for (const SceneBody& sb : scene.bodies) {
     if (sb.name == "world" || body_ids.count(sb.name))
@@ -421,7 +422,7 @@ MechanismModel build_model(const SceneDescription& scene) {
       const GeomSpec& gb = m.geoms[b];
       if (ga.body == gb.body) continue;
       if (ga.body == kWorld && gb.body == kWorld) continue;
-      if (!pair_supported(ga.shape, gb.shape))
+      if (!pair_supported(ga.shape, gb.shape) && !(scene.box_box && ga.shape == Shape::Box && gb.shape == Shape::Box))
         throw ModelError(UnsupportedCollisionPair, std::string("unsupported collision pair: ") +
                                                        shape_name(ga.shape) + "-" + shape_name(gb.shape));
     }
@@ -585,6 +586,185 @@ void box_plane(const MechanismModel& m, int box, int plane, const std::vector<Po
     out.push_back(cp);
   }
 }
+
+// ---- box_box: EXTENSION, not in the reference (it rejects box-box pairs,
+// model.cpp:56-62), so parity is unpinned: this restatement and the device
+// narrow phase (kd_assemble.cu) implement the same algorithm.
+//   SAT over the 15 axes (3 + 3 face normals, 9 edge cross products; edge
+//   axes shorter than 1e-6 skipped); any axis with overlap <= -margin separates.
+//   Face case (a face axis has the least overlap, edges preferred only below
+//   best_face - 1e-5 - 0.05 |best_face|): the incident face of the other box
+//   (most anti-parallel) is clipped against the reference face's four side
+//   planes (Sutherland-Hodgman, order +s1 -s1 +s2 -s2); each clipped point
+//   with depth = -(p - face_center) . n_face > -margin becomes a contact at the
+//   midpoint of the point and its projection on the reference face; more than
+//   4 -> the deepest (first on ties), then three farthest-point picks (largest
+//   minimum squared distance to the picked points, first on ties), emitted in
+//   clip order.
+//   Edge case: one contact at the midpoint of the closest points of the two
+//   supporting edges, depth = the axis overlap.
+//   Normal from b to a (the sphere_sphere convention), geom_a < geom_b.
+void box_box(const MechanismModel& m, int a, int b, const std::vector<Pose>& poses, double margin,
+             std::vector<ContactPoint>& out) {
+  const GeomSpec& ga = m.geoms[a];
+  const GeomSpec& gb = m.geoms[b];
+  const Vec3 ca = poses[ga.body].position, cb = poses[gb.body].position;
+  const Mat3 Ra = poses[ga.body].rotation(), Rb = poses[gb.body].rotation();
+  const Vec3 ha = ga.half_extents, hb = gb.half_extents;
+  const Vec3 d = ca - cb;
+  auto radius = [](const Mat3& R, const Vec3& h, const Vec3& L) {
+    return (h.x * std::abs(dot(R.col(0), L)) + h.y * std::abs(dot(R.col(1), L))) + h.z * std::abs(dot(R.col(2), L));
+  };
+  double best_face = 1e300, best_edge = 1e300;
+  int face = -1, ei = -1, ej = -1;
+  for (int f = 0; f < 6; ++f) {
+    const Vec3 L = f < 3 ? Ra.col(f) : Rb.col(f - 3);
+    const double ov = (radius(Ra, ha, L) + radius(Rb, hb, L)) - std::abs(dot(d, L));
+    if (ov <= -margin) return;
+    if (ov < best_face) {
+      best_face = ov;
+      face = f;
+    }
+  }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      Vec3 L = cross(Ra.col(i), Rb.col(j));
+      const double l = norm(L);
+      if (l < 1e-6) continue;
+      L = L / l;
+      const double ov = (radius(Ra, ha, L) + radius(Rb, hb, L)) - std::abs(dot(d, L));
+      if (ov <= -margin) return;
+      if (ov < best_edge) {
+        best_edge = ov;
+        ei = i;
+        ej = j;
+      }
+    }
+  const double mu = combined_mu(ga, gb), e = combined_e(ga, gb);
+  if (ei >= 0 && best_edge < best_face - 1e-5 - 0.05 * std::abs(best_face)) {
+    Vec3 n = normalized(cross(Ra.col(ei), Rb.col(ej)));
+    if (dot(d, n) < 0) n = -n;
+    Vec3 pa = ca, pb = cb;
+    for (int k = 0; k < 3; ++k) {
+      if (k != ei) pa = pa + (dot(Ra.col(k), n) > 0 ? -ha[k] : ha[k]) * Ra.col(k);
+      if (k != ej) pb = pb + (dot(Rb.col(k), n) > 0 ? hb[k] : -hb[k]) * Rb.col(k);
+    }
+    const Vec3 da = Ra.col(ei), db = Rb.col(ej), r = pa - pb;
+    const double a12 = dot(da, db), b1 = dot(da, r), b2 = dot(db, r), den = 1.0 - a12 * a12;
+    double s = den > 1e-12 ? (a12 * b2 - b1) / den : 0.0;
+    s = std::min(std::max(s, -ha[ei]), ha[ei]);
+    double t = b2 + s * a12;
+    t = std::min(std::max(t, -hb[ej]), hb[ej]);
+    ContactPoint cp;
+    cp.geom_a = a;
+    cp.geom_b = b;
+    cp.normal = n;
+    cp.position = 0.5 * ((pa + s * da) + (pb + t * db));
+    cp.depth = best_edge;
+    cp.mu = mu;
+    cp.restitution = e;
+    out.push_back(cp);
+    return;
+  }
+  // face case: reference box R (owner of the face axis), incident box I
+  const bool refA = face < 3;
+  const int fi = refA ? face : face - 3;
+  const Mat3& RR = refA ? Ra : Rb;
+  const Mat3& RI = refA ? Rb : Ra;
+  const Vec3 cR = refA ? ca : cb, cI = refA ? cb : ca;
+  const Vec3 hR = refA ? ha : hb, hI = refA ? hb : ha;
+  const Vec3 L = RR.col(fi);
+  const double sdl = dot(d, L);
+  // outward normal of the reference face toward the other box; contact normal b -> a
+  const Vec3 nf = refA ? (sdl > 0 ? -L : L) : (sdl < 0 ? -L : L);
+  const Vec3 n = refA ? -nf : nf;
+  int k = 0;
+  double best = -1.0;
+  for (int q = 0; q < 3; ++q) {
+    const double c = std::abs(dot(RI.col(q), nf));
+    if (c > best) {
+      best = c;
+      k = q;
+    }
+  }
+  const Vec3 fnI = dot(RI.col(k), nf) > 0 ? -RI.col(k) : RI.col(k);
+  const int k1 = k == 0 ? 1 : 0, k2 = k == 2 ? 1 : 2;
+  const Vec3 fc = cI + hI[k] * fnI, u1 = hI[k1] * RI.col(k1), u2 = hI[k2] * RI.col(k2);
+  Vec3 poly[8], tmp[8];
+  int np = 4;
+  poly[0] = (fc - u1) - u2;
+  poly[1] = (fc + u1) - u2;
+  poly[2] = (fc + u1) + u2;
+  poly[3] = (fc - u1) + u2;
+  const int i1 = fi == 0 ? 1 : 0, i2 = fi == 2 ? 1 : 2;
+  const Vec3 rc = cR + hR[fi] * nf;
+  for (int pl = 0; pl < 4 && np > 0; ++pl) {
+    const Vec3 sdir = (pl & 1) ? -RR.col(pl < 2 ? i1 : i2) : RR.col(pl < 2 ? i1 : i2);
+    const double ext = hR[pl < 2 ? i1 : i2];
+    int nt = 0;
+    Vec3 prev = poly[np - 1];
+    double dp = dot(prev - rc, sdir) - ext;
+    for (int q = 0; q < np; ++q) {
+      const Vec3 cur = poly[q];
+      const double dc = dot(cur - rc, sdir) - ext;
+      if (dc <= 0) {
+        if (dp > 0) tmp[nt++] = prev + (dp / (dp - dc)) * (cur - prev);
+        tmp[nt++] = cur;
+      } else if (dp <= 0) {
+        tmp[nt++] = prev + (dp / (dp - dc)) * (cur - prev);
+      }
+      prev = cur;
+      dp = dc;
+    }
+    np = nt;
+    for (int q = 0; q < np; ++q) poly[q] = tmp[q];
+  }
+  struct Hit {
+    int index;
+    Vec3 point;
+    double depth;
+  };
+  std::vector<Hit> hits;
+  for (int q = 0; q < np; ++q) {
+    const double depth = -dot(poly[q] - rc, nf);
+    if (depth > -margin) hits.push_back({q, poly[q] + (0.5 * depth) * nf, depth});
+  }
+  if (hits.size() > 4) {  // the deepest point, then farthest-point picks (spread support), clip order
+    std::vector<int> pick;
+    int first = 0;
+    for (int q = 1; q < (int)hits.size(); ++q)
+      if (hits[q].depth > hits[first].depth) first = q;
+    pick.push_back(first);
+    while (pick.size() < 4) {
+      int bq = -1;
+      double bd = -1.0;
+      for (int q = 0; q < (int)hits.size(); ++q) {
+        double md = 1e300;
+        for (int pq : pick) md = std::min(md, squared_norm(hits[q].point - hits[pq].point));
+        if (md > bd) {
+          bd = md;
+          bq = q;
+        }
+      }
+      pick.push_back(bq);
+    }
+    std::sort(pick.begin(), pick.end());
+    std::vector<Hit> kept;
+    for (int q : pick) kept.push_back(hits[q]);
+    hits = kept;
+  }
+  for (const Hit& h : hits) {
+    ContactPoint cp;
+    cp.geom_a = a;
+    cp.geom_b = b;
+    cp.normal = n;
+    cp.position = h.point;
+    cp.depth = h.depth;
+    cp.mu = mu;
+    cp.restitution = e;
+    out.push_back(cp);
+  }
+}
 }  // namespace
 
 // contact_frame: contacts.cpp:110-117
@@ -615,6 +795,7 @@ std::vector<ContactPoint> collide(const MechanismModel& m, const std::vector<Pos
       else if (gi.shape == Shape::Plane && gj.shape == Shape::Sphere) sphere_plane(m, j, i, poses, margin, out);
       else if (gi.shape == Shape::Box && gj.shape == Shape::Plane) box_plane(m, i, j, poses, margin, out);
       else if (gi.shape == Shape::Plane && gj.shape == Shape::Box) box_plane(m, j, i, poses, margin, out);
+      else if (gi.shape == Shape::Box && gj.shape == Shape::Box && m.box_box) box_box(m, i, j, poses, margin, out);
     }
   return out;
 }

@@ -201,6 +201,7 @@ struct SceneDescription {
   std::vector<SceneBody> bodies;
   std::vector<SceneJoint> joints;
   std::vector<SceneGeom> geoms;
+  bool box_box = false;  // extension (not in the reference, which rejects box-box pairs, model.cpp:56-62)
 };
 
 constexpr int kWorld = -1;
@@ -254,6 +255,7 @@ struct MechanismModel {
   Vec3 gravity{0, 0, -9.81};
   std::vector<JointLayout> joint_layout;
   int n_bilateral_rows = 0, n_dynamics_rows = 0, n_loops = 0;
+  bool box_box = false;  // extension: box-box pairs collide (box_box below)
   int n_bodies() const { return (int)bodies.size(); }
 };
 int joint_row_count(JointType t);

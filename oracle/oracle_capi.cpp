@@ -170,11 +170,13 @@ void or_step_config_default(kd_step_config* c) {
   c->warm_start = 1;
 }
 
-int or_model_build(const kd_scene_desc* scene, void** out) {
+int or_model_build_ex(const kd_scene_desc* scene, uint32_t extensions, void** out) {
   if (!scene || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   try {
     auto* m = new OrModel;
-    m->m = std::make_shared<const MechanismModel>(build_model(to_scene(scene)));
+    SceneDescription sd = to_scene(scene);
+    sd.box_box = (extensions & KD_EXT_BOX_BOX) != 0;
+    m->m = std::make_shared<const MechanismModel>(build_model(sd));
     m->info = make_info(*m->m);
     *out = m;
     return KD_OK;
@@ -184,6 +186,8 @@ int or_model_build(const kd_scene_desc* scene, void** out) {
     return fail(KD_ERR_INVALID_ARGUMENT, e.what());
   }
 }
+
+int or_model_build(const kd_scene_desc* scene, void** out) { return or_model_build_ex(scene, 0, out); }
 
 void or_model_destroy(void* m) { delete static_cast<OrModel*>(m); }
 

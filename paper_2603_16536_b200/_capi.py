@@ -180,6 +180,7 @@ class kd_row_dump(C.Structure):
 _H = C.c_void_p
 SIGNATURES = {
     "model_build": (C.c_int, [C.POINTER(kd_scene_desc), C.POINTER(C.c_void_p)]),
+    "model_build_ex": (C.c_int, [C.POINTER(kd_scene_desc), C.c_uint32, C.POINTER(C.c_void_p)]),
     "model_destroy": (None, [_H]),
     "model_get_info": (C.c_int, [_H, C.POINTER(kd_model_info)]),
     "model_joint_layout": (C.c_int, [_H, c_int32_p, c_int32_p, c_int32_p, c_int32_p]),

@@ -29,6 +29,156 @@ struct CP {
   double depth;
 };
 
+// box_box: EXTENSION (KD_EXT_BOX_BOX), not in the reference, which rejects
+// box-box pairs (model.cpp:56-62); parity is against the oracle's restatement
+// of the same algorithm (oracle.cpp box_box): SAT over 15 axes, then either one
+// edge-edge contact or the incident face clipped against the reference face's
+// side planes (up to 8 points, at most 4 kept, in clip order).  Normal from
+// b to a, contact at the midpoint between the incident point and the reference
+// face; more than 4 clipped points -> the deepest plus three farthest-point
+// picks.  Same operation order as the oracle.
+__device__ __noinline__ int box_box_dev(V3 ca, const M3& Ra, const double* ha, V3 cb, const M3& Rb, const double* hb,
+                                        double margin, CP* cps) {
+  const V3 d = sub(ca, cb);
+  auto radius = [](const M3& R, const double* h, V3 L) {
+    return (h[0] * fabs(dot(mcol(R, 0), L)) + h[1] * fabs(dot(mcol(R, 1), L))) + h[2] * fabs(dot(mcol(R, 2), L));
+  };
+  double best_face = 1e300, best_edge = 1e300;
+  int face = -1, ei = -1, ej = -1;
+  for (int f = 0; f < 6; ++f) {
+    const V3 L = f < 3 ? mcol(Ra, f) : mcol(Rb, f - 3);
+    const double ov = (radius(Ra, ha, L) + radius(Rb, hb, L)) - fabs(dot(d, L));
+    if (ov <= -margin) return 0;
+    if (ov < best_face) {
+      best_face = ov;
+      face = f;
+    }
+  }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      V3 L = cross(mcol(Ra, i), mcol(Rb, j));
+      const double l = norm(L);
+      if (l < 1e-6) continue;
+      L = V3{L.x / l, L.y / l, L.z / l};
+      const double ov = (radius(Ra, ha, L) + radius(Rb, hb, L)) - fabs(dot(d, L));
+      if (ov <= -margin) return 0;
+      if (ov < best_edge) {
+        best_edge = ov;
+        ei = i;
+        ej = j;
+      }
+    }
+  if (ei >= 0 && best_edge < best_face - 1e-5 - 0.05 * fabs(best_face)) {
+    V3 n = cross(mcol(Ra, ei), mcol(Rb, ej));
+    const double ln = norm(n);
+    n = V3{n.x / ln, n.y / ln, n.z / ln};
+    if (dot(d, n) < 0) n = neg(n);
+    V3 pa = ca, pb = cb;
+    for (int k = 0; k < 3; ++k) {
+      if (k != ei) pa = add(pa, scl(dot(mcol(Ra, k), n) > 0 ? -ha[k] : ha[k], mcol(Ra, k)));
+      if (k != ej) pb = add(pb, scl(dot(mcol(Rb, k), n) > 0 ? hb[k] : -hb[k], mcol(Rb, k)));
+    }
+    const V3 da = mcol(Ra, ei), db = mcol(Rb, ej), r = sub(pa, pb);
+    const double a12 = dot(da, db), b1 = dot(da, r), b2 = dot(db, r), den = 1.0 - a12 * a12;
+    double s = den > 1e-12 ? (a12 * b2 - b1) / den : 0.0;
+    s = fmin(fmax(s, -ha[ei]), ha[ei]);
+    double t = b2 + s * a12;
+    t = fmin(fmax(t, -hb[ej]), hb[ej]);
+    cps[0] = CP{scl(0.5, add(add(pa, scl(s, da)), add(pb, scl(t, db)))), n, best_edge};
+    return 1;
+  }
+  const bool refA = face < 3;
+  const int fi = refA ? face : face - 3;
+  const M3& RR = refA ? Ra : Rb;
+  const M3& RI = refA ? Rb : Ra;
+  const V3 cR = refA ? ca : cb, cI = refA ? cb : ca;
+  const double* hR = refA ? ha : hb;
+  const double* hI = refA ? hb : ha;
+  const V3 L = mcol(RR, fi);
+  const double sdl = dot(d, L);
+  const V3 nf = refA ? (sdl > 0 ? neg(L) : L) : (sdl < 0 ? neg(L) : L);
+  const V3 n = refA ? neg(nf) : nf;
+  int k = 0;
+  double best = -1.0;
+  for (int q = 0; q < 3; ++q) {
+    const double c = fabs(dot(mcol(RI, q), nf));
+    if (c > best) {
+      best = c;
+      k = q;
+    }
+  }
+  const V3 fnI = dot(mcol(RI, k), nf) > 0 ? neg(mcol(RI, k)) : mcol(RI, k);
+  const int k1 = k == 0 ? 1 : 0, k2 = k == 2 ? 1 : 2;
+  const V3 fc = add(cI, scl(hI[k], fnI)), u1 = scl(hI[k1], mcol(RI, k1)), u2 = scl(hI[k2], mcol(RI, k2));
+  V3 poly[8], tmp[8];
+  int np = 4;
+  poly[0] = sub(sub(fc, u1), u2);
+  poly[1] = sub(add(fc, u1), u2);
+  poly[2] = add(add(fc, u1), u2);
+  poly[3] = add(sub(fc, u1), u2);
+  const int i1 = fi == 0 ? 1 : 0, i2 = fi == 2 ? 1 : 2;
+  const V3 rc = add(cR, scl(hR[fi], nf));
+  for (int pl = 0; pl < 4 && np > 0; ++pl) {
+    const V3 sax = mcol(RR, pl < 2 ? i1 : i2);
+    const V3 sdir = (pl & 1) ? neg(sax) : sax;
+    const double ext = hR[pl < 2 ? i1 : i2];
+    int nt = 0;
+    V3 prev = poly[np - 1];
+    double dp = dot(sub(prev, rc), sdir) - ext;
+    for (int q = 0; q < np; ++q) {
+      const V3 cur = poly[q];
+      const double dc = dot(sub(cur, rc), sdir) - ext;
+      if (dc <= 0) {
+        if (dp > 0) tmp[nt++] = add(prev, scl(dp / (dp - dc), sub(cur, prev)));
+        tmp[nt++] = cur;
+      } else if (dp <= 0) {
+        tmp[nt++] = add(prev, scl(dp / (dp - dc), sub(cur, prev)));
+      }
+      prev = cur;
+      dp = dc;
+    }
+    np = nt;
+    for (int q = 0; q < np; ++q) poly[q] = tmp[q];
+  }
+  double dep[8];
+  int hits = 0;
+  for (int q = 0; q < np; ++q) {
+    dep[q] = -dot(sub(poly[q], rc), nf);
+    if (dep[q] > -margin) hits |= 1 << q;
+    poly[q] = add(poly[q], scl(0.5 * dep[q], nf));  // the contact position
+  }
+  if (__popc(hits) > 4) {  // the deepest, then farthest-point picks, clip order (as the oracle)
+    int first = -1;
+    for (int q = 0; q < np; ++q)
+      if ((hits >> q & 1) && (first < 0 || dep[q] > dep[first])) first = q;
+    int pick = 1 << first;
+    for (int r = 1; r < 4; ++r) {
+      int bq = -1;
+      double bd = -1.0;
+      for (int q = 0; q < np; ++q) {
+        if (!(hits >> q & 1)) continue;
+        double md = 1e300;
+        for (int pq = 0; pq < np; ++pq) {
+          if (!(pick >> pq & 1)) continue;
+          const V3 dv = sub(poly[q], poly[pq]);
+          md = fmin(md, dot(dv, dv));
+        }
+        if (md > bd) {
+          bd = md;
+          bq = q;
+        }
+      }
+      pick |= 1 << bq;
+    }
+    hits = pick;
+  }
+  int cnt = 0;
+  for (int q = 0; q < np; ++q)
+    if (hits >> q & 1) cps[cnt++] = CP{poly[q], n, dep[q]};
+  return cnt;
+}
+
+
 }  // namespace
 
 __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams sp) {
@@ -131,6 +281,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
           cps[0] = CP{scl(0.5, add(sub(ca, scl(ga.radius, n)), add(cb, scl(gb.radius, n)))), n, depth};
           cnt = 1;
         }
+      } else if (pr.kind == P_BOX_BOX) {  // extension (box_box_dev)
+        cnt = box_box_dev(ld3(bs[ga.body].ep), ldm(bs[ga.body].eR), ga.he, ld3(bs[gb.body].ep), ldm(bs[gb.body].eR),
+                          gb.he, sp.contact_margin, cps);
       } else {  // box_plane (contacts.cpp:66-106)
         const V3 c = ld3(bs[ga.body].ep);
         const M3 R = ldm(bs[ga.body].eR);

@@ -174,11 +174,14 @@ void kd_step_config_default(kd_step_config* c) {
   c->warm_start = 1;
 }
 
-int kd_model_build(const kd_scene_desc* scene, kd_model** out) {
+int kd_model_build(const kd_scene_desc* scene, kd_model** out) { return kd_model_build_ex(scene, 0, out); }
+
+int kd_model_build_ex(const kd_scene_desc* scene, uint32_t extensions, kd_model** out) {
   if (!scene || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (extensions & ~KD_EXT_BOX_BOX) return fail(KD_ERR_INVALID_ARGUMENT, "unknown extension bits");
   auto* m = new kd_model;
   std::string err;
-  const int code = build_host_model(scene, m->m, err);
+  const int code = build_host_model(scene, m->m, err, extensions);
   if (code != KD_OK) {
     delete m;
     return fail(code, err);
@@ -349,9 +352,12 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     d.n_bil = m.n_bil;
     d.n_dyn = m.n_dyn;
     d.n_limited = m.info.n_limited_joints;
-    // contact capacity: every supported pair can produce 1 (4 for box-plane)
-    // contact, capped for large piles at 6 per geom (+16); overflow is an error.
-    contact_cap[i] = std::min(m.info.max_contacts, 6 * d.ng + 16);
+    // contact capacity: every supported pair can produce 1 (4 for box-plane and
+    // box-box) contact, capped for large piles at 6 per geom (8 with box-box
+    // pairs: face contacts carry 4 points) + 16; overflow is an error.
+    bool box_box = false;
+    for (const DevPair& pr : m.pairs) box_box = box_box || pr.kind == P_BOX_BOX;
+    contact_cap[i] = std::min(m.info.max_contacts, (box_box ? 8 : 6) * d.ng + 16);
     d.max_contacts = contact_cap[i];
     row_cap[i] = d.n_bil + d.n_dyn + 2 * d.n_limited + 3 * contact_cap[i];
     d.row_cap = row_cap[i];

@@ -30,7 +30,7 @@ struct HostModel {
   std::string sn_why;
 };
 
-int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err);
+int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err, uint32_t extensions = 0);
 double host_joint_coordinate(const HostModel& m, int joint, const double* poses7);
 
 // kernel launchers (one per translation unit)

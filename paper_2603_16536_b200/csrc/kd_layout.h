@@ -24,7 +24,7 @@ enum JointKind : int32_t { J_FIXED = 0, J_REVOLUTE = 1, J_PRISMATIC = 2, J_SPHER
 enum GeomShape : int32_t { G_SPHERE = 0, G_PLANE = 1, G_BOX = 2 };
 // Collision pair kinds in collide() dispatch order (contacts.cpp:130-140);
 // `a` is always the moving geom (ContactPoint::geom_a), `b` the other one.
-enum PairKind : int32_t { P_SPHERE_SPHERE = 0, P_SPHERE_PLANE = 1, P_BOX_PLANE = 2 };
+enum PairKind : int32_t { P_SPHERE_SPHERE = 0, P_SPHERE_PLANE = 1, P_BOX_PLANE = 2, P_BOX_BOX = 3 };
 enum RowKind : int32_t { ROW_BILATERAL = 0, ROW_LIMIT = 1, ROW_CONTACT = 2 };
 // BE_DENSE_SN: the supernodal kernel factors (plan order) and hands L to the
 // dense kernel, which forms L^-1 and runs the PADMM solves

@@ -96,7 +96,7 @@ double host_joint_coordinate(const HostModel& m, int joint, const double* poses7
   return dot(axis, mvec(mtrans(Rp), sub(ac, ap)));
 }
 
-int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err) {
+int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err, uint32_t extensions) {
   try {
     m.name = s(d->name);
     for (int k = 0; k < 3; ++k) m.gravity[k] = d->gravity[k];
@@ -266,10 +266,12 @@ int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err) {
         else if (ga.shape == G_PLANE && gb.shape == G_SPHERE) p = DevPair{b, a, P_SPHERE_PLANE, 0};
         else if (ga.shape == G_BOX && gb.shape == G_PLANE) p = DevPair{a, b, P_BOX_PLANE, 0};
         else if (ga.shape == G_PLANE && gb.shape == G_BOX) p = DevPair{b, a, P_BOX_PLANE, 0};
+        else if (ga.shape == G_BOX && gb.shape == G_BOX && (extensions & KD_EXT_BOX_BOX))
+          p = DevPair{a, b, P_BOX_BOX, 0};  // extension (kd_assemble.cu box_box)
         else
           fail(KD_ERR_MODEL_UNSUPPORTED_COLLISION_PAIR,
                std::string("unsupported collision pair: ") + names[ga.shape] + "-" + names[gb.shape]);
-        max_contacts += p.kind == P_BOX_PLANE ? 4 : 1;
+        max_contacts += (p.kind == P_BOX_PLANE || p.kind == P_BOX_BOX) ? 4 : 1;
         m.pairs.push_back(p);
       }
     // row layout (model.cpp:254-276)

@@ -59,7 +59,7 @@ class Model:
     def __init__(self, scene: SceneDescription):
         desc, keep = scene.to_ctypes()
         h = C.c_void_p()
-        _check(lib().kd_model_build(C.byref(desc), C.byref(h)))
+        _check(lib().kd_model_build_ex(C.byref(desc), C.c_uint32(scene.extension_bits()), C.byref(h)))
         self.handle = h
         self.scene = scene
         self.name = scene.name

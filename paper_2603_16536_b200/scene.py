@@ -100,6 +100,17 @@ class SceneDescription:
     joints: List[SceneJoint] = field(default_factory=list)
     geoms: List[SceneGeom] = field(default_factory=list)
     config: SceneConfig = field(default_factory=SceneConfig)
+    # opt-in extensions beyond the reference (kd_model_build_ex): "box_box"
+    extensions: List[str] = field(default_factory=list)
+
+    def extension_bits(self) -> int:
+        bits = {"box_box": 1}  # KD_EXT_BOX_BOX
+        out = 0
+        for e in self.extensions:
+            if e not in bits:
+                raise ValueError(f"unknown extension '{e}'")
+            out |= bits[e]
+        return out
 
     def copy(self) -> "SceneDescription":
         return dataclasses.replace(
@@ -109,6 +120,7 @@ class SceneDescription:
             joints=[dataclasses.replace(j) for j in self.joints],
             geoms=[dataclasses.replace(g) for g in self.geoms],
             config=dataclasses.replace(self.config),
+            extensions=list(self.extensions),
         )
 
     # ---- C-ABI marshalling -------------------------------------------------
@@ -306,6 +318,9 @@ def parse_scene_obj(root: dict, origin: str = "<string>") -> SceneDescription:
         g.mu = _get_number(jg, "mu", origin, where, 0.0)
         g.restitution = _get_number(jg, "restitution", origin, where, 0.0)
         scene.geoms.append(g)
+    if "extensions" in root:  # not in the reference's scene format (opt-in, kd_model_build_ex)
+        scene.extensions = [str(e) for e in root["extensions"]]
+        scene.extension_bits()
     if "config" in root:  # scene.cpp:159-172
         jc = root["config"]
         c = scene.config

@@ -192,3 +192,46 @@ def sphere_pile(n_spheres=100, radius=0.05, mu=0.5, seed=7) -> SceneDescription:
     for nrm, off in walls:
         b.geom(body="world", shape="plane", normal=nrm, offset=off, mu=mu, restitution=0.0)
     return b.scene()
+
+
+def box_pile(n_boxes=64, half=0.05, mu=0.5, seed=11) -> SceneDescription:
+    """Config 5 as written (BASELINE.json configs[4]): a pile of boxes in a bin
+    of five world planes.  Needs the opt-in box-box extension
+    (KD_EXT_BOX_BOX; the reference rejects box-box pairs, model.cpp:56-62, so
+    this scene has no reference counterpart and its parity is against the
+    oracle's restatement of the same narrow phase).  Layers of side x side
+    boxes, 0.02 apart horizontally (beyond the 0.01 contact margin), each layer
+    dropped 0.004 above the one below with a small deterministic yaw."""
+    import random
+    rng = random.Random(seed)
+    b = _Builder("box_pile")
+    side = int(math.ceil(math.sqrt(n_boxes / 4.0)))
+    pitch = 2.0 * half + 0.02
+    extent = side * pitch / 2.0
+    m = 0.1
+    k = 0
+    layer = 0
+    while k < n_boxes:
+        for i in range(side):
+            for j in range(side):
+                if k >= n_boxes:
+                    break
+                x = -extent + pitch / 2 + i * pitch + rng.uniform(-1e-3, 1e-3)
+                y = -extent + pitch / 2 + j * pitch + rng.uniform(-1e-3, 1e-3)
+                z = half + layer * (2.0 * half + 0.004)
+                yaw = rng.uniform(-0.05, 0.05)
+                name = f"b{k}"
+                b.pos[name] = [x, y, z]
+                b.root["bodies"].append({"name": name, "mass": m, "inertia": _box_inertia(m, 2 * half, 2 * half, 2 * half),
+                                         "position": [x, y, z],
+                                         "orientation": [math.cos(yaw / 2), 0.0, 0.0, math.sin(yaw / 2)]})
+                b.geom(body=name, shape="box", half_extents=[half, half, half], mu=mu, restitution=0.0)
+                k += 1
+        layer += 1
+    wall = extent + 0.01
+    walls = (([0.0, 0.0, 1.0], 0.0), ([1.0, 0.0, 0.0], -wall), ([-1.0, 0.0, 0.0], -wall),
+             ([0.0, 1.0, 0.0], -wall), ([0.0, -1.0, 0.0], -wall))
+    for nrm, off in walls:
+        b.geom(body="world", shape="plane", normal=nrm, offset=off, mu=mu, restitution=0.0)
+    b.root["extensions"] = ["box_box"]
+    return b.scene()
