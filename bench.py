@@ -29,7 +29,9 @@ is dr_legs): fourbar (configs[0]'s scene batched, 16384 worlds), hetero
 (configs[2]: four-bar / DR-Legs / serial_chain_10 by w % 3, 16384 worlds),
 closed_chain (configs[3]: 1024 ladder worlds, n = 340 -> matrix-free CR),
 sphere_pile (configs[4] substitute: 100 spheres in a bin, 8192 worlds per GPU,
-CR).  The roofline object then describes the workload's dominant kernel family.
+CR), box_pile (configs[4] as written: 64 boxes in a bin with the opt-in box-box
+narrow phase, 8192 worlds per GPU, CR).  The roofline object then describes the
+workload's dominant kernel family.
 
 Multi-GPU: one process per GPU (torchrun); rank r owns global worlds
 [r*W, (r+1)*W): worlds are independent, so there is no collective on the data
@@ -58,7 +60,7 @@ UNIT = "world-steps/s"
 def workloads():
     """name -> (scene builders, world -> model index, default worlds per GPU, BASELINE config)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from paper_2603_16536_b200.scenes import closed_chain, dr_legs, sphere_pile
+    from paper_2603_16536_b200.scenes import box_pile, closed_chain, dr_legs, sphere_pile
 
     def bundled(name):
         def make():
@@ -76,6 +78,10 @@ def workloads():
         "sphere_pile": ([lambda: sphere_pile(100)], lambda w: 0, 8192,
                         "configs[4] substitute: 100 spheres in a 5-plane bin (box-box is rejected, "
                         "model.cpp:56-62), matrix-free CR"),
+        "box_pile": ([lambda: box_pile(64)], lambda w: 0, 8192,
+                     "configs[4] as written: 64 boxes in a 5-plane bin (256+ frictional contacts per world) "
+                     "with the opt-in box-box narrow phase (KD_EXT_BOX_BOX; the reference rejects box-box "
+                     "pairs, model.cpp:56-62), matrix-free CR"),
     }
 
 
@@ -87,7 +93,7 @@ def parse():
     ap.add_argument("--settle", type=int, default=50)
     ap.add_argument("--worlds-per-gpu", type=int, default=0, help="0: the workload's default")
     ap.add_argument("--workload", default="dr_legs",
-                    choices=["dr_legs", "fourbar", "hetero", "closed_chain", "sphere_pile"])
+                    choices=["dr_legs", "fourbar", "hetero", "closed_chain", "sphere_pile", "box_pile"])
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
