@@ -85,6 +85,7 @@ struct SceneDescription {
   std::vector<SceneJoint> joints;
   std::vector<SceneGeom> geoms;
   SceneConfig config;
+  uint32_t extensions = 0;  // KD_EXT_* opt-in extensions (no reference counterpart)
 };
 
 // ---- errors (model.hpp:76-94)
@@ -182,7 +183,7 @@ class MechanismModel {
     d.n_geoms = (int32_t)g.size();
     d.geoms = g.data();
     kd_model* m = nullptr;
-    detail::check(kd_model_build(&d, &m));
+    detail::check(kd_model_build_ex(&d, s.extensions, &m));
     handle_.reset(m, kd_model_destroy);
     detail::check(kd_model_get_info(m, &info_));
   }
