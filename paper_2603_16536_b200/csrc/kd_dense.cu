@@ -467,8 +467,19 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, u
 
 }  // namespace
 
+// small bins (<= 128 rows, little shared memory) would be register-limited to
+// four CTAs per SM at 255 registers: cap them so more worlds stay resident
+#ifndef KD_DENSE_MINB64
+#define KD_DENSE_MINB64 8
+#endif
+#ifndef KD_DENSE_MINB128
+#define KD_DENSE_MINB128 4
+#endif
+template <int NT>
+constexpr int dense_min_blocks() { return NT <= 64 ? KD_DENSE_MINB64 : (NT <= 128 ? KD_DENSE_MINB128 : 1); }
+
 template <int NT, bool GLOBAL_L>
-__global__ void __launch_bounds__(NT, 1) dense_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
+__global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
   extern __shared__ __align__(16) double smem[];
   const int w = bin_worlds[blockIdx.x];
   WorldStep& ws = bv.wstep[w];
