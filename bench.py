@@ -276,13 +276,19 @@ def run_reference(args):
 def ncu_traffic(kernel, workload, worlds_in_launch):
     """dram bytes (read + write) per launch from the committed ncu capture of
     this kernel on this workload's model (profiles/ncu_traffic.json, per
-    world), scaled to this launch's worlds; None if there is no capture."""
+    world), scaled to this launch's worlds, and the capture's on-chip pipe
+    utilisation; (None, None, None) if there is no capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             rec = json.load(f)[f"{kernel}@{workload}"]
-        return rec["bytes_per_world"] * worlds_in_launch, rec["source"]
+        onchip = rec.get("onchip")
+        if onchip is not None:
+            onchip = dict(onchip, source=rec["source"],
+                          note="shared-memory pipe = smem wavefronts / SM active cycles (one per cycle peak); "
+                               "the smem-resident kernels are bound here and by latency, not by HBM")
+        return rec["bytes_per_world"] * worlds_in_launch, rec["source"], onchip
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def make_chunks(K, torch, b, models, wmodel, W, local):
@@ -434,7 +440,7 @@ def main():
                 "shared-memory resident, so HBM is not the binding roof (see DESIGN.md)")
     achieved = fam_bytes / (fam_ms / 1e3) / 1e9
     worlds_in_launch = sum(v for k, v in kern_count.items() if (k == "cr") == (fam == "cr") and k != "none") / rsteps
-    traffic, traffic_src = ncu_traffic(kname.split(" ")[0], args.workload, worlds_in_launch)
+    traffic, traffic_src, onchip = ncu_traffic(kname.split(" ")[0], args.workload, worlds_in_launch)
     d = b.diagnostics()
     rows_mean = float(np.mean([d[w].n_rows for w in range(W)]))
     from paper_2603_16536_b200 import sharding
@@ -509,7 +515,7 @@ def main():
                        "parallelism": f"worlds sharded over {ws} GPU(s), no data-path collective"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_kind": peak_kind, "kernel": kname,
+                         "peak_kind": peak_kind, "kernel": kname, "onchip": onchip,
                          "kernel_ms_per_launch": fam_ms, "kernel_share_of_step": fam_ms / step_ms_fam,
                          "algorithmic_bytes_per_launch": fam_bytes,
                          "path_bytes_per_step": bytes_path / rsteps if fam == "dense" else None,
