@@ -12,7 +12,7 @@ import oracle_lib
 import paper_2603_16536_b200 as K
 from paper_2603_16536_b200 import _capi
 from paper_2603_16536_b200.scene import ModelError, SceneBody, SceneDescription, SceneGeom, SceneJoint
-from paper_2603_16536_b200.scenes import closed_chain, dr_legs, sphere_pile
+from paper_2603_16536_b200.scenes import box_pile, closed_chain, dr_legs, sphere_pile
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "kamino_b200.h")
 
@@ -65,7 +65,7 @@ def test_model_build_matches_oracle(name):
 
 
 def test_synthetic_models_match_oracle():
-    for sc in (dr_legs(), closed_chain(16), sphere_pile(20)):
+    for sc in (dr_legs(), closed_chain(16), sphere_pile(20), box_pile(8)):
         m, o = K.build_model(sc), oracle_lib.OracleModel(sc)
         for f, _ in m.info._fields_:
             assert getattr(m.info, f) == getattr(o.info, f), (sc.name, f)
