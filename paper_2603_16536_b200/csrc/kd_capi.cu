@@ -310,7 +310,8 @@ int kd_joint_coordinate(const kd_model* mp, int32_t joint, const double* poses7,
 // --------------------------------------------------------------------- batch
 int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_models, const int32_t* world_model,
                     int32_t n_worlds, kd_batch** out) {
-  if (!models || !out || n_models <= 0 || n_worlds < 0 || (n_worlds > 0 && !world_model))
+  // an empty batch (no models, no worlds) is valid, as WorldBatch() is (batch.hpp:14-54)
+  if (!out || n_models < 0 || (n_models > 0 && !models) || n_worlds < 0 || (n_worlds > 0 && (!world_model || n_models == 0)))
     return fail(KD_ERR_INVALID_ARGUMENT, "invalid arguments");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)

@@ -194,9 +194,9 @@ def sphere_pile(n_spheres=100, radius=0.05, mu=0.5, seed=7) -> SceneDescription:
     return b.scene()
 
 
-def box_pile(n_boxes=64, half=0.05, mu=0.5, seed=11) -> SceneDescription:
+def box_pile(n_boxes=64, half=0.05, mu=0.5, seed=11, gap=0.02) -> SceneDescription:
     """Config 5 as written (BASELINE.json configs[4]): a pile of boxes in a bin
-    of five world planes.  Needs the opt-in box-box extension
+    of five world planes (`gap` between neighbours in a layer).  Needs the opt-in box-box extension
     (KD_EXT_BOX_BOX; the reference rejects box-box pairs, model.cpp:56-62, so
     this scene has no reference counterpart and its parity is against the
     oracle's restatement of the same narrow phase).  Layers of side x side
@@ -206,7 +206,7 @@ def box_pile(n_boxes=64, half=0.05, mu=0.5, seed=11) -> SceneDescription:
     rng = random.Random(seed)
     b = _Builder("box_pile")
     side = int(math.ceil(math.sqrt(n_boxes / 4.0)))
-    pitch = 2.0 * half + 0.02
+    pitch = 2.0 * half + gap
     extent = side * pitch / 2.0
     m = 0.1
     k = 0
@@ -219,7 +219,7 @@ def box_pile(n_boxes=64, half=0.05, mu=0.5, seed=11) -> SceneDescription:
                 x = -extent + pitch / 2 + i * pitch + rng.uniform(-1e-3, 1e-3)
                 y = -extent + pitch / 2 + j * pitch + rng.uniform(-1e-3, 1e-3)
                 z = half + layer * (2.0 * half + 0.004)
-                yaw = rng.uniform(-0.05, 0.05)
+                yaw = rng.uniform(-0.05, 0.05) if gap > 0 else 0.0
                 name = f"b{k}"
                 b.pos[name] = [x, y, z]
                 b.root["bodies"].append({"name": name, "mass": m, "inertia": _box_inertia(m, 2 * half, 2 * half, 2 * half),

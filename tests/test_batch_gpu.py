@@ -226,3 +226,25 @@ def test_full_size_batch_equals_sampled_solo_runs(workload, nw, steps):
     d = b.diagnostics()
     assert max(d[w].kkt_momentum_inf for w in range(nw)) < 1e-5
     assert len(set(b.kernels())) == 1
+
+
+def test_empty_batch_steps_and_reports_nothing():
+    b = K.WorldBatch()
+    cfg = K.StepConfig()
+    b.step(cfg, 3)
+    p, t, tm = b.get_state()
+    assert len(p) == 0 and len(t) == 0 and len(tm) == 0
+
+
+def test_contact_capacity_overflow_is_reported():
+    """A pile whose boxes touch on every side makes more contacts than the
+    per-world capacity (8 per geom + 16 with box-box pairs): the step fails
+    with KD_ERR_CAPACITY instead of dropping contacts silently."""
+    from paper_2603_16536_b200.scenes import box_pile
+    sc = box_pile(64, gap=0.0)
+    m = K.build_model(sc)
+    b = K.WorldBatch()
+    b.add_world(m)
+    with pytest.raises(K.KaminoError) as e:
+        b.step(K.config_for(sc), 1)
+    assert "capacity" in str(e.value)
