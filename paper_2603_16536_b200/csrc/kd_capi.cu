@@ -586,6 +586,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     std::vector<uint32_t> tmap, prog, gslot, gpair;
     std::vector<int32_t> pslot;
     std::vector<uint16_t> spos;
+    std::vector<uint8_t> kmask;
     for (int i = 0; i < n_models; ++i) {
       DevSnPlan& d = dp[i];
       d = DevSnPlan{};
@@ -601,6 +602,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       d.lmask_hi = (int32_t)(uint32_t)(p.lmask >> 32);
       d.xmask_lo = (int32_t)(uint32_t)(p.xmask & 0xffffffffull);
       d.xmask_hi = (int32_t)(uint32_t)(p.xmask >> 32);
+      d.kmask_off = (int)kmask.size();
+      kmask.insert(kmask.end(), p.kmask.begin(), p.kmask.end());
       d.n_sph = p.n_sph;
       d.gram_off = (int)gram.size();
       d.n_gram = (int)p.gram.size();
@@ -661,6 +664,7 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     KD_CK(up(v.sn_slot_pos, spos));
     KD_CK(up(v.sn_prow, prow));
     KD_CK(up(v.sn_scat, scat));
+    KD_CK(up(v.sn_kmask, kmask));
   }
   for (cudaEvent_t& e : b->ev) KD_CK(cudaEventCreate(&e));
   KD_CK(cudaDeviceSynchronize());

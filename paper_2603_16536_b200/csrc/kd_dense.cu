@@ -220,11 +220,14 @@ struct DiagLT {  // transpose of a packed lower diagonal tile (upper)
 };
 
 // acc[mb][nb][h] += sum_k A(8mb+l/4, k) B(k, 8nb+2(l%4)+h), k < 32
+// kmask: the 4-wide k steps to execute (a step whose A columns are all
+// structurally zero adds exact zeros: skipping it leaves the result bitwise equal)
 template <class LA, class LB>
-__device__ __forceinline__ void mma_tile(double acc[4][4][2], const LA& la, const LB& lb) {
+__device__ __forceinline__ void mma_tile(double acc[4][4][2], const LA& la, const LB& lb, unsigned kmask = 0xffu) {
   const int lane = threadIdx.x & 31, qr = lane >> 2, qc = lane & 3;
 #pragma unroll 2
   for (int ks = 0; ks < 8; ++ks) {
+    if (!((kmask >> ks) & 1u)) continue;
     double a[4], b[4];
 #pragma unroll
     for (int mb = 0; mb < 4; ++mb) a[mb] = la(8 * mb + qr, 4 * ks + qc);
@@ -311,21 +314,21 @@ __device__ __forceinline__ void trmm_left(double* L, int k, int j, int n, int la
 }
 
 // B_ik = -L_ik * Linv_kk (in place)
-__device__ __forceinline__ void trmm_right_neg(double* L, int i, int k, int n, int lane) {
+__device__ __forceinline__ void trmm_right_neg(double* L, int i, int k, int n, int lane, unsigned km = 0xffu) {
   double acc[4][4][2];
   zero_acc(acc);
   const int ri = tile_rows(i, n);
   double* C = L + off_tile(i, k, n);
-  mma_tile(acc, OffT{C, ri}, DiagL{L + diag_tile(k, n), 32});
+  mma_tile(acc, OffT{C, ri}, DiagL{L + diag_tile(k, n), 32}, km);
   __syncwarp();
   store_off(C, ri, acc, -1.0, false);
 }
 
 // C_ij -= A_ik * X_kj
-__device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, int lane) {
+__device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, int lane, unsigned km = 0xffu) {
   double acc[4][4][2];
   zero_acc(acc);
-  mma_tile(acc, OffT{L + off_tile(i, k, n), tile_rows(i, n)}, OffT{L + off_tile(k, j, n), 32});
+  mma_tile(acc, OffT{L + off_tile(i, k, n), tile_rows(i, n)}, OffT{L + off_tile(k, j, n), 32}, km);
   store_off(L + off_tile(i, j, n), tile_rows(i, n), acc, -1.0, true);
 }
 
@@ -339,7 +342,9 @@ __device__ __forceinline__ bool mtile(unsigned long long mask, int ti, int tj) {
   return (mask >> (ti * (ti + 1) / 2 + tj)) & 1ull;
 }
 template <int NT>
-__device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, unsigned long long xmask) {
+__device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, unsigned long long xmask,
+                            const uint8_t* kmask = nullptr) {
+  auto km = [&](int i, int k) -> unsigned { return kmask ? kmask[i * (i + 1) / 2 + k] : 0xffu; };
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   auto nth_bit = [](unsigned m, int q) {  // position of the q-th set bit
@@ -360,10 +365,16 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, u
     for (int u = wid; u < nc; u += NW) trmm_left(L, kk, nth_bit(cols, u), n, lane);
     __syncthreads();
     // phase 2 (step kk): B_ij -= L_i,kk X_kk,j for i > kk, j < kk
-    for (int u = wid; u < below * nc; u += NW) gemm_sub(L, nth_bit(rows, u / nc), nth_bit(cols, u % nc), kk, n, lane);
+    for (int u = wid; u < below * nc; u += NW) {
+      const int i = nth_bit(rows, u / nc);
+      gemm_sub(L, i, nth_bit(cols, u % nc), kk, n, lane, km(i, kk));
+    }
     __syncthreads();
     // phase 3 (step kk): B_i,kk = -L_i,kk Linv_kk for i > kk
-    for (int u = wid; u < below; u += NW) trmm_right_neg(L, nth_bit(rows, u), kk, n, lane);
+    for (int u = wid; u < below; u += NW) {
+      const int i = nth_bit(rows, u);
+      trmm_right_neg(L, i, kk, n, lane, km(i, kk));
+    }
     __syncthreads();
   }
   // final step T-1: X_T-1,j = Linv B for j < T-1
@@ -679,7 +690,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
       lm = ((unsigned long long)(uint32_t)SP.lmask_hi << 32) | (uint32_t)SP.lmask_lo;
       xm = ((unsigned long long)(uint32_t)SP.xmask_hi << 32) | (uint32_t)SP.xmask_lo;
     }
-    tri_inverse<NT>(L, n, T, lm, xm);
+    tri_inverse<NT>(L, n, T, lm, xm, handoff ? bv.sn_kmask + bv.snplan[W.model].kmask_off : nullptr);
   }
   stamp(3);
 

@@ -127,7 +127,7 @@ struct DevSnPlan {
   int32_t n_sph, max_slots, smem_doubles, pad0;  // smem_doubles: per-warp footprint of K2s
   int32_t gbody_off, n_gbody, kmax, vreg;  // vreg: per-warp vector region (doubles)
   int32_t lmask_lo, lmask_hi, scat_off, n_scat;  // nonzero 32x32 tiles of L in plan order; hand-off scatter list
-  int32_t xmask_lo, xmask_hi, pad1, pad2;        // nonzero 32x32 tiles of L^-1
+  int32_t xmask_lo, xmask_hi, kmask_off, pad2;   // nonzero 32x32 tiles of L^-1; per-L-tile column-group masks
 };
 
 // Per-world indexing (prefix sums over model capacities).
@@ -247,6 +247,7 @@ struct BatchView {
   const uint16_t* sn_slot_pos;
   const int32_t* sn_prow;  // panel-row positions of every supernode
   const uint32_t* sn_scat; // hand-off scatter lists (Lv index | tile index << 16)
+  const uint8_t* sn_kmask;  // per-L-tile 4-column-group nonzero masks (36 per planned model)
   double* sn_lv;           // BE_DENSE_SN hand-off: the factor array per world
   int32_t* sn_r2p;         // BE_DENSE_SN hand-off: compact row -> position per world
 };

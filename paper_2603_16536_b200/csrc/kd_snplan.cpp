@@ -224,6 +224,13 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       p.lmask |= 1ull << ((j / 32) * (j / 32 + 1) / 2 + j / 32);
       for (int i : cs[j]) p.lmask |= 1ull << ((i / 32) * (i / 32 + 1) / 2 + j / 32);
     }
+    // column groups (4 wide, the DMMA k step) of every L tile that hold a
+    // nonzero: the L^-1 tile products skip the others (their terms are exact zeros)
+    p.kmask.assign(36, 0);
+    for (int j = 0; j < S; ++j) {
+      p.kmask[(j / 32) * (j / 32 + 1) / 2 + j / 32] |= (uint8_t)(1u << ((j % 32) / 4));
+      for (int i : cs[j]) p.kmask[(i / 32) * (i / 32 + 1) / 2 + j / 32] |= (uint8_t)(1u << ((j % 32) / 4));
+    }
     // X = L^-1: X_ij != 0 only if i is j or an elimination-tree ancestor of j
     p.xmask = 0;
     for (int j = 0; j < S; ++j)
@@ -233,6 +240,7 @@ bool build_sn_plan(const HostModel& m, SnPlanHost& p, std::string& why) {
       }
   } else {
     p.lmask = p.xmask = ~0ull;
+    p.kmask.assign(36, 0xff);
   }
   // row patterns
   std::vector<std::vector<int>> rp(S);

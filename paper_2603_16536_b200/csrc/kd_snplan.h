@@ -48,6 +48,7 @@ struct SnPlanHost {
   int vreg = 0;          // per-warp vector region (doubles)
   uint64_t lmask = 0;      // nonzero 32x32 tiles of L (tile ti(ti+1)/2 + tj), for S <= 256
   uint64_t xmask = 0;      // nonzero 32x32 tiles of X = L^-1 (same numbering)
+  std::vector<uint8_t> kmask;  // per L tile (same numbering, S <= 256): 4-column groups with a nonzero
   std::vector<int32_t> pair_slot;   // per collision pair: first contact slot, -1 if unplanned
   std::vector<uint16_t> slot_pos;   // slot -> elimination position
   std::vector<int32_t> slot_body;   // 2 per slot: (body a, body b or -1)
