@@ -58,7 +58,7 @@ class OracleModel:
     def __init__(self, scene):
         desc, keep = scene.to_ctypes()
         h = C.c_void_p()
-        _check(lib().or_model_build(C.byref(desc), C.byref(h)))
+        _check(lib().or_model_build_ex(C.byref(desc), C.c_uint32(scene.extension_bits()), C.byref(h)))
         self.handle = h
         self.scene = scene
         info = _capi.kd_model_info()
