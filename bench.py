@@ -293,11 +293,11 @@ def ncu_traffic(kernel, workload, worlds_in_launch):
 
 def make_chunks(K, torch, b, models, wmodel, W, local):
     """Split the batch's worlds into independent WorldBatches (own stream and
-    pinned host state buffers each) for the end-to-end pass: two chunks when each
-    still fills the GPU four times over, else one."""
+    pinned host state buffers each) for the end-to-end pass: up to three chunks,
+    each still filling the GPU eight times over (KD_E2E_CHUNKS overrides)."""
     p_all, t_all, tm_all = b.get_state()
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    nch = 2 if W >= 8 * nsm else 1
+    nch = int(os.environ.get("KD_E2E_CHUNKS", "0")) or min(3, max(1, W // (8 * nsm)))
     H = (W + nch - 1) // nch
     out = []
     for lo in range(0, W, H):
@@ -485,9 +485,9 @@ def main():
         e2e = {"value": total_worlds * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 8 * (b.pose_len + b.twist_len) * ws,
                "d2h_bytes_per_step": 8 * (b.pose_len + b.twist_len) * ws,
-               "what": "per step and per chunk (a WorldBatch per chunk, one stream each, two chunks when each "
-                       "fills the GPU 4x over): H2D poses+twists from pinned host memory, batch step, D2H "
-                       "poses+twists; one chunk's copies overlap the other chunk's kernels"}
+               "what": "per step and per chunk (a WorldBatch per chunk, one stream each, up to three chunks "
+                       "that each fill the GPU 8x over): H2D poses+twists from pinned host memory, batch step, "
+                       "D2H poses+twists; one chunk's copies overlap the other chunks' kernels"}
         del halves
 
     cpu = None

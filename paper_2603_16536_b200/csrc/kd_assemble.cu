@@ -181,10 +181,10 @@ __device__ __noinline__ int box_box_dev(V3 ca, const M3& Ra, const double* ha, V
 
 }  // namespace
 
-__global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams sp) {
+__global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams sp, int w0, int w1) {
   const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= bv.n_worlds) return;
+  const int w = w0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= w1) return;
   WorldStep& ws = bv.wstep[w];
   if (!bv.active[w]) {
     if (lane == 0) ws.backend = BE_NONE, ws.n_rows = -1;
@@ -734,10 +734,11 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
   }
 }
 
-void launch_assemble(const BatchView& bv, const StepParams& sp, cudaStream_t s) {
+void launch_assemble(const BatchView& bv, const StepParams& sp, cudaStream_t s, int w0, int w1) {
   const int wpb = 8;
-  const int grid = (bv.n_worlds + wpb - 1) / wpb;
-  if (grid > 0) assemble_kernel<<<grid, 32 * wpb, 0, s>>>(bv, sp);
+  if (w1 < 0) w1 = bv.n_worlds;
+  const int grid = (w1 - w0 + wpb - 1) / wpb;
+  if (grid > 0) assemble_kernel<<<grid, 32 * wpb, 0, s>>>(bv, sp, w0, w1);
 }
 
 }  // namespace kd

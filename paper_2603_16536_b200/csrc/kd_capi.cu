@@ -63,6 +63,16 @@ struct Bin {
   int count = 0;
   int32_t* d_worlds = nullptr;
   std::vector<int32_t> worlds;
+  // the batch's parts (world ranges [cut[p], cut[p+1])): this bin's worlds in each
+  int hoff[4] = {0, 0, 0, 0}, hcount[4] = {0, 0, 0, 0};
+  void set_parts(const int* cut, int np) {
+    int k = 0;
+    for (int p = 0; p < np; ++p) {
+      hoff[p] = k;
+      while (k < (int)worlds.size() && worlds[k] < cut[p + 1]) ++k;
+      hcount[p] = k - hoff[p];
+    }
+  }
 };
 
 // dense shared-memory classes: (row capacity, threads per CTA)
@@ -77,6 +87,13 @@ constexpr int kSnAutoMaxSlots = 32;     // supernodal kernel by default up to on
 struct kd_batch {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // large batches step as independent parts (contiguous world ranges) on
+  // their own streams, so one part's kernel tails overlap the other parts'
+  // kernels; KD_SPLIT=n sets the part count (1 disables, default 2)
+  int n_halves = 1;
+  int cut[5] = {0, 0, 0, 0, 0};
+  cudaStream_t pstream[4] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[4] = {};
   std::vector<HostModel> models;
   std::vector<int32_t> world_model;
   int n_worlds = 0;
@@ -134,6 +151,11 @@ struct kd_batch {
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     drop_graph();
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    for (int p = 1; p < 4; ++p) {
+      if (ev_join[p]) cudaEventDestroy(ev_join[p]);
+      if (pstream[p]) cudaStreamDestroy(pstream[p]);
+    }
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -559,6 +581,24 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
   v.error_count = b->d_err;
   if (b->pose_len) KD_CK(cudaMemcpy(v.poses, h_pose.data(), 8 * b->pose_len, cudaMemcpyHostToDevice));
   if (b->twist_len) KD_CK(cudaMemcpy(v.twists, h_twist.data(), 8 * b->twist_len, cudaMemcpyHostToDevice));
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    const char* e = getenv("KD_SPLIT");
+    int np = e ? std::max(1, std::min(4, atoi(e))) : 2;
+    while (np > 1 && n_worlds < 8 * nsm * np) --np;  // every part still fills the GPU 8 times
+    b->n_halves = np;
+    for (int p = 0; p <= np; ++p) b->cut[p] = (int)((int64_t)n_worlds * p / np);
+    b->pstream[0] = b->stream;
+    if (np > 1) KD_CK(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+    for (int p = 1; p < np; ++p) {
+      KD_CK(cudaStreamCreateWithFlags(&b->pstream[p], cudaStreamNonBlocking));
+      KD_CK(cudaEventCreateWithFlags(&b->ev_join[p], cudaEventDisableTiming));
+    }
+  }
+  for (Bin* bin : {&b->global_bin, &b->cr_auto_bin, &b->cr_all_bin}) bin->set_parts(b->cut, b->n_halves);
+  for (Bin& bin : b->dense_bins) bin.set_parts(b->cut, b->n_halves);
+  for (auto& sbn : b->sn_bins) sbn.bin.set_parts(b->cut, b->n_halves);
   for (Bin* bin : {&b->global_bin, &b->cr_auto_bin, &b->cr_all_bin}) {
     bin->count = (int)bin->worlds.size();
     if (bin->count) {
@@ -761,7 +801,7 @@ int kd_batch_get_history(kd_batch* b, double* out) {
 
 static int resolve_timing(kd_batch* b) {
   if (b->ev_done == b->ev_used) return KD_OK;
-  KD_CK(cudaEventSynchronize(b->evpool[b->ev_used - 1]));
+  for (int p = 0; p < b->n_halves; ++p) KD_CK(cudaStreamSynchronize(b->pstream[p]));
   for (size_t k = b->ev_done; k < b->ev_used; k += 5)
     for (int i = 0; i < 4; ++i) {
       float t = 0.f;
@@ -823,51 +863,76 @@ static StepParams step_params(const kd_batch* b, const kd_step_config* c) {
 // One step's launches: K1 -> K2s bins -> K2 bins -> K2g -> K2b -> K3.
 static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& sp) {
   const BatchView& v = b->view;
-  cudaStream_t s = b->stream;
-  auto mark = [&](int i) {
-    if (b->timing) cudaEventRecord(b->evpool[b->ev_used + i], s);
-  };
-  {
-    if (b->timing) {
-      while (b->evpool.size() < b->ev_used + 5) {
-        cudaEvent_t e;
-        KD_CK(cudaEventCreate(&e));
-        b->evpool.push_back(e);
-      }
+  if (b->timing) {
+    while (b->evpool.size() < b->ev_used + 5 * (size_t)b->n_halves) {
+      cudaEvent_t e;
+      KD_CK(cudaEventCreate(&e));
+      b->evpool.push_back(e);
     }
+  }
+  if (b->n_halves > 1) {  // fork: the parts' streams wait for everything before this step
+    KD_CK(cudaEventRecord(b->ev_fork, b->stream));
+    for (int p = 1; p < b->n_halves; ++p) KD_CK(cudaStreamWaitEvent(b->pstream[p], b->ev_fork, 0));
+  }
+  for (int h = 0; h < b->n_halves; ++h) {
+    cudaStream_t s = b->pstream[h];
+    const int w0 = b->cut[h], w1 = b->cut[h + 1];
+    const size_t eb = b->ev_used + 5 * (size_t)h;
+    auto mark = [&](int i) {
+      if (b->timing) cudaEventRecord(b->evpool[eb + i], s);
+    };
+    auto part = [&](const Bin& bin, int& cnt) -> const int32_t* {
+      cnt = bin.hcount[h];
+      return bin.d_worlds + bin.hoff[h];
+    };
+    int cnt = 0;
     mark(0);
-    launch_assemble(v, sp, s);
+    launch_assemble(v, sp, s, w0, w1);
     KD_CK(cudaGetLastError());
     ++b->launches;
     mark(1);
     if (c->backend != KD_BACKEND_MATRIX_FREE) {
       for (const auto& sbn : b->sn_bins) {
-        if (sbn.hand) KD_CK(launch_snfactor(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.hand_smem, s));
-        else KD_CK(launch_sparse(v, sp, sbn.bin.d_worlds, sbn.bin.count, sbn.per_warp, sbn.wpc, sbn.prog_words, s));
+        const int32_t* wl = part(sbn.bin, cnt);
+        if (!cnt) continue;
+        if (sbn.hand) KD_CK(launch_snfactor(v, sp, wl, cnt, sbn.hand_smem, s));
+        else KD_CK(launch_sparse(v, sp, wl, cnt, sbn.per_warp, sbn.wpc, sbn.prog_words, s));
         ++b->launches;
       }
       for (const Bin& bin : b->dense_bins) {
-        KD_CK(launch_dense(v, sp, bin.d_worlds, bin.count, bin.cap, bin.nt, false, s));
+        const int32_t* wl = part(bin, cnt);
+        if (!cnt) continue;
+        KD_CK(launch_dense(v, sp, wl, cnt, bin.cap, bin.nt, false, s));
         ++b->launches;
       }
-      if (b->global_bin.count) {
-        KD_CK(launch_dense(v, sp, b->global_bin.d_worlds, b->global_bin.count, b->global_bin.cap, 256, true, s));
-        ++b->launches;
+      {
+        const int32_t* wl = part(b->global_bin, cnt);
+        if (cnt) {
+          KD_CK(launch_dense(v, sp, wl, cnt, b->global_bin.cap, 256, true, s));
+          ++b->launches;
+        }
       }
     }
     mark(2);
     const Bin& cr = c->backend == KD_BACKEND_MATRIX_FREE ? b->cr_all_bin : b->cr_auto_bin;
-    if (c->backend != KD_BACKEND_DENSE && cr.count) {
-      KD_CK(launch_cr(v, sp, cr.d_worlds, cr.count, cr.cap, cr.nbcap, cr.nt, s));
-      ++b->launches;
+    if (c->backend != KD_BACKEND_DENSE) {
+      const int32_t* wl = part(cr, cnt);
+      if (cnt) {
+        KD_CK(launch_cr(v, sp, wl, cnt, cr.cap, cr.nbcap, cr.nt, s));
+        ++b->launches;
+      }
     }
     mark(3);
-    launch_recover(v, sp, s);
+    launch_recover(v, sp, s, w0, w1);
     KD_CK(cudaGetLastError());
     ++b->launches;
     mark(4);
-    if (b->timing) b->ev_used += 5;  // per-family device time, resolved lazily
   }
+  for (int p = 1; p < b->n_halves; ++p) {  // join: the main stream waits for every part
+    KD_CK(cudaEventRecord(b->ev_join[p], b->pstream[p]));
+    KD_CK(cudaStreamWaitEvent(b->stream, b->ev_join[p], 0));
+  }
+  if (b->timing) b->ev_used += 5 * (size_t)b->n_halves;  // per-family device time, resolved lazily
   return KD_OK;
 }
 

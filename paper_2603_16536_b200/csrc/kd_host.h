@@ -34,7 +34,7 @@ int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err, uin
 double host_joint_coordinate(const HostModel& m, int joint, const double* poses7);
 
 // kernel launchers (one per translation unit)
-void launch_assemble(const BatchView& bv, const StepParams& sp, cudaStream_t s);
+void launch_assemble(const BatchView& bv, const StepParams& sp, cudaStream_t s, int w0 = 0, int w1 = -1);
 cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int cap, int nt,
                   bool global_l, cudaStream_t s);
 cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
@@ -47,7 +47,7 @@ size_t snfactor_smem_bytes(int nLv, int S);
 cudaError_t launch_fk(const BatchView& bv, const int32_t* tj, const double* tv, int nt, double tol, int max_iters,
                       double lm0, int32_t* iters, double* res, uint8_t* conv, size_t smem, cudaStream_t s);
 size_t fk_smem_bytes(int nb, int nr);
-void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s);
+void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s, int w0 = 0, int w1 = -1);
 size_t dense_smem_bytes(int n, int nt, bool global_l);
 size_t dense_factor_doubles(int n);
 size_t cr_smem_bytes(int n, int nb, int nt);

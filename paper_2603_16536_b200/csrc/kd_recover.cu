@@ -11,10 +11,10 @@
 
 namespace kd {
 
-__global__ void __launch_bounds__(256) recover_kernel(BatchView bv, StepParams sp) {
+__global__ void __launch_bounds__(256) recover_kernel(BatchView bv, StepParams sp, int w0, int w1) {
   const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= bv.n_worlds) return;
+  const int w = w0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= w1) return;
   if (!bv.active[w]) return;
   WorldStep& ws = bv.wstep[w];
   const DevWorld W = bv.worlds[w];
@@ -153,10 +153,11 @@ __global__ void __launch_bounds__(256) recover_kernel(BatchView bv, StepParams s
   }
 }
 
-void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s) {
+void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s, int w0, int w1) {
   const int wpb = 8;
-  const int grid = (bv.n_worlds + wpb - 1) / wpb;
-  if (grid > 0) recover_kernel<<<grid, 32 * wpb, 0, s>>>(bv, sp);
+  if (w1 < 0) w1 = bv.n_worlds;
+  const int grid = (w1 - w0 + wpb - 1) / wpb;
+  if (grid > 0) recover_kernel<<<grid, 32 * wpb, 0, s>>>(bv, sp, w0, w1);
 }
 
 }  // namespace kd
