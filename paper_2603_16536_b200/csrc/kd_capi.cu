@@ -799,15 +799,30 @@ int kd_batch_get_history(kd_batch* b, double* out) {
   return KD_OK;
 }
 
+// Per step and kernel family: the span from the family's first start to its
+// last end over the batch's parts (parts overlap in time, so a family's span is
+// its active wall time; with one part it is the family's own duration).  Part
+// 0's first mark precedes the fork, so every other event follows it.
 static int resolve_timing(kd_batch* b) {
   if (b->ev_done == b->ev_used) return KD_OK;
   for (int p = 0; p < b->n_halves; ++p) KD_CK(cudaStreamSynchronize(b->pstream[p]));
-  for (size_t k = b->ev_done; k < b->ev_used; k += 5)
+  const size_t per = 5 * (size_t)b->n_halves;
+  for (size_t k = b->ev_done; k < b->ev_used; k += per) {
+    float t[4][5];
+    for (int p = 0; p < b->n_halves; ++p)
+      for (int i = 0; i < 5; ++i) {
+        t[p][i] = 0.f;
+        if (p || i) KD_CK(cudaEventElapsedTime(&t[p][i], b->evpool[k], b->evpool[k + 5 * p + i]));
+      }
     for (int i = 0; i < 4; ++i) {
-      float t = 0.f;
-      KD_CK(cudaEventElapsedTime(&t, b->evpool[k + i], b->evpool[k + i + 1]));
-      b->ms[i] += t;
+      float lo = t[0][i], hi = t[0][i + 1];
+      for (int p = 1; p < b->n_halves; ++p) {
+        lo = std::min(lo, t[p][i]);
+        hi = std::max(hi, t[p][i + 1]);
+      }
+      b->ms[i] += hi - lo;
     }
+  }
   b->ev_done = b->ev_used = 0;
   return KD_OK;
 }
@@ -870,6 +885,7 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
       b->evpool.push_back(e);
     }
   }
+  if (b->timing) KD_CK(cudaEventRecord(b->evpool[b->ev_used], b->stream));  // part 0's mark 0, before the fork
   if (b->n_halves > 1) {  // fork: the parts' streams wait for everything before this step
     KD_CK(cudaEventRecord(b->ev_fork, b->stream));
     for (int p = 1; p < b->n_halves; ++p) KD_CK(cudaStreamWaitEvent(b->pstream[p], b->ev_fork, 0));
@@ -886,7 +902,7 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
       return bin.d_worlds + bin.hoff[h];
     };
     int cnt = 0;
-    mark(0);
+    if (h) mark(0);
     launch_assemble(v, sp, s, w0, w1);
     KD_CK(cudaGetLastError());
     ++b->launches;
