@@ -291,13 +291,17 @@ def ncu_traffic(kernel, workload, worlds_in_launch):
         return None, None, None
 
 
-def make_chunks(K, torch, b, models, wmodel, W, local):
+def make_chunks(K, torch, b, models, wmodel, W, local, workload):
     """Split the batch's worlds into independent WorldBatches (own stream and
     pinned host state buffers each) for the end-to-end pass: up to three chunks,
-    each still filling the GPU eight times over (KD_E2E_CHUNKS overrides)."""
+    each still filling the GPU eight times over, for the many-kernel dense
+    workloads; one batch (which steps as two parts internally when large) for
+    the matrix-free workloads, whose long CR kernels overlap their own copies
+    best that way (measured); KD_E2E_CHUNKS overrides."""
     p_all, t_all, tm_all = b.get_state()
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    nch = int(os.environ.get("KD_E2E_CHUNKS", "0")) or min(3, max(1, W // (8 * nsm)))
+    cr_workload = workload in ("closed_chain", "sphere_pile", "box_pile")
+    nch = int(os.environ.get("KD_E2E_CHUNKS", "0")) or (1 if cr_workload else min(3, max(1, W // (8 * nsm))))
     H = (W + nch - 1) // nch
     out = []
     for lo in range(0, W, H):
@@ -339,7 +343,7 @@ def main():
     # stepped through the same settle/warm-up, so the e2e pass times exactly the
     # trajectory segment (and warm-start caches) of the device-timed pass
     # (worlds are independent; results do not depend on the batch split)
-    chunks = [] if args.no_e2e else make_chunks(K, torch, b, models, wmodel, W, local)
+    chunks = [] if args.no_e2e else make_chunks(K, torch, b, models, wmodel, W, local, args.workload)
     # settle + warm-up (untimed)
     for bb in [b] + [c[0] for c in chunks]:
         bb.step(cfg, args.settle)
@@ -485,9 +489,10 @@ def main():
         e2e = {"value": total_worlds * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 8 * (b.pose_len + b.twist_len) * ws,
                "d2h_bytes_per_step": 8 * (b.pose_len + b.twist_len) * ws,
-               "what": "per step and per chunk (a WorldBatch per chunk, one stream each, up to three chunks "
-                       "that each fill the GPU 8x over): H2D poses+twists from pinned host memory, batch step, "
-                       "D2H poses+twists; one chunk's copies overlap the other chunks' kernels"}
+               "what": "per step and per chunk (a WorldBatch per chunk, one stream each; up to three chunks "
+                       "that each fill the GPU 8x over for the dense workloads, one for the matrix-free ones): "
+                       "H2D poses+twists from pinned host memory, batch step, D2H poses+twists; one chunk's "
+                       "copies overlap the other chunks' kernels"}
         del halves
 
     cpu = None
