@@ -586,7 +586,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     const char* e = getenv("KD_SPLIT");
     int np = e ? std::max(1, std::min(4, atoi(e))) : 2;
-    while (np > 1 && n_worlds < 8 * nsm * np) --np;  // every part still fills the GPU 8 times
+    const char* em = getenv("KD_SPLIT_MIN");  // worlds per part at least (default 8 per SM)
+    const int per = em ? std::max(1, atoi(em)) : 8 * nsm;
+    while (np > 1 && n_worlds < per * np) --np;  // every part still fills the GPU
     b->n_halves = np;
     for (int p = 0; p <= np; ++p) b->cut[p] = (int)((int64_t)n_worlds * p / np);
     b->pstream[0] = b->stream;
