@@ -152,23 +152,26 @@ __device__ __noinline__ int box_box_dev(V3 ca, const M3& Ra, const double* ha, V
     for (int q = 0; q < np; ++q)
       if ((hits >> q & 1) && (first < 0 || dep[q] > dep[first])) first = q;
     int pick = 1 << first;
+    // md[q]: squared distance from q to the nearest picked point, updated per
+    // pick (the same minimum the oracle recomputes over the picked set)
+    double md[8];
+    for (int q = 0; q < np; ++q) {
+      const V3 dv = sub(poly[q], poly[first]);
+      md[q] = dot(dv, dv);
+    }
     for (int r = 1; r < 4; ++r) {
       int bq = -1;
       double bd = -1.0;
-      for (int q = 0; q < np; ++q) {
-        if (!(hits >> q & 1)) continue;
-        double md = 1e300;
-        for (int pq = 0; pq < np; ++pq) {
-          if (!(pick >> pq & 1)) continue;
-          const V3 dv = sub(poly[q], poly[pq]);
-          md = fmin(md, dot(dv, dv));
-        }
-        if (md > bd) {
-          bd = md;
+      for (int q = 0; q < np; ++q)
+        if ((hits >> q & 1) && md[q] > bd) {
+          bd = md[q];
           bq = q;
         }
-      }
       pick |= 1 << bq;
+      for (int q = 0; q < np; ++q) {
+        const V3 dv = sub(poly[q], poly[bq]);
+        md[q] = fmin(md[q], dot(dv, dv));
+      }
     }
     hits = pick;
   }
