@@ -542,8 +542,15 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
       // candidates (dist, entry, contact) within tolerance 1e-3
       double cd[16];
       int ce[16], cc[16], ncand = 0;
-      for (int e = 0; e < ncache; ++e) {
-        if (cache[e].ga != cp.ga || cache[e].gb != cp.gb) continue;
+      // the pair's entries: the cache is sorted by pair index (K3 writes it in
+      // contact order), so bisect to the first one (same candidates, same order)
+      int e0 = 0, e1 = ncache;
+      while (e0 < e1) {
+        const int mid = (e0 + e1) >> 1;
+        if (cache[mid].pair < cp.pair) e0 = mid + 1;
+        else e1 = mid;
+      }
+      for (int e = e0; e < ncache && cache[e].pair == cp.pair; ++e) {
         for (int k = 0; k < gsize; ++k) {
           const double dd = norm(sub(ld3(cache[e].pos), ld3(ct[c + k].pos)));
           if (dd <= 1e-3 && ncand < 16) {

@@ -174,7 +174,7 @@ struct Contact {
 };
 
 struct CacheEntry {
-  int32_t ga, gb, pad0, pad1;
+  int32_t ga, gb, pair, pad1;  // pair: index in the model's pair list (the cache is sorted by it)
   double pos[3], imp[3], dual[3];
 };
 

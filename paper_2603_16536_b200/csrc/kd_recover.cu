@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(256) recover_kernel(BatchView bv, StepParams s
       const int r = first_contact + 3 * c;
       e.ga = cp.ga;
       e.gb = cp.gb;
+      e.pair = cp.pair;  // the cache stays sorted by pair (contact order): K1 finds a pair's entries by bisection
       for (int d = 0; d < 3; ++d) {
         e.pos[d] = cp.pos[d];
         e.imp[d] = imp[r + d];
