@@ -1092,7 +1092,8 @@ static cudaError_t launch_cr_op_p(const BatchView& bv, const StepParams& sp, con
 static int cr_reg_mode();
 
 // KD_CR_REG: 0 = shared-memory kernel only, 1 (default) = incidence-owner then
-// register-row kernels, 2 = the same with phase clocks, 3 = register-row only
+// register-row kernels, 2 = the same with phase clocks, 3 = register-row only,
+// 4 = the 512-thread incidence-owner launch for 513..1024-row bins
 template <int NT, int RPT, int MINB>
 static cudaError_t launch_cr_reg_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
                                    int ncap, int nbcap, cudaStream_t s) {
@@ -1127,7 +1128,7 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
   // shared-memory kernel for the rest (both launched over the bin; each skips
   // the other's worlds)
   int n_reg = 0;
-  if (cr_reg_mode() && cr_common_bytes(std::min(ncap, 1024), 512) + RegOp<512, 2, false>::smem_bytes(std::min(ncap, 1024), nbcap) <= 232448) {
+  if (cr_reg_mode() && cr_common_bytes(std::min(ncap, 1024), 512) + RegOp<256, 4, false>::smem_bytes(std::min(ncap, 1024), nbcap) <= 232448) {
     cudaError_t e;
     if (ncap <= 256) {
       n_reg = 256;
@@ -1136,8 +1137,16 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
       n_reg = 512;
       e = launch_cr_reg_t<256, 2, 2>(bv, sp, worlds, count, ncap, nbcap, s);
     } else {
+      // 513..1024 rows: row owners with four rows each on 256 threads, one CTA
+      // per SM (254 registers, no spills).  Measured against the 512-thread
+      // incidence-owner launch: box pile 173k -> 227k, sphere pile 25.5k ->
+      // 26.8k world-steps/s (half the warps per barrier and block reduction).
+      // KD_CR_REG=4 restores the 512-thread launch.
       n_reg = 1024;
-      e = launch_cr_reg_t<512, 2, 1>(bv, sp, worlds, count, ncap, nbcap, s);
+      if (cr_reg_mode() == 4) e = launch_cr_reg_t<512, 2, 1>(bv, sp, worlds, count, ncap, nbcap, s);
+      else if (cr_reg_mode() == 2)
+        e = launch_cr_op_p<RegOp<256, 4, true>, 256, 4, 1, true, false>(bv, sp, worlds, count, ncap, nbcap, 0, s);
+      else e = launch_cr_op_p<RegOp<256, 4, false>, 256, 4, 1, false, false>(bv, sp, worlds, count, ncap, nbcap, 0, s);
     }
     if (e != cudaSuccess) return e;
     if (ncap <= n_reg) return cudaSuccess;
