@@ -30,7 +30,7 @@ __device__ __forceinline__ int pad2(int x) { return (x + 1) & ~1; }
 
 }  // namespace
 
-__global__ void __launch_bounds__(256, 1) sparse_kernel(BatchView bv, StepParams sp, const int32_t* worlds, int count,
+__global__ void __launch_bounds__(256, 3) sparse_kernel(BatchView bv, StepParams sp, const int32_t* worlds, int count,
                                                         int per_warp, int prog_words) {
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
