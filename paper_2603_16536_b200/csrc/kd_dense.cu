@@ -546,9 +546,18 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     const DevSnPlan SP = bv.snplan[W.model];
     const double* lv = bv.sn_lv + W.snlv_off;
     const uint32_t* sc = bv.sn_scat + SP.scat_off;
-    for (int e = tid; e < SP.n_scat; e += NT) {
-      const uint32_t q = sc[e];
-      L[q >> 16] = lv[q & 0xffff];
+    // eight entries per thread and pass: all index loads, then all value loads,
+    // then the stores (the two dependent L2 round trips overlap across entries)
+    for (int e0 = tid; e0 < SP.n_scat; e0 += 8 * NT) {
+      uint32_t q[8];
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) q[k] = e0 + k * NT < SP.n_scat ? __ldg(sc + e0 + k * NT) : 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = q[k] != 0xffffffffu ? lv[q[k] & 0xffff] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (q[k] != 0xffffffffu) L[q[k] >> 16] = v[k];
     }
     __syncthreads();
     for (int k = wid; k < T; k += NW) diag_invert_rinv(L + diag_tile(k, n), tile_rows(k, n), lane);
