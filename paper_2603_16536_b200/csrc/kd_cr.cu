@@ -1137,16 +1137,23 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
       n_reg = 512;
       e = launch_cr_reg_t<256, 2, 2>(bv, sp, worlds, count, ncap, nbcap, s);
     } else {
-      // 513..1024 rows: row owners with four rows each on 256 threads, one CTA
-      // per SM (254 registers, no spills).  Measured against the 512-thread
-      // incidence-owner launch: box pile 173k -> 227k, sphere pile 25.5k ->
-      // 26.8k world-steps/s (half the warps per barrier and block reduction).
-      // KD_CR_REG=4 restores the 512-thread launch.
+      // 513..1024 rows: 256 threads with four rows each, one CTA per SM:
+      // incidence owners with pieces of <= 8 incidences (254 registers, no
+      // spills), row owners for the worlds whose bodies do not fit the lanes.
+      // Measured against the 512-thread incidence-owner launch: sphere pile
+      // 25.5k -> 33.4k, box pile 173k -> 217k world-steps/s (226k with row
+      // owners alone, KD_CR_REG=3); KD_CR_REG=4 restores the 512-thread launch.
       n_reg = 1024;
       if (cr_reg_mode() == 4) e = launch_cr_reg_t<512, 2, 1>(bv, sp, worlds, count, ncap, nbcap, s);
       else if (cr_reg_mode() == 2)
         e = launch_cr_op_p<RegOp<256, 4, true>, 256, 4, 1, true, false>(bv, sp, worlds, count, ncap, nbcap, 0, s);
-      else e = launch_cr_op_p<RegOp<256, 4, false>, 256, 4, 1, false, false>(bv, sp, worlds, count, ncap, nbcap, 0, s);
+      else if (cr_reg_mode() == 3)
+        e = launch_cr_op_p<RegOp<256, 4, false>, 256, 4, 1, false, false>(bv, sp, worlds, count, ncap, nbcap, 0, s);
+      else {
+        e = launch_cr_op_p<IncOp<256, 4, 8, false>, 256, 4, 1, false, true>(bv, sp, worlds, count, ncap, nbcap, 0, s);
+        if (e == cudaSuccess)
+          e = launch_cr_op_p<RegOp<256, 4, false>, 256, 4, 1, false, false>(bv, sp, worlds, count, ncap, nbcap, 1, s);
+      }
     }
     if (e != cudaSuccess) return e;
     if (ncap <= n_reg) return cudaSuccess;
