@@ -1,4 +1,5 @@
-"""Small fixed workload for ncu captures (DR-Legs, 148 worlds = one CTA per SM)."""
+"""Small fixed workload for ncu captures (DR-Legs, 148 worlds = one CTA per SM;
+argv[3] = fourbar for the bundled four-bar)."""
 import os
 import sys
 
@@ -8,7 +9,13 @@ from paper_2603_16536_b200.scenes import dr_legs  # noqa: E402
 
 nw = int(sys.argv[1]) if len(sys.argv) > 1 else 148
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-sc = dr_legs()
+if len(sys.argv) > 3 and sys.argv[3] == "fourbar":
+    import json
+    from paper_2603_16536_b200.scene import parse_scene_obj
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sc = parse_scene_obj(json.load(open(os.path.join(root, "tests", "golden", "scenes_bundle.json")))["fourbar"], "fourbar")
+else:
+    sc = dr_legs()
 cfg = K.config_for(sc)
 m = K.build_model(sc)
 b = K.WorldBatch()
