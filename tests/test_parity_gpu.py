@@ -246,9 +246,12 @@ def test_cr_kernel_paths_vs_oracle(cells, steps):
     assert np.abs(pg - po).max() < 1e-7 and np.abs(tg - to).max() < 1e-5
 
 
-def test_cr_incidence_vs_rows_kernels():
+@pytest.mark.parametrize("scene_expr", ["closed_chain(22)", "sphere_pile(100)"])
+def test_cr_incidence_vs_rows_kernels(scene_expr):
     """The incidence-owner and row-owner kernels on the same states (the
-    second via KD_CR_REG=3 in a subprocess): impulses within 1e-9 relative."""
+    second via KD_CR_REG=3 in a subprocess): impulses within 1e-9 relative.
+    closed_chain(22): 440 rows, 256 x 2 launch; sphere_pile(100): 780 rows,
+    256 x 4 launch with pieces of up to 8 incidences."""
     import json
     import os
     import subprocess
@@ -258,8 +261,8 @@ import json, sys
 sys.path.insert(0, sys.argv[1])
 import numpy as np
 import paper_2603_16536_b200 as K
-from paper_2603_16536_b200.scenes import closed_chain
-sc = closed_chain(22)
+from paper_2603_16536_b200.scenes import closed_chain, sphere_pile
+sc = eval(sys.argv[2])
 cfg = K.config_for(sc)
 m = K.build_model(sc)
 b = K.WorldBatch()
@@ -276,9 +279,33 @@ print(json.dumps({"paths": b.cr_paths(), "imp": b.impulses().tolist(),
     out = {}
     for mode in ("1", "3"):
         env = dict(os.environ, KD_CR_REG=mode)
-        r = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, check=True)
+        r = subprocess.run([sys.executable, "-c", code, root, scene_expr], env=env, capture_output=True, text=True,
+                           check=True)
         out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
     assert set(out["1"]["paths"]) == {"incidence"} and set(out["3"]["paths"]) == {"rows"}
     assert out["1"]["it"] == out["3"]["it"]
     a, b = np.array(out["1"]["imp"]), np.array(out["3"]["imp"])
     assert np.abs(a - b).max() <= 1e-9 * max(1.0, np.abs(b).max())
+
+
+def test_sphere_pile_768_row_path_vs_oracle():
+    """The 513..1024-row CR launch (incidence owners, 256 x 4) on the full
+    100-sphere pile against the oracle: contact order bit-exact, the same row
+    counts and PADMM iteration counts, poses after 3 steps within 1e-9."""
+    sc = sphere_pile(100)
+    cfg = K.config_for(sc)
+    gb, ob = pair(sc)
+    ob.set_trace(True)
+    for _ in range(3):
+        gb.step(cfg)
+        ob.step(cfg)
+        cg, _ = gb.dump_contacts(0)
+        co, _ = ob.dump_contacts(0)
+        assert cg.shape == co.shape and (cg == co).all()
+        dg, do = gb.diagnostics()[0], ob.diagnostics()[0]
+        assert dg.n_rows == do.n_rows > 512
+        assert dg.iterations == do.iterations
+    assert gb.cr_paths() == ["incidence"]
+    pg, _, _ = gb.get_state()
+    po, _, _ = ob.get_state()
+    assert np.abs(pg - po).max() < 1e-9
