@@ -178,6 +178,16 @@ int kd_model_build(const kd_scene_desc* scene, kd_model** out);
 #define KD_EXT_BOX_BOX 1u
 int kd_model_build_ex(const kd_scene_desc* scene, uint32_t extensions, kd_model** out);
 void kd_model_destroy(kd_model* model);
+/* Contacts a world of this model can hold per step (batches created after the
+ * call).  Default: min(max_contacts, 6 n_geoms + 16), 8 n_geoms + 16 with
+ * box-box pairs.  The reference's collide() is unbounded (contacts.cpp:119-145)
+ * but can never produce more than kd_model_info.max_contacts (1 per sphere
+ * pair, 4 per box pair), so capacity = max_contacts reproduces it exactly at
+ * the cost of row storage.  A step whose contacts overflow the capacity
+ * returns KD_ERR_CAPACITY from kd_batch_step / kd_batch_sync; the overflowing
+ * world's state and caches are left unchanged, the other worlds step.
+ * capacity <= 0 restores the default; larger values are clamped to max_contacts. */
+int kd_model_set_contact_capacity(kd_model* model, int32_t capacity);
 int kd_model_get_info(const kd_model* model, kd_model_info* out);
 /* JointLayout (model.hpp:63-74): per joint row_offset,row_count,dyn_offset,dyn_count */
 int kd_model_joint_layout(const kd_model* model, int32_t* row_offset, int32_t* row_count,
@@ -251,6 +261,41 @@ int kd_batch_get_impulses(kd_batch* batch, double* out);
  * before stepping; out is [n_worlds][capacity], unused tail = -1. */
 int kd_batch_set_history_capacity(kd_batch* batch, int32_t capacity);
 int kd_batch_get_history(kd_batch* batch, double* out);
+
+/* ---- warm-start caches (WorldState caches, stepper.hpp:38-56; contacts.hpp:32-38) */
+/* LimitReactionCache entry: key (joint, bound) -> (lambda, z), physical scale. */
+typedef struct kd_limit_cache_entry {
+  int32_t joint, bound;
+  double lambda, z;
+} kd_limit_cache_entry;
+/* ReactionCacheEntry (contacts.hpp:32-38): impulse and dual in the contact frame. */
+typedef struct kd_contact_cache_entry {
+  int32_t geom_a, geom_b;
+  double position[3];
+  double impulse[3];
+  double dual[3];
+} kd_contact_cache_entry;
+/* Sizes of world w's caches: joint_len = n_bilateral + n_dynamics rows,
+ * joint_valid (JointReactionCache::valid), the number of limit entries and of
+ * contact entries. */
+int kd_batch_get_cache_sizes(kd_batch* batch, int32_t world, int32_t* joint_len, int32_t* joint_valid,
+                             int32_t* n_limits, int32_t* n_contacts);
+/* extract_state's cache part (batch.cpp:42-44): joint lambda / z (joint_len
+ * doubles each), limit entries in (joint, bound) order (std::map order) and
+ * contact entries in contact order.  Capacities too small -> KD_ERR_CAPACITY. */
+int kd_batch_get_caches(kd_batch* batch, int32_t world, double* joint_lambda, double* joint_z,
+                        int32_t* joint_valid, kd_limit_cache_entry* limits, int32_t limit_capacity,
+                        int32_t* n_limits, kd_contact_cache_entry* contacts, int32_t contact_capacity,
+                        int32_t* n_contacts);
+/* insert_state's cache part (batch.cpp:68-70).  The joint cache is used only
+ * if joint_len equals the world's n_bilateral + n_dynamics (gather_warmstart,
+ * stepper.cpp:25).  Limit keys of joints without limits and contact entries
+ * whose (geom_a, geom_b) is not a collision pair of the model can never match
+ * a row, so they are dropped.  More contact entries than the world's contact
+ * capacity -> KD_ERR_CAPACITY. */
+int kd_batch_set_caches(kd_batch* batch, int32_t world, const double* joint_lambda, const double* joint_z,
+                        int32_t joint_len, int32_t joint_valid, const kd_limit_cache_entry* limits,
+                        int32_t n_limits, const kd_contact_cache_entry* contacts, int32_t n_contacts);
 
 /* ---- one-step introspection for parity (ConstraintSet constraints.hpp:39-65) -- */
 typedef struct kd_row_dump {
@@ -330,8 +375,9 @@ int kd_model_sparse_plan_selftest(const kd_model* model, uint64_t seed, double* 
 const char* kd_last_error(void);
 const char* kd_version(void);
 /* ABI self-check: writes sizeof of kd_body_desc, kd_joint_desc, kd_geom_desc,
- * kd_scene_desc, kd_step_config, kd_step_diag, kd_model_info, kd_row_dump
- * (in that order) into out[0..7]; returns the count written. */
+ * kd_scene_desc, kd_step_config, kd_step_diag, kd_model_info, kd_row_dump,
+ * kd_limit_cache_entry and kd_contact_cache_entry, in that order, into
+ * out[0..9]; returns the count written (at most capacity). */
 int kd_abi_sizes(int32_t* out, int32_t capacity);
 
 #ifdef __cplusplus

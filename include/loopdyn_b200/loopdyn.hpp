@@ -25,6 +25,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -290,10 +291,28 @@ struct StepDiagnostics {
   std::vector<double> impulses;
   double f_inf = 0, kkt_momentum_inf = 0, bilateral_velocity_inf = 0;
 };
+// Warm-start caches (stepper.hpp:38-47, contacts.hpp:32-38), physical scale.
+struct JointReactionCache {
+  std::vector<double> lambda, z;
+  bool valid = false;
+};
+struct LimitReactionCache {
+  std::map<std::pair<int, int>, std::pair<double, double>> entries;  // (joint, bound) -> (lambda, z)
+};
+struct ReactionCacheEntry {
+  int geom_a = -1, geom_b = -1;
+  std::array<double, 3> position{}, impulse{}, dual{};  // impulse / dual in the contact frame (n, t1, t2)
+};
+struct ReactionCache {
+  std::vector<ReactionCacheEntry> entries;
+};
 struct WorldState {
   std::vector<Pose> poses;
   std::vector<Twist> twists;
   double time = 0.0;
+  JointReactionCache joint_cache;
+  LimitReactionCache limit_cache;
+  ReactionCache contact_cache;
 };
 
 inline WorldState initial_state(const MechanismModel& m) {
@@ -342,7 +361,52 @@ class WorldBatch {
       s.twists.push_back(Twist{{t[0], t[1], t[2]}, {t[3], t[4], t[5]}});
     }
     s.time = time_[w];
+    get_caches(w, s);
     return s;
+  }
+  // extract_state's cache part (batch.cpp:42-44)
+  void get_caches(int w, WorldState& s) {
+    ensure();
+    int32_t jl = 0, jv = 0, nl = 0, nc = 0;
+    detail::check(kd_batch_get_cache_sizes(batch_.get(), w, &jl, &jv, &nl, &nc));
+    s.joint_cache.lambda.assign(jl, 0.0);
+    s.joint_cache.z.assign(jl, 0.0);
+    std::vector<kd_limit_cache_entry> lim(std::max(1, nl));
+    std::vector<kd_contact_cache_entry> con(std::max(1, nc));
+    int32_t jv2 = 0, nl2 = 0, nc2 = 0;
+    detail::check(kd_batch_get_caches(batch_.get(), w, s.joint_cache.lambda.data(), s.joint_cache.z.data(), &jv2,
+                                      lim.data(), (int32_t)lim.size(), &nl2, con.data(), (int32_t)con.size(), &nc2));
+    s.joint_cache.valid = jv2 != 0;
+    s.limit_cache.entries.clear();
+    for (int k = 0; k < nl2; ++k) s.limit_cache.entries[{lim[k].joint, lim[k].bound}] = {lim[k].lambda, lim[k].z};
+    s.contact_cache.entries.clear();
+    for (int k = 0; k < nc2; ++k) {
+      ReactionCacheEntry e;
+      e.geom_a = con[k].geom_a;
+      e.geom_b = con[k].geom_b;
+      for (int d = 0; d < 3; ++d) e.position[d] = con[k].position[d], e.impulse[d] = con[k].impulse[d],
+                                  e.dual[d] = con[k].dual[d];
+      s.contact_cache.entries.push_back(e);
+    }
+  }
+  // insert_state's cache part (batch.cpp:68-70)
+  void set_caches(int w, const WorldState& s) {
+    ensure();
+    std::vector<kd_limit_cache_entry> lim;
+    for (const auto& [key, val] : s.limit_cache.entries)
+      lim.push_back(kd_limit_cache_entry{key.first, key.second, val.first, val.second});
+    std::vector<kd_contact_cache_entry> con;
+    for (const ReactionCacheEntry& e : s.contact_cache.entries) {
+      kd_contact_cache_entry c{};
+      c.geom_a = e.geom_a;
+      c.geom_b = e.geom_b;
+      for (int d = 0; d < 3; ++d) c.position[d] = e.position[d], c.impulse[d] = e.impulse[d], c.dual[d] = e.dual[d];
+      con.push_back(c);
+    }
+    const bool jok = s.joint_cache.z.size() == s.joint_cache.lambda.size();
+    detail::check(kd_batch_set_caches(batch_.get(), w, s.joint_cache.lambda.data(), s.joint_cache.z.data(),
+                                      jok ? (int32_t)s.joint_cache.lambda.size() : -1, s.joint_cache.valid ? 1 : 0,
+                                      lim.data(), (int32_t)lim.size(), con.data(), (int32_t)con.size()));
   }
   void insert_state(int w, const WorldState& s) {
     sync_host();
@@ -355,6 +419,7 @@ class WorldBatch {
     }
     time_[w] = s.time;
     detail::check(kd_batch_set_state(batch_.get(), poses_.data(), twists_.data(), time_.data()));
+    set_caches(w, s);
   }
   void set_active(int w, bool a) {
     ensure();
@@ -441,6 +506,7 @@ class WorldBatch {
     }
     detail::check(kd_batch_set_state(b, poses_.data(), twists_.data(), time_.data()));
     host_valid_ = true;
+    for (int w = 0; w < n; ++w) set_caches(w, init_[w]);
   }
   void sync_host() {
     ensure();
@@ -471,8 +537,11 @@ inline void batch_step(WorldBatch& batch, const StepConfig& config, int n_thread
   batch.host_valid_ = false;
 }
 
-// step (stepper.hpp:84) for one world: a one-world device batch.  For many
-// worlds use WorldBatch; this exists for drop-in completeness.
+// step (stepper.hpp:84) for one world: a one-world device batch that starts
+// from `state` including its warm-start caches (gather_warmstart,
+// stepper.cpp:19-46), and writes the new state and caches back (store_caches,
+// stepper.cpp:48-70).  For many worlds use WorldBatch; this exists for drop-in
+// completeness.  `scratch` (optional) keeps the one-world batch between calls.
 inline StepDiagnostics step(const std::shared_ptr<const MechanismModel>& model, WorldState& state,
                             const StepConfig& config, WorldBatch* scratch = nullptr) {
   WorldBatch local;
@@ -482,6 +551,11 @@ inline StepDiagnostics step(const std::shared_ptr<const MechanismModel>& model, 
   batch_step(b, config);
   state = b.extract_state(0);
   return b.diagnostics(0);
+}
+// The reference signature, step(const MechanismModel&, WorldState&, const
+// StepConfig&) (stepper.hpp:84): the model is borrowed for the call.
+inline StepDiagnostics step(const MechanismModel& model, WorldState& state, const StepConfig& config) {
+  return step(std::shared_ptr<const MechanismModel>(&model, [](const MechanismModel*) {}), state, config);
 }
 
 }  // namespace loopdyn_b200

@@ -321,6 +321,40 @@ int or_batch_reset_caches(void* bp) {
   return KD_OK;
 }
 
+// extract_state's caches (batch.cpp:42-44) in the kd_batch_get_caches layout.
+int or_batch_get_caches(void* bp, int32_t w, double* jlam, double* jz, int32_t* jvalid, kd_limit_cache_entry* lim,
+                        int32_t lcap, int32_t* nl, kd_contact_cache_entry* con, int32_t ccap, int32_t* nc) {
+  OrBatch* b = static_cast<OrBatch*>(bp);
+  const WorldState s = b->batch.extract_state(w);
+  if (jvalid) *jvalid = s.joint_cache.valid ? 1 : 0;
+  for (size_t k = 0; k < s.joint_cache.lambda.size(); ++k) {
+    if (jlam) jlam[k] = s.joint_cache.lambda[k];
+    if (jz) jz[k] = s.joint_cache.z[k];
+  }
+  int k = 0;
+  for (const auto& e : s.limit_cache) {
+    if (lim && k < lcap) lim[k] = kd_limit_cache_entry{e.first.first, e.first.second, e.second.first, e.second.second};
+    ++k;
+  }
+  if (nl) *nl = k;
+  const int n = (int)s.contact_cache.size();
+  if (nc) *nc = n;
+  for (int c = 0; c < n && con && c < ccap; ++c) {
+    const ReactionCacheEntry& e = s.contact_cache[c];
+    con[c].geom_a = e.geom_a;
+    con[c].geom_b = e.geom_b;
+    const double p[3] = {e.position.x, e.position.y, e.position.z};
+    const double i3[3] = {e.impulse.x, e.impulse.y, e.impulse.z};
+    const double d3[3] = {e.dual.x, e.dual.y, e.dual.z};
+    for (int d = 0; d < 3; ++d) {
+      con[c].position[d] = p[d];
+      con[c].impulse[d] = i3[d];
+      con[c].dual[d] = d3[d];
+    }
+  }
+  return (k > lcap || n > ccap) ? KD_ERR_CAPACITY : KD_OK;
+}
+
 int or_batch_set_active(void* bp, const uint8_t* active) {
   OrBatch* b = static_cast<OrBatch*>(bp);
   for (int w = 0; w < b->batch.size(); ++w) b->batch.set_active(w, active[w] != 0);

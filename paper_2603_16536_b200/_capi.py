@@ -177,6 +177,15 @@ class kd_row_dump(C.Structure):
 
 
 # name -> (restype, argtypes); the handle type is an opaque void*.
+class kd_limit_cache_entry(C.Structure):
+    _fields_ = [("joint", C.c_int32), ("bound", C.c_int32), ("lambda_", C.c_double), ("z", C.c_double)]
+
+
+class kd_contact_cache_entry(C.Structure):
+    _fields_ = [("geom_a", C.c_int32), ("geom_b", C.c_int32), ("position", C.c_double * 3),
+                ("impulse", C.c_double * 3), ("dual", C.c_double * 3)]
+
+
 _H = C.c_void_p
 SIGNATURES = {
     "model_build": (C.c_int, [C.POINTER(kd_scene_desc), C.POINTER(C.c_void_p)]),
@@ -228,6 +237,14 @@ KD_ONLY = {
     "batch_device_state": (C.c_int, [_H, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "model_sparse_plan_info": (C.c_int, [_H, c_int64_p]),
     "model_sparse_plan_selftest": (C.c_int, [_H, C.c_uint64, c_double_p]),
+    "model_set_contact_capacity": (C.c_int, [_H, C.c_int32]),
+    "batch_get_cache_sizes": (C.c_int, [_H, C.c_int32, c_int32_p, c_int32_p, c_int32_p, c_int32_p]),
+    "batch_get_caches": (C.c_int, [_H, C.c_int32, c_double_p, c_double_p, c_int32_p,
+                                   C.POINTER(kd_limit_cache_entry), C.c_int32, c_int32_p,
+                                   C.POINTER(kd_contact_cache_entry), C.c_int32, c_int32_p]),
+    "batch_set_caches": (C.c_int, [_H, C.c_int32, c_double_p, c_double_p, C.c_int32, C.c_int32,
+                                   C.POINTER(kd_limit_cache_entry), C.c_int32,
+                                   C.POINTER(kd_contact_cache_entry), C.c_int32]),
 }
 
 

@@ -48,13 +48,30 @@ struct DevMem {
     void* p = nullptr;
     const cudaError_t e = cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T));
     if (e == cudaSuccess) {
+      // zero-fill on the legacy stream and wait for it: the batch streams are
+      // non-blocking, so nothing else would order this fill before their work
       cudaMemset(p, 0, std::max<size_t>(1, count) * sizeof(T));
+      cudaStreamSynchronize(0);
       ptrs.push_back(p);
       out = static_cast<T*>(p);
     }
     return e;
   }
+  void release(void* p) {
+    for (void*& q : ptrs)
+      if (q == p) {
+        cudaFree(q);
+        q = nullptr;
+      }
+  }
 };
+
+// Per-world dense-global slab: the factor (tile layout) followed by the PADMM
+// unit state y, z, y_hat, z_hat (4 x 32 T doubles) of dense_kernel<., true>.
+int64_t slab_doubles(int cap) {
+  const int64_t t = (cap + 31) / 32;
+  return (((int64_t)dense_factor_doubles(cap) + 1) & ~(int64_t)1) + 4 * 32 * t + 2;
+}
 
 struct Bin {
   int cap = 0;  // rows (dense) / rows (cr)
@@ -84,6 +101,12 @@ constexpr int kSnAutoMaxSlots = 32;     // supernodal kernel by default up to on
 
 }  // namespace
 
+struct kd_batch;
+namespace {
+cudaError_t to_dev(kd_batch* b, void* dst, const void* src, size_t bytes);
+cudaError_t to_host(kd_batch* b, void* dst, const void* src, size_t bytes);
+}  // namespace
+
 struct kd_batch {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -101,6 +124,11 @@ struct kd_batch {
   std::vector<int32_t> pose_off, twist_off;
   std::vector<int64_t> row_off;
   int64_t total_rows = 0, pose_len = 0, twist_len = 0, total_lslab = 0;
+  // the dense-global slab holds min(capacity, 300) rows per world (Auto never
+  // factors more); the first step with backend = Dense re-sizes it to the full
+  // row capacity of every world above 300 rows (build_backend factors densely
+  // at any n, delassus.cpp:203-216)
+  bool dense_full = false, has_big = false;
   int total_bodies = 0, total_contacts = 0, total_jcache = 0, total_lslots = 0;
   DevMem mem;
   BatchView view{};
@@ -160,17 +188,34 @@ struct kd_batch {
   }
 };
 
+namespace {
+// Host<->device copies of the batch API, ordered on the batch stream (which is
+// non-blocking, so legacy-stream cudaMemcpy would race with in-flight steps):
+// enqueue after the stream's pending work, then wait for the copy itself.
+cudaError_t to_dev(kd_batch* b, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return cudaSuccess;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, b->stream);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(b->stream);
+}
+cudaError_t to_host(kd_batch* b, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return cudaSuccess;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, b->stream);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(b->stream);
+}
+}  // namespace
+
 extern "C" {
 
 const char* kd_last_error(void) { return g_err.c_str(); }
 const char* kd_version(void) { return "kamino_b200 0.1 (sm_100a)"; }
 
 int kd_abi_sizes(int32_t* out, int32_t cap) {
-  const int32_t s[8] = {(int32_t)sizeof(kd_body_desc),   (int32_t)sizeof(kd_joint_desc),
-                        (int32_t)sizeof(kd_geom_desc),   (int32_t)sizeof(kd_scene_desc),
-                        (int32_t)sizeof(kd_step_config), (int32_t)sizeof(kd_step_diag),
-                        (int32_t)sizeof(kd_model_info),  (int32_t)sizeof(kd_row_dump)};
-  const int n = cap < 8 ? cap : 8;
+  const int32_t s[10] = {(int32_t)sizeof(kd_body_desc),   (int32_t)sizeof(kd_joint_desc),
+                         (int32_t)sizeof(kd_geom_desc),   (int32_t)sizeof(kd_scene_desc),
+                         (int32_t)sizeof(kd_step_config), (int32_t)sizeof(kd_step_diag),
+                         (int32_t)sizeof(kd_model_info),  (int32_t)sizeof(kd_row_dump),
+                         (int32_t)sizeof(kd_limit_cache_entry), (int32_t)sizeof(kd_contact_cache_entry)};
+  const int n = cap < 10 ? cap : 10;
   for (int i = 0; i < n; ++i) out[i] = s[i];
   return n;
 }
@@ -293,6 +338,12 @@ int kd_model_sparse_plan_selftest(const kd_model* mp, uint64_t seed, double* max
 
 void kd_model_destroy(kd_model* m) { delete m; }
 
+int kd_model_set_contact_capacity(kd_model* m, int32_t capacity) {
+  if (!m) return fail(KD_ERR_INVALID_ARGUMENT, "null model");
+  m->m.contact_cap = capacity > 0 ? std::min(capacity, m->m.info.max_contacts) : 0;
+  return KD_OK;
+}
+
 int kd_model_get_info(const kd_model* m, kd_model_info* out) {
   if (!m || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   *out = m->m.info;
@@ -380,7 +431,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     // pairs: face contacts carry 4 points) + 16; overflow is an error.
     bool box_box = false;
     for (const DevPair& pr : m.pairs) box_box = box_box || pr.kind == P_BOX_BOX;
-    contact_cap[i] = std::min(m.info.max_contacts, (box_box ? 8 : 6) * d.ng + 16);
+    contact_cap[i] = m.contact_cap > 0 ? std::min(m.info.max_contacts, m.contact_cap)
+                                       : std::min(m.info.max_contacts, (box_box ? 8 : 6) * d.ng + 16);
     d.max_contacts = contact_cap[i];
     row_cap[i] = d.n_bil + d.n_dyn + 2 * d.n_limited + 3 * contact_cap[i];
     d.row_cap = row_cap[i];
@@ -455,8 +507,10 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     if (rc > kSmemMaxRows) {
       W.slab_cap = std::min(rc, kDenseGlobalMaxRows);
       W.lslab_off = b->total_lslab;
-      b->total_lslab += (int64_t)dense_factor_doubles(W.slab_cap) + 2;
+      b->total_lslab += slab_doubles(W.slab_cap);
       b->global_bin.worlds.push_back(w);
+      b->global_bin.cap = std::max(b->global_bin.cap, W.slab_cap);
+      b->has_big = b->has_big || rc > kDenseGlobalMaxRows;
     }
     if (rc > kDenseGlobalMaxRows) {
       b->cr_auto_bin.worlds.push_back(w);
@@ -501,7 +555,6 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       if (world_model[w] == i) sbn.bin.worlds.push_back(w);
     if (!sbn.bin.worlds.empty()) b->sn_bins.push_back(sbn);
   }
-  b->global_bin.cap = kDenseGlobalMaxRows;
   b->global_bin.nt = 256;
   for (Bin* bin : {&b->cr_auto_bin, &b->cr_all_bin}) bin->nt = bin->cap > 256 ? 512 : (bin->cap > 128 ? 256 : 128);
   if (cr_smem_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) > 232448)
@@ -740,9 +793,9 @@ int kd_batch_offsets(const kd_batch* b, int32_t* po, int32_t* to) {
 int kd_batch_set_state(kd_batch* b, const double* poses, const double* twists, const double* time) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
   KD_CK(cudaSetDevice(b->device));
-  if (poses && b->pose_len) KD_CK(cudaMemcpy(b->view.poses, poses, 8 * b->pose_len, cudaMemcpyHostToDevice));
-  if (twists && b->twist_len) KD_CK(cudaMemcpy(b->view.twists, twists, 8 * b->twist_len, cudaMemcpyHostToDevice));
-  if (time && b->n_worlds) KD_CK(cudaMemcpy(b->view.time, time, 8 * b->n_worlds, cudaMemcpyHostToDevice));
+  if (poses && b->pose_len) KD_CK(to_dev(b, b->view.poses, poses, 8 * b->pose_len));
+  if (twists && b->twist_len) KD_CK(to_dev(b, b->view.twists, twists, 8 * b->twist_len));
+  if (time && b->n_worlds) KD_CK(to_dev(b, b->view.time, time, 8 * b->n_worlds));
   return KD_OK;
 }
 
@@ -750,9 +803,9 @@ int kd_batch_get_state(kd_batch* b, double* poses, double* twists, double* time)
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
   KD_CK(cudaSetDevice(b->device));
   KD_CK(cudaStreamSynchronize(b->stream));
-  if (poses && b->pose_len) KD_CK(cudaMemcpy(poses, b->view.poses, 8 * b->pose_len, cudaMemcpyDeviceToHost));
-  if (twists && b->twist_len) KD_CK(cudaMemcpy(twists, b->view.twists, 8 * b->twist_len, cudaMemcpyDeviceToHost));
-  if (time && b->n_worlds) KD_CK(cudaMemcpy(time, b->view.time, 8 * b->n_worlds, cudaMemcpyDeviceToHost));
+  if (poses && b->pose_len) KD_CK(to_host(b, poses, b->view.poses, 8 * b->pose_len));
+  if (twists && b->twist_len) KD_CK(to_host(b, twists, b->view.twists, 8 * b->twist_len));
+  if (time && b->n_worlds) KD_CK(to_host(b, time, b->view.time, 8 * b->n_worlds));
   return KD_OK;
 }
 
@@ -761,14 +814,17 @@ int kd_batch_reset_caches(kd_batch* b) {
   KD_CK(cudaSetDevice(b->device));
   std::vector<WorldStep> ws(b->n_worlds);
   if (b->n_worlds) {
-    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+    KD_CK(to_host(b, ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds));
     for (WorldStep& s : ws) {
       s.jcache_valid = 0;
       s.ccache_count = 0;
     }
-    KD_CK(cudaMemcpy(b->view.wstep, ws.data(), sizeof(WorldStep) * b->n_worlds, cudaMemcpyHostToDevice));
+    KD_CK(to_dev(b, b->view.wstep, ws.data(), sizeof(WorldStep) * b->n_worlds));
   }
-  if (b->total_lslots) KD_CK(cudaMemset(b->view.ls_valid, 0, 4 * b->total_lslots));
+  if (b->total_lslots) {
+    KD_CK(cudaMemsetAsync(b->view.ls_valid, 0, 4 * b->total_lslots, b->stream));
+    KD_CK(cudaStreamSynchronize(b->stream));
+  }
   return KD_OK;
 }
 
@@ -776,7 +832,7 @@ int kd_batch_set_active(kd_batch* b, const uint8_t* active) {
   if (!b || !active) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   KD_CK(cudaSetDevice(b->device));
   if (b->n_worlds)
-    KD_CK(cudaMemcpy(const_cast<uint8_t*>(b->view.active), active, b->n_worlds, cudaMemcpyHostToDevice));
+    KD_CK(to_dev(b, const_cast<uint8_t*>(b->view.active), active, b->n_worlds));
   return KD_OK;
 }
 
@@ -797,7 +853,7 @@ int kd_batch_get_history(kd_batch* b, double* out) {
   if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   KD_CK(cudaSetDevice(b->device));
   if (b->hist_cap && b->n_worlds)
-    KD_CK(cudaMemcpy(out, b->d_hist, 8 * (size_t)b->hist_cap * b->n_worlds, cudaMemcpyDeviceToHost));
+    KD_CK(to_host(b, out, b->d_hist, 8 * (size_t)b->hist_cap * b->n_worlds));
   return KD_OK;
 }
 
@@ -972,15 +1028,56 @@ static int ensure_nest_table(kd_batch* b, int max_iters) {
   }
   double* d = nullptr;
   KD_CK(b->mem.alloc(d, cap));
-  KD_CK(cudaMemcpy(d, t.data(), 8 * (size_t)cap, cudaMemcpyHostToDevice));
+  KD_CK(to_dev(b, d, t.data(), 8 * (size_t)cap));
   b->d_nest = d;
   b->nest_cap = cap;
+  return KD_OK;
+}
+
+// backend = Dense: grow the dense-global slab to every world's full row
+// capacity (once; Auto keeps using the same slab, whose worlds then have room
+// for any n <= capacity).
+static int ensure_dense_full(kd_batch* b) {
+  if (b->dense_full || !b->has_big) return KD_OK;
+  int64_t total = 0;
+  std::vector<DevWorld> W = b->worlds;
+  int cap = 0;
+  for (int w : b->global_bin.worlds) {
+    const int rcw = (int)((w + 1 < b->n_worlds ? b->row_off[w + 1] : b->total_rows) - b->row_off[w]);  // capacity
+    W[w].slab_cap = rcw;
+    W[w].lslab_off = total;
+    total += slab_doubles(rcw);
+    cap = std::max(cap, rcw);
+  }
+  double* slab = nullptr;
+  if (cudaMalloc(&slab, 8 * (size_t)std::max<int64_t>(1, total)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KD_ERR_CAPACITY, "dense backend: the factor storage of the worlds above 300 rows (" +
+                                     std::to_string(8.0 * total / 1e9) + " GB) does not fit device memory");
+  }
+  KD_CK(cudaMemsetAsync(slab, 0, 8 * (size_t)std::max<int64_t>(1, total), b->stream));
+  KD_CK(cudaStreamSynchronize(b->stream));
+  b->mem.ptrs.push_back(slab);
+  b->mem.release(b->view.lslab);
+  b->view.lslab = slab;
+  b->total_lslab = total;
+  b->worlds = W;
+  KD_CK(cudaMemcpyAsync(const_cast<DevWorld*>(b->view.worlds), W.data(), sizeof(DevWorld) * W.size(),
+                        cudaMemcpyHostToDevice, b->stream));
+  KD_CK(cudaStreamSynchronize(b->stream));
+  b->global_bin.cap = cap;
+  b->dense_full = true;
+  b->drop_graph();
   return KD_OK;
 }
 
 static int enqueue_steps(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
   const int nrc = ensure_nest_table(b, c->max_iters);
   if (nrc != KD_OK) return nrc;
+  if (c->backend == KD_BACKEND_DENSE) {
+    const int drc = ensure_dense_full(b);
+    if (drc != KD_OK) return drc;
+  }
   const StepParams sp = step_params(b, c);
   if (!b->graphs || b->timing || n_steps < 2) {
     for (int k = 0; k < n_steps; ++k) {
@@ -1028,7 +1125,7 @@ int kd_batch_sync(kd_batch* b) {
     if (rc != KD_OK) return rc;
   }
   int32_t err[4];
-  KD_CK(cudaMemcpy(err, b->d_err, 16, cudaMemcpyDeviceToHost));
+  KD_CK(to_host(b, err, b->d_err, 16));
   if (err[0]) return fail(KD_ERR_SPD_FAILURE, "Delassus factorization failed on an SPD system (" +
                                                   std::to_string(err[0]) + " worlds)");
   if (err[1]) return fail(KD_ERR_CAPACITY, "contact or dense-slab capacity exceeded in " + std::to_string(err[1]) +
@@ -1040,6 +1137,8 @@ int kd_batch_step_async(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
   if (!b || !c) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   if (b->n_worlds == 0 || n_steps <= 0) return KD_OK;
   KD_CK(cudaSetDevice(b->device));
+  // the error word covers the steps of this call only (kd_batch_sync reads it)
+  KD_CK(cudaMemsetAsync(b->d_err, 0, 16, b->stream));
   return enqueue_steps(b, c, n_steps);
 }
 
@@ -1103,10 +1202,10 @@ int kd_batch_fk(kd_batch* b, const int32_t* joints, const double* values, int32_
   }
   cudaError_t e = launch_fk(b->view, d_j, d_v, nt, tol, max_iters, lm0, d_it, d_res, d_conv, smem, b->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(b->stream);
-  if (e == cudaSuccess && iterations) e = cudaMemcpy(iterations, d_it, 4 * (size_t)b->n_worlds, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && iterations) e = to_host(b, iterations, d_it, 4 * (size_t)b->n_worlds);
   if (e == cudaSuccess && residual_inf)
-    e = cudaMemcpy(residual_inf, d_res, 8 * (size_t)b->n_worlds, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && converged) e = cudaMemcpy(converged, d_conv, (size_t)b->n_worlds, cudaMemcpyDeviceToHost);
+    e = to_host(b, residual_inf, d_res, 8 * (size_t)b->n_worlds);
+  if (e == cudaSuccess && converged) e = to_host(b, converged, d_conv, (size_t)b->n_worlds);
   if (e != cudaSuccess) rc = fail(KD_ERR_CUDA, std::string("kd_batch_fk: ") + cudaGetErrorString(e));
   cudaFree(d_j);
   cudaFree(d_v);
@@ -1118,6 +1217,7 @@ int kd_batch_fk(kd_batch* b, const int32_t* joints, const double* values, int32_
 
 int kd_batch_set_state_async(kd_batch* b, const double* poses, const double* twists) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
   if (poses && b->pose_len)
     KD_CK(cudaMemcpyAsync(b->view.poses, poses, 8 * b->pose_len, cudaMemcpyHostToDevice, b->stream));
   if (twists && b->twist_len)
@@ -1127,6 +1227,7 @@ int kd_batch_set_state_async(kd_batch* b, const double* poses, const double* twi
 
 int kd_batch_get_state_async(kd_batch* b, double* poses, double* twists) {
   if (!b) return fail(KD_ERR_INVALID_ARGUMENT, "null batch");
+  KD_CK(cudaSetDevice(b->device));
   if (poses && b->pose_len)
     KD_CK(cudaMemcpyAsync(poses, b->view.poses, 8 * b->pose_len, cudaMemcpyDeviceToHost, b->stream));
   if (twists && b->twist_len)
@@ -1139,7 +1240,7 @@ int kd_batch_get_diagnostics(kd_batch* b, kd_step_diag* out) {
   KD_CK(cudaSetDevice(b->device));
   std::vector<WorldStep> ws(b->n_worlds);
   if (b->n_worlds)
-    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+    KD_CK(to_host(b, ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds));
   for (int w = 0; w < b->n_worlds; ++w) {
     const WorldStep& s = ws[w];
     const HostModel& m = b->models[b->world_model[w]];
@@ -1169,7 +1270,7 @@ int kd_batch_get_phase_cycles(kd_batch* b, int64_t* out) {
   KD_CK(cudaSetDevice(b->device));
   std::vector<WorldStep> ws(b->n_worlds);
   if (b->n_worlds)
-    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+    KD_CK(to_host(b, ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds));
   for (int w = 0; w < b->n_worlds; ++w)
     for (int k = 0; k < 8; ++k) out[8 * w + k] = (ws[w].backend == BE_DENSE_SMEM || ws[w].backend == BE_SPARSE || ws[w].backend == BE_DENSE_SN || ws[w].backend == BE_MATRIX_FREE) ? ws[w].phase_cycles[k] : 0;
   return KD_OK;
@@ -1180,7 +1281,7 @@ int kd_batch_get_kernels(kd_batch* b, int32_t* out) {
   KD_CK(cudaSetDevice(b->device));
   std::vector<WorldStep> ws(b->n_worlds);
   if (b->n_worlds)
-    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+    KD_CK(to_host(b, ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds));
   for (int w = 0; w < b->n_worlds; ++w) {
     const int be = ws[w].backend;
     out[w] = be == BE_SPARSE ? KD_KERNEL_SUPERNODAL
@@ -1196,7 +1297,7 @@ int kd_batch_get_cr_paths(kd_batch* b, int32_t* out) {
   KD_CK(cudaSetDevice(b->device));
   std::vector<WorldStep> ws(b->n_worlds);
   if (b->n_worlds)
-    KD_CK(cudaMemcpy(ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds, cudaMemcpyDeviceToHost));
+    KD_CK(to_host(b, ws.data(), b->view.wstep, sizeof(WorldStep) * b->n_worlds));
   for (int w = 0; w < b->n_worlds; ++w)
     out[w] = ws[w].backend == BE_MATRIX_FREE ? ws[w].cr_path : KD_CR_PATH_NONE;
   return KD_OK;
@@ -1212,7 +1313,7 @@ int kd_batch_row_offsets(const kd_batch* b, int64_t* ro, int64_t* total) {
 int kd_batch_get_impulses(kd_batch* b, double* out) {
   if (!b || !out) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
   KD_CK(cudaSetDevice(b->device));
-  KD_CK(cudaMemcpy(out, b->view.imp, 8 * b->total_rows, cudaMemcpyDeviceToHost));
+  KD_CK(to_host(b, out, b->view.imp, 8 * b->total_rows));
   return KD_OK;
 }
 
@@ -1220,7 +1321,7 @@ int kd_batch_dump_rows(kd_batch* b, int32_t w, kd_row_dump* out, int32_t cap, in
   if (!b || !out || !n_rows || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
   KD_CK(cudaSetDevice(b->device));
   WorldStep s;
-  KD_CK(cudaMemcpy(&s, b->view.wstep + w, sizeof(s), cudaMemcpyDeviceToHost));
+  KD_CK(to_host(b, &s, b->view.wstep + w, sizeof(s)));
   const int n = std::max(0, s.n_rows);
   *n_rows = n;
   if (n > cap) return fail(KD_ERR_CAPACITY, "dump capacity too small");
@@ -1230,15 +1331,15 @@ int kd_batch_dump_rows(kd_batch* b, int32_t w, kd_row_dump* out, int32_t cap, in
   std::vector<int32_t> rb(2 * n), rk(n);
   std::vector<double> bias(n), reg(n), scale(n), vf(n), lam(n), zo(n);
   const BatchView& v = b->view;
-  KD_CK(cudaMemcpy(rj.data(), v.rowj + R0, sizeof(RowJ) * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(rb.data(), v.rbody + 2 * R0, 8 * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(rk.data(), v.rkind + R0, 4 * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(bias.data(), v.bias + R0, 8 * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(reg.data(), v.reg + R0, 8 * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(scale.data(), v.scale + R0, 8 * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(vf.data(), v.vf + R0, 8 * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(lam.data(), v.lam + R0, 8 * n, cudaMemcpyDeviceToHost));
-  KD_CK(cudaMemcpy(zo.data(), v.zo + R0, 8 * n, cudaMemcpyDeviceToHost));
+  KD_CK(to_host(b, rj.data(), v.rowj + R0, sizeof(RowJ) * n));
+  KD_CK(to_host(b, rb.data(), v.rbody + 2 * R0, 8 * n));
+  KD_CK(to_host(b, rk.data(), v.rkind + R0, 4 * n));
+  KD_CK(to_host(b, bias.data(), v.bias + R0, 8 * n));
+  KD_CK(to_host(b, reg.data(), v.reg + R0, 8 * n));
+  KD_CK(to_host(b, scale.data(), v.scale + R0, 8 * n));
+  KD_CK(to_host(b, vf.data(), v.vf + R0, 8 * n));
+  KD_CK(to_host(b, lam.data(), v.lam + R0, 8 * n));
+  KD_CK(to_host(b, zo.data(), v.zo + R0, 8 * n));
   for (int r = 0; r < n; ++r) {
     kd_row_dump& o = out[r];
     std::memset(&o, 0, sizeof(o));
@@ -1263,13 +1364,12 @@ int kd_batch_dump_contacts(kd_batch* b, int32_t w, int32_t* geoms, double* data9
   if (!b || !nc || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
   KD_CK(cudaSetDevice(b->device));
   WorldStep s;
-  KD_CK(cudaMemcpy(&s, b->view.wstep + w, sizeof(s), cudaMemcpyDeviceToHost));
+  KD_CK(to_host(b, &s, b->view.wstep + w, sizeof(s)));
   *nc = std::max(0, s.n_contacts);
   if (*nc > cap) return fail(KD_ERR_CAPACITY, "dump capacity too small");
   std::vector<Contact> ct(*nc);
   if (*nc)
-    KD_CK(cudaMemcpy(ct.data(), b->view.contacts + b->worlds[w].contact_off, sizeof(Contact) * *nc,
-                     cudaMemcpyDeviceToHost));
+    KD_CK(to_host(b, ct.data(), b->view.contacts + b->worlds[w].contact_off, sizeof(Contact) * *nc));
   for (int c = 0; c < *nc; ++c) {
     geoms[2 * c] = ct[c].ga;
     geoms[2 * c + 1] = ct[c].gb;
@@ -1289,12 +1389,152 @@ int kd_batch_dump_limits(kd_batch* b, int32_t w, int32_t* keys2, int32_t cap, in
   if (!b || !nl || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
   KD_CK(cudaSetDevice(b->device));
   WorldStep s;
-  KD_CK(cudaMemcpy(&s, b->view.wstep + w, sizeof(s), cudaMemcpyDeviceToHost));
+  KD_CK(to_host(b, &s, b->view.wstep + w, sizeof(s)));
   *nl = std::max(0, s.n_limits);
   if (*nl > cap) return fail(KD_ERR_CAPACITY, "dump capacity too small");
   const HostModel& m = b->models[b->world_model[w]];
   const int64_t first = b->row_off[w] + m.n_bil + m.n_dyn;
-  if (*nl) KD_CK(cudaMemcpy(keys2, b->view.lkey + 2 * first, 8 * *nl, cudaMemcpyDeviceToHost));
+  if (*nl) KD_CK(to_host(b, keys2, b->view.lkey + 2 * first, 8 * *nl));
+  return KD_OK;
+}
+
+// ---- warm-start caches (extract_state / insert_state, batch.cpp:27-72)
+int kd_batch_get_cache_sizes(kd_batch* b, int32_t w, int32_t* jl, int32_t* jv, int32_t* nl, int32_t* nc) {
+  if (!b || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
+  KD_CK(cudaSetDevice(b->device));
+  const HostModel& m = b->models[b->world_model[w]];
+  const DevWorld& W = b->worlds[w];
+  WorldStep s;
+  KD_CK(to_host(b, &s, b->view.wstep + w, sizeof(s)));
+  if (jl) *jl = m.n_bil + m.n_dyn;
+  if (jv) *jv = s.jcache_valid;
+  if (nl) {
+    std::vector<int32_t> valid(2 * (size_t)m.info.n_limited_joints);
+    if (!valid.empty()) KD_CK(to_host(b, valid.data(), b->view.ls_valid + W.lslot_off, 4 * valid.size()));
+    int k = 0;
+    for (int32_t v : valid) k += v != 0;
+    *nl = k;
+  }
+  if (nc) *nc = s.ccache_count;
+  return KD_OK;
+}
+
+int kd_batch_get_caches(kd_batch* b, int32_t w, double* jlam, double* jz, int32_t* jvalid, kd_limit_cache_entry* lim,
+                        int32_t lcap, int32_t* nl, kd_contact_cache_entry* con, int32_t ccap, int32_t* nc) {
+  if (!b || w < 0 || w >= b->n_worlds) return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
+  KD_CK(cudaSetDevice(b->device));
+  const HostModel& m = b->models[b->world_model[w]];
+  const DevWorld& W = b->worlds[w];
+  const BatchView& v = b->view;
+  WorldStep s;
+  KD_CK(to_host(b, &s, v.wstep + w, sizeof(s)));
+  const int njd = m.n_bil + m.n_dyn;
+  if (jvalid) *jvalid = s.jcache_valid;
+  if (jlam && njd) KD_CK(to_host(b, jlam, v.jc_lam + W.jcache_off, 8 * (size_t)njd));
+  if (jz && njd) KD_CK(to_host(b, jz, v.jc_z + W.jcache_off, 8 * (size_t)njd));
+  // limit slots 2 * limit_slot + bound, listed in (joint, bound) order
+  const int nls = 2 * m.info.n_limited_joints;
+  std::vector<int32_t> valid(nls);
+  std::vector<double> ll(nls), lz(nls);
+  if (nls) {
+    KD_CK(to_host(b, valid.data(), v.ls_valid + W.lslot_off, 4 * (size_t)nls));
+    KD_CK(to_host(b, ll.data(), v.ls_lam + W.lslot_off, 8 * (size_t)nls));
+    KD_CK(to_host(b, lz.data(), v.ls_z + W.lslot_off, 8 * (size_t)nls));
+  }
+  int k = 0;
+  for (size_t j = 0; j < m.joints.size(); ++j) {
+    if (!(m.joints[j].flags & JF_LIMITS)) continue;
+    for (int bound = 0; bound < 2; ++bound) {
+      const int slot = 2 * m.joints[j].limit_slot + bound;
+      if (!valid[slot]) continue;
+      if (lim && k < lcap) lim[k] = kd_limit_cache_entry{(int32_t)j, bound, ll[slot], lz[slot]};
+      ++k;
+    }
+  }
+  if (nl) *nl = k;
+  if (lim && k > lcap) return fail(KD_ERR_CAPACITY, "limit cache capacity too small");
+  const int n = s.ccache_count;
+  if (nc) *nc = n;
+  if (con && n > ccap) return fail(KD_ERR_CAPACITY, "contact cache capacity too small");
+  if (con && n) {
+    std::vector<CacheEntry> ce(n);
+    KD_CK(to_host(b, ce.data(), v.ccache + W.contact_off, sizeof(CacheEntry) * n));
+    for (int c = 0; c < n; ++c) {
+      kd_contact_cache_entry& o = con[c];
+      o.geom_a = ce[c].ga;
+      o.geom_b = ce[c].gb;
+      for (int d = 0; d < 3; ++d) {
+        o.position[d] = ce[c].pos[d];
+        o.impulse[d] = ce[c].imp[d];
+        o.dual[d] = ce[c].dual[d];
+      }
+    }
+  }
+  return KD_OK;
+}
+
+int kd_batch_set_caches(kd_batch* b, int32_t w, const double* jlam, const double* jz, int32_t jlen, int32_t jvalid,
+                        const kd_limit_cache_entry* lim, int32_t nlim, const kd_contact_cache_entry* con,
+                        int32_t ncon) {
+  if (!b || w < 0 || w >= b->n_worlds || nlim < 0 || ncon < 0 || (nlim && !lim) || (ncon && !con))
+    return fail(KD_ERR_INVALID_ARGUMENT, "invalid argument");
+  KD_CK(cudaSetDevice(b->device));
+  const HostModel& m = b->models[b->world_model[w]];
+  const DevWorld& W = b->worlds[w];
+  const BatchView& v = b->view;
+  const int njd = m.n_bil + m.n_dyn;
+  // contact entries -> model pair index (collide()'s pair list); the device
+  // cache is kept sorted by pair (K1 bisects it).  A stable sort keeps the
+  // entry order within a pair, the only order match_warmstart's (dist, entry,
+  // contact) tie-break can see, since candidates compete only within a pair.
+  std::vector<CacheEntry> ce;
+  for (int c = 0; c < ncon; ++c) {
+    int pair = -1;
+    for (size_t p = 0; p < m.pairs.size() && pair < 0; ++p)
+      if (m.pairs[p].a == con[c].geom_a && m.pairs[p].b == con[c].geom_b) pair = (int)p;
+    if (pair < 0) continue;
+    CacheEntry e{};
+    e.ga = con[c].geom_a;
+    e.gb = con[c].geom_b;
+    e.pair = pair;
+    for (int d = 0; d < 3; ++d) {
+      e.pos[d] = con[c].position[d];
+      e.imp[d] = con[c].impulse[d];
+      e.dual[d] = con[c].dual[d];
+    }
+    ce.push_back(e);
+  }
+  std::stable_sort(ce.begin(), ce.end(), [](const CacheEntry& x, const CacheEntry& y) { return x.pair < y.pair; });
+  if ((int)ce.size() > W.contact_cap)
+    return fail(KD_ERR_CAPACITY, "contact cache: " + std::to_string(ce.size()) + " entries exceed the world's " +
+                                     std::to_string(W.contact_cap) + "-contact capacity");
+  WorldStep s;
+  KD_CK(to_host(b, &s, v.wstep + w, sizeof(s)));
+  s.jcache_valid = (jvalid && jlen == njd) ? 1 : 0;
+  if (s.jcache_valid && njd) {
+    if (!jlam || !jz) return fail(KD_ERR_INVALID_ARGUMENT, "joint cache arrays are null");
+    KD_CK(to_dev(b, v.jc_lam + W.jcache_off, jlam, 8 * (size_t)njd));
+    KD_CK(to_dev(b, v.jc_z + W.jcache_off, jz, 8 * (size_t)njd));
+  }
+  const int nls = 2 * m.info.n_limited_joints;
+  if (nls) {
+    std::vector<int32_t> valid(nls, 0);
+    std::vector<double> ll(nls, 0.0), lz(nls, 0.0);
+    for (int k = 0; k < nlim; ++k) {
+      const int j = lim[k].joint, bound = lim[k].bound;
+      if (j < 0 || j >= (int)m.joints.size() || bound < 0 || bound > 1 || !(m.joints[j].flags & JF_LIMITS)) continue;
+      const int slot = 2 * m.joints[j].limit_slot + bound;
+      valid[slot] = 1;
+      ll[slot] = lim[k].lambda;
+      lz[slot] = lim[k].z;
+    }
+    KD_CK(to_dev(b, v.ls_valid + W.lslot_off, valid.data(), 4 * (size_t)nls));
+    KD_CK(to_dev(b, v.ls_lam + W.lslot_off, ll.data(), 8 * (size_t)nls));
+    KD_CK(to_dev(b, v.ls_z + W.lslot_off, lz.data(), 8 * (size_t)nls));
+  }
+  if (!ce.empty()) KD_CK(to_dev(b, v.ccache + W.contact_off, ce.data(), sizeof(CacheEntry) * ce.size()));
+  s.ccache_count = (int)ce.size();
+  KD_CK(to_dev(b, v.wstep + w, &s, sizeof(s)));
   return KD_OK;
 }
 

@@ -1063,11 +1063,10 @@ static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const 
                                int nbcap, int n_reg, cudaStream_t s) {
   const size_t smem = std::max(cr_smem_bytes(ncap, nbcap, NT),
                                std::min<size_t>(232448 / MINB, cr_staged_bytes(ncap, nbcap, NT)));
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(cr_kernel<NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static SmemAttrCache attr;
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(cr_kernel<NT, MINB>), smem, attr);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   cr_kernel<NT, MINB><<<count, NT, smem, s>>>(bv, sp, worlds, (int)(smem / 8), n_reg);
   return cudaGetLastError();
@@ -1078,12 +1077,10 @@ static cudaError_t launch_cr_op_p(const BatchView& bv, const StepParams& sp, con
                                   int ncap, int nbcap, int skip_marked, cudaStream_t s) {
   const int nc = std::min(ncap, RPT * NT);
   const size_t smem = cr_common_bytes(nc, NT) + Op::smem_bytes(nc, nbcap);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(cr_op_kernel<Op, NT, RPT, MINB, PROF, MARK>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static SmemAttrCache attr;
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(cr_op_kernel<Op, NT, RPT, MINB, PROF, MARK>), smem, attr);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   cr_op_kernel<Op, NT, RPT, MINB, PROF, MARK><<<count, NT, smem, s>>>(bv, sp, worlds, skip_marked);
   return cudaGetLastError();

@@ -338,8 +338,10 @@ __device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, 
 // be nonzero (all ones unless the factor came from a supernodal plan).  A zero
 // tile L_i,kk contributes nothing to phases 2 and 3; a structurally zero tile
 // X_kk,j is never formed (phase 1) nor used (phase 2).
+// (masks exist only for supernodal hand-off factors, T <= 8; an all-ones mask
+// means "every tile", valid for any T)
 __device__ __forceinline__ bool mtile(unsigned long long mask, int ti, int tj) {
-  return (mask >> (ti * (ti + 1) / 2 + tj)) & 1ull;
+  return mask == ~0ull || ((mask >> (ti * (ti + 1) / 2 + tj)) & 1ull);
 }
 template <int NT>
 __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, unsigned long long xmask,
@@ -351,28 +353,35 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, u
     for (int t = 0; t < q; ++t) m &= m - 1;
     return __ffs(m) - 1;
   };
+  const bool full = lmask == ~0ull && xmask == ~0ull;  // dense factor: every tile, any T
   for (int k = 1; k < T; ++k) {
     // the column-(k-1) contributions B_i,k-1 = -L_i,k-1 Linv_k-1 (phase 3 of step k-1)
     // and B_ij -= L_i,k-1 X_k-1,j (phase 2) are applied below, in order.
     const int kk = k - 1;
     unsigned rows = 0, cols = 0;  // rows i > kk with L_i,kk != 0; columns j < kk with X_kk,j != 0
-    for (int i = kk + 1; i < T; ++i)
-      if (mtile(lmask, i, kk)) rows |= 1u << i;
-    for (int j = 0; j < kk; ++j)
-      if (mtile(xmask, kk, j)) cols |= 1u << j;
-    const int below = __popc(rows), nc = __popc(cols);
+    int below = T - 1 - kk, nc = kk;
+    if (!full) {
+      for (int i = kk + 1; i < T; ++i)
+        if (mtile(lmask, i, kk)) rows |= 1u << i;
+      for (int j = 0; j < kk; ++j)
+        if (mtile(xmask, kk, j)) cols |= 1u << j;
+      below = __popc(rows);
+      nc = __popc(cols);
+    }
+    auto row_at = [&](int q) { return full ? kk + 1 + q : nth_bit(rows, q); };
+    auto col_at = [&](int q) { return full ? q : nth_bit(cols, q); };
     // phase 1 (step kk): X_kk,j = Linv_kk B_kk,j for j < kk
-    for (int u = wid; u < nc; u += NW) trmm_left(L, kk, nth_bit(cols, u), n, lane);
+    for (int u = wid; u < nc; u += NW) trmm_left(L, kk, col_at(u), n, lane);
     __syncthreads();
     // phase 2 (step kk): B_ij -= L_i,kk X_kk,j for i > kk, j < kk
     for (int u = wid; u < below * nc; u += NW) {
-      const int i = nth_bit(rows, u / nc);
-      gemm_sub(L, i, nth_bit(cols, u % nc), kk, n, lane, km(i, kk));
+      const int i = row_at(u / nc);
+      gemm_sub(L, i, col_at(u % nc), kk, n, lane, km(i, kk));
     }
     __syncthreads();
     // phase 3 (step kk): B_i,kk = -L_i,kk Linv_kk for i > kk
     for (int u = wid; u < below; u += NW) {
-      const int i = nth_bit(rows, u);
+      const int i = row_at(u);
       trmm_right_neg(L, i, kk, n, lane, km(i, kk));
     }
     __syncthreads();
@@ -475,6 +484,149 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, u
 #endif
 }
 
+
+
+// PADMM loop of the dense kernel for GLOBAL_L worlds (any n): the same
+// arithmetic as the register-resident loop of dense_kernel, with every thread
+// looping over its cone units (u = tid, tid + NT, ...).  Per-unit state y, z,
+// y_hat, z_hat is kept in the world's slab after the factor (4 npad doubles);
+// the residual maxima are exact (max is associative), so the loop's results do
+// not depend on how units map to threads.
+template <int NT>
+__device__ void padmm_units_global(const BatchView& bv, const StepParams& sp, int w, WorldStep& ws, const double* L,
+                                   double* xv, double* wv_s, double* red, int n, int T, int nlen) {
+  const int tid = threadIdx.x;
+  const DevWorld W = bv.worlds[w];
+  const int64_t R0 = W.row_off;
+  const int npad = 32 * T;
+  double* ys = const_cast<double*>(L) + ((nlen + 1) & ~1);
+  double* zs = ys + npad;
+  double* yhs = zs + npad;
+  double* zhs = yhs + npad;
+  const int n_jd = ws.n_rows - ws.n_limits - 3 * ws.n_contacts;
+  const int first_contact = n_jd + ws.n_limits;
+  const int n_units = first_contact + ws.n_contacts;
+  const double eta = sp.eta, rho = sp.rho, inv_rho = 1.0 / rho;
+  const double* vfg = bv.vf + R0;
+  const double* rmu = bv.rmu + R0;
+  auto unit_rows = [&](int u, int& row0, int& kind, int& nr) {
+    row0 = u < first_contact ? u : first_contact + 3 * (u - first_contact);
+    kind = u < n_jd ? ROW_BILATERAL : (u < first_contact ? ROW_LIMIT : ROW_CONTACT);
+    nr = kind == ROW_CONTACT ? 3 : 1;
+  };
+  // y = Pi_K(x0); hats; first right-hand side
+  for (int u = tid; u < n_units; u += NT) {
+    int row0, kind, nr;
+    unit_rows(u, row0, kind, nr);
+    double x[3] = {0, 0, 0}, y[3] = {0, 0, 0}, z[3] = {0, 0, 0};
+    for (int d = 0; d < nr; ++d) {
+      x[d] = bv.x0[R0 + row0 + d];
+      z[d] = bv.z0[R0 + row0 + d];
+    }
+    const double mu = rmu[row0];
+    if (kind == ROW_CONTACT) project_soc(x, mu, 1.0 / (1.0 + mu * mu), y);
+    else y[0] = kind == ROW_LIMIT ? fmax(0.0, x[0]) : x[0];
+    const double s0 = kind == ROW_CONTACT ? mu * fast_sqrt(z[1] * z[1] + z[2] * z[2]) : 0.0;
+    for (int d = 0; d < nr; ++d) {
+      ys[row0 + d] = yhs[row0 + d] = y[d];
+      zs[row0 + d] = zhs[row0 + d] = z[d];
+      xv[row0 + d] = -((((vfg[row0 + d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * y[d]) - z[d]);
+    }
+  }
+  double prev = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  double rp = 0.0, dmax = 0.0, rc = 0.0;
+  int restarts = 0, it = 1, m = 0;
+  bool converged = false;
+  const int hcap = bv.hist_cap;
+  const unsigned long long xm = ~0ull;
+  for (it = 1; it <= sp.max_iters; ++it) {
+    inv_solve<NT>(L, xv, wv_s, n, T, xm);  // barriers on entry and exit
+    const double beta = sp.acceleration ? sp.nest_beta[m] : 0.0;
+    rp = dmax = rc = 0.0;
+    for (int u = tid; u < n_units; u += NT) {
+      int row0, kind, nr;
+      unit_rows(u, row0, kind, nr);
+      const double mu = rmu[row0];
+      double x[3] = {0, 0, 0}, wv[3] = {0, 0, 0}, yn[3] = {0, 0, 0};
+      for (int d = 0; d < nr; ++d) {
+        x[d] = xv[row0 + d];
+        wv[d] = x[d] - zhs[row0 + d] * inv_rho;
+      }
+      if (kind == ROW_CONTACT) project_soc(wv, mu, 1.0 / (1.0 + mu * mu), yn);
+      else yn[0] = kind == ROW_LIMIT ? fmax(0.0, wv[0]) : wv[0];
+      double ymax = 0.0, zmax = 0.0;
+      for (int d = 0; d < nr; ++d) {
+        const double zn = zhs[row0 + d] - rho * (x[d] - yn[d]);
+        rp = fmax(rp, fabs(x[d] - yn[d]));
+        dmax = fmax(dmax, fabs(yn[d] - ys[row0 + d]));
+        ymax = fmax(ymax, fabs(yn[d]));
+        zmax = fmax(zmax, fabs(zn));
+        // y_prev / z_prev parked in the hat slots until the Nesterov step
+        yhs[row0 + d] = ys[row0 + d];
+        zhs[row0 + d] = zs[row0 + d];
+        ys[row0 + d] = yn[d];
+        zs[row0 + d] = zn;
+      }
+      if (kind != ROW_BILATERAL) rc = fmax(rc, fmin(ymax, zmax));
+    }
+    const double combined = block_max_nonneg<NT>(fmax(rp, fmax(rho * dmax, rc)), red);
+    if (tid == 0 && it <= hcap) bv.hist[(int64_t)w * hcap + it - 1] = combined;
+    if (!sp.fixed_mode && combined < sp.eps) {
+      converged = true;
+      break;
+    }
+    bool restart = false;
+    if (sp.acceleration) {
+      restart = sp.restart && combined > prev;
+      if (restart) {
+        m = 0;
+        ++restarts;
+      } else {
+        ++m;
+      }
+    }
+    prev = combined;
+    for (int u = tid; u < n_units; u += NT) {
+      int row0, kind, nr;
+      unit_rows(u, row0, kind, nr);
+      double zh[3] = {0, 0, 0};
+      for (int d = 0; d < nr; ++d) {
+        const double yv = ys[row0 + d], zv = zs[row0 + d];
+        double yh = yv, zhd = zv;  // restart, or no acceleration
+        if (sp.acceleration && !restart) {
+          yh = yv + beta * (yv - yhs[row0 + d]);
+          zhd = zv + beta * (zv - zhs[row0 + d]);
+        }
+        yhs[row0 + d] = yh;
+        zhs[row0 + d] = zhd;
+        zh[d] = zhd;
+      }
+      const double mu = rmu[row0];
+      const double s0 = kind == ROW_CONTACT ? mu * fast_sqrt(zh[1] * zh[1] + zh[2] * zh[2]) : 0.0;
+      for (int d = 0; d < nr; ++d)
+        xv[row0 + d] = -((((vfg[row0 + d] + (d == 0 ? s0 : 0.0)) - eta * xv[row0 + d]) - rho * yhs[row0 + d]) - zh[d]);
+    }
+  }
+  __syncthreads();  // red is still being read by the last reduction
+  block_max3<NT>(rp, dmax, rc, red);
+  const double r_p = rp, r_d = rho * dmax, r_c = rc;
+  for (int r = tid; r < n; r += NT) {
+    bv.lam[R0 + r] = ys[r];
+    bv.zo[R0 + r] = zs[r];
+  }
+  if (tid == 0) {
+    const int done = min(it, sp.max_iters);
+    ws.iterations = done;
+    ws.r_p = r_p;
+    ws.r_d = r_d;
+    ws.r_c = r_c;
+    ws.restarts = restarts;
+    ws.converged = (converged || fmax(r_p, fmax(r_d, r_c)) < sp.eps) ? 1 : 0;
+    ws.cr_iterations = 0;
+    ws.cr_breakdown = 0;
+    for (int i = done; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
+  }
+}
 
 }  // namespace
 
@@ -703,6 +855,14 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   }
   stamp(3);
 
+  if constexpr (GLOBAL_L) {
+    // ---- 3'. PADMM (padmm.cpp:87-159) for worlds of any size: thread t owns
+    // cone units t, t + NT, ...; y, z, y_hat, z_hat live in the world's HBM
+    // slab after the factor (L2-resident), the solve vector in shared memory.
+    padmm_units_global<NT>(bv, sp, w, ws, L, xv, wv_s, red, n, T, nlen);
+    stamp(4);
+    return;
+  } else {
   // ---- 3. PADMM (padmm.cpp:87-159), one cone unit per thread
   const int n_jd = ws.n_rows - ws.n_limits - 3 * ws.n_contacts;
   const int first_contact = n_jd + ws.n_limits;
@@ -865,6 +1025,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     ws.cr_breakdown = 0;
     for (int i = done; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
   }
+  }  // !GLOBAL_L
 }
 
 // Shared-memory bytes the dense kernel needs for n rows with NT threads.
@@ -887,11 +1048,10 @@ template <int NT, bool G>
 static cudaError_t launch_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int cap,
                             cudaStream_t s) {
   const size_t smem = dense_smem_bytes(cap, NT, G);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(dense_kernel<NT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static SmemAttrCache attr;
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(dense_kernel<NT, G>), smem, attr);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   dense_kernel<NT, G><<<count, NT, smem, s>>>(bv, sp, worlds);
   return cudaGetLastError();

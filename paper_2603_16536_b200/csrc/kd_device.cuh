@@ -3,10 +3,38 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "kd_layout.h"
 #include "kd_math.cuh"
 
 namespace kd {
+
+// Opt-in to more than 48 KB of dynamic shared memory for kernel `fn` on the
+// current device.  The attribute is per device, so the largest size already
+// configured is cached per device (one slot per device ordinal, updated with a
+// compare-exchange: safe when host threads drive different GPUs at once).
+struct SmemAttrCache {
+  static constexpr int kMaxDevices = 64;
+  std::atomic<size_t> bytes[kMaxDevices];
+  SmemAttrCache() {
+    for (auto& b : bytes) b.store(0);
+  }
+};
+inline cudaError_t ensure_smem_attr(const void* fn, size_t smem, SmemAttrCache& cache) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const bool cached = dev >= 0 && dev < SmemAttrCache::kMaxDevices;
+  if (cached && cache.bytes[dev].load() >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess || !cached) return e;
+  size_t cur = cache.bytes[dev].load();
+  while (cur < smem && !cache.bytes[dev].compare_exchange_weak(cur, smem)) {
+  }
+  return cudaSuccess;
+}
 
 __device__ __forceinline__ V3 ld3(const double* p) { return V3{p[0], p[1], p[2]}; }
 __device__ __forceinline__ Q4 ldq(const double* p) { return Q4{p[0], p[1], p[2], p[3]}; }

@@ -256,11 +256,10 @@ size_t fk_smem_bytes(int nb, int nr) {
 cudaError_t launch_fk(const BatchView& bv, const int32_t* tj, const double* tv, int nt, double tol, int max_iters,
                       double lm0, int32_t* iters, double* res, uint8_t* conv, size_t smem, cudaStream_t s) {
   if (bv.n_worlds <= 0) return cudaSuccess;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(fk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static SmemAttrCache attr;
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(fk_kernel), smem, attr);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   fk_kernel<<<bv.n_worlds, kFkThreads, smem, s>>>(bv, tj, tv, nt, tol, max_iters, lm0, iters, res, conv);
   return cudaGetLastError();

@@ -28,6 +28,7 @@ struct HostModel {
   // supernodal sparse-LLT plan (kd_snplan.h); null if the model is unsuited
   std::shared_ptr<SnPlanHost> sn;
   std::string sn_why;
+  int contact_cap = 0;  // kd_model_set_contact_capacity (0: default)
 };
 
 int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err, uint32_t extensions = 0);

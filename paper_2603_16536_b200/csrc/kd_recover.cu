@@ -17,6 +17,10 @@ __global__ void __launch_bounds__(256) recover_kernel(BatchView bv, StepParams s
   if (w >= w1) return;
   if (!bv.active[w]) return;
   WorldStep& ws = bv.wstep[w];
+  // a world whose solve was skipped this step (contact or slab capacity
+  // overflow, fail = 2) or failed (non-SPD factor, fail = 1) keeps its state
+  // and caches untouched; the step reports the error (kd_batch_sync)
+  if (ws.fail != 0 || (ws.n_rows > 0 && ws.backend == BE_NONE)) return;
   const DevWorld W = bv.worlds[w];
   const DevModel M = bv.models[W.model];
   const int n = ws.n_rows;

@@ -264,11 +264,10 @@ size_t snfactor_smem_bytes(int nLv, int S) {
 cudaError_t launch_snfactor(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, size_t smem,
                             cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(snfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static SmemAttrCache attr;
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(snfactor_kernel), smem, attr);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   snfactor_kernel<<<count, kFactorThreads, smem, s>>>(bv, sp, worlds);
   return cudaGetLastError();

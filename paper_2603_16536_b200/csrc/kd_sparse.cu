@@ -435,11 +435,10 @@ cudaError_t launch_sparse(const BatchView& bv, const StepParams& sp, const int32
                           int wpc, int prog_words, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const size_t smem = ((size_t)prog_words + 3) / 4 * 16 + (size_t)per_warp * wpc * sizeof(double);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static SmemAttrCache attr;
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(sparse_kernel), smem, attr);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   sparse_kernel<<<(count + wpc - 1) / wpc, 32 * wpc, smem, s>>>(bv, sp, worlds, count, per_warp, prog_words);
   return cudaGetLastError();

@@ -138,12 +138,35 @@ def build_model(scene: SceneDescription) -> Model:
 
 
 @dataclass
+class JointReactionCache:
+    """Converged bilateral + joint-dynamics reactions (stepper.hpp:38-43)."""
+    lambda_: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    z: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    valid: bool = False
+
+
+@dataclass
+class ReactionCacheEntry:
+    """Contact reaction cache entry (contacts.hpp:32-38); impulse and dual in
+    the contact frame (n, t1, t2)."""
+    geom_a: int
+    geom_b: int
+    position: np.ndarray
+    impulse: np.ndarray
+    dual: np.ndarray
+
+
+@dataclass
 class WorldState:
-    """Body poses [x y z qw qx qy qz] and twists [v; w] of one world
-    (stepper.hpp:49-56; the warm-start caches stay on the device)."""
+    """One world's state (stepper.hpp:49-56): body poses [x y z qw qx qy qz],
+    twists [v; w], time and the three warm-start caches.  `limit_cache` maps
+    (joint, bound) -> (lambda, z) like LimitReactionCache's std::map."""
     poses: np.ndarray
     twists: np.ndarray
     time: float = 0.0
+    joint_cache: JointReactionCache = field(default_factory=JointReactionCache)
+    limit_cache: dict = field(default_factory=dict)
+    contact_cache: List[ReactionCacheEntry] = field(default_factory=list)
 
 
 # ------------------------------------------------------------------ batch
@@ -197,6 +220,9 @@ class WorldBatch:
                     t[self._twist_off[w]: self._twist_off[w] + 6 * nb] = np.asarray(s.twists).reshape(-1)
                     tm[w] = s.time
             self.set_state(p, t, tm)
+            for w, s in enumerate(self._init):
+                if s is not None:
+                    self.set_caches(w, s.joint_cache, s.limit_cache, s.contact_cache)
         self._active = np.ones(max(1, self.n_worlds), np.uint8)
 
     def __del__(self):
@@ -227,13 +253,17 @@ class WorldBatch:
         return self.get_state()[1]
 
     def extract_state(self, w) -> WorldState:
+        """extract_state (batch.cpp:27-45): state and warm-start caches."""
         p, t, tm = self.get_state()
         nb = self.model(w).n_bodies
         po, to = self._pose_off[w], self._twist_off[w]
-        return WorldState(p[po: po + 7 * nb].reshape(nb, 7).copy(), t[to: to + 6 * nb].reshape(nb, 6).copy(),
-                          float(tm[w]))
+        s = WorldState(p[po: po + 7 * nb].reshape(nb, 7).copy(), t[to: to + 6 * nb].reshape(nb, 6).copy(),
+                       float(tm[w]))
+        s.joint_cache, s.limit_cache, s.contact_cache = self.get_caches(w)
+        return s
 
     def insert_state(self, w, s: WorldState):
+        """insert_state (batch.cpp:47-71): state and warm-start caches."""
         p, t, tm = self.get_state()
         nb = self.model(w).n_bodies
         po, to = self._pose_off[w], self._twist_off[w]
@@ -241,6 +271,46 @@ class WorldBatch:
         t[to: to + 6 * nb] = np.asarray(s.twists).reshape(-1)
         tm[w] = s.time
         self.set_state(p, t, tm)
+        self.set_caches(w, s.joint_cache, s.limit_cache, s.contact_cache)
+
+    def get_caches(self, w):
+        """(JointReactionCache, {(joint, bound): (lambda, z)}, [ReactionCacheEntry])
+        of world w (kd_batch_get_caches)."""
+        self._ensure()
+        jl, jv, nl, nc = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().kd_batch_get_cache_sizes(self.handle, int(w), C.byref(jl), C.byref(jv), C.byref(nl),
+                                              C.byref(nc)))
+        lam, z = np.zeros(max(1, jl.value)), np.zeros(max(1, jl.value))
+        lim = (_capi.kd_limit_cache_entry * max(1, nl.value))()
+        con = (_capi.kd_contact_cache_entry * max(1, nc.value))()
+        nl2, nc2, jv2 = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().kd_batch_get_caches(self.handle, int(w), _capi.dptr(lam), _capi.dptr(z), C.byref(jv2), lim,
+                                         max(1, nl.value), C.byref(nl2), con, max(1, nc.value), C.byref(nc2)))
+        jc = JointReactionCache(lam[: jl.value].copy(), z[: jl.value].copy(), bool(jv2.value))
+        lc = {(lim[k].joint, lim[k].bound): (lim[k].lambda_, lim[k].z) for k in range(nl2.value)}
+        cc = [ReactionCacheEntry(con[k].geom_a, con[k].geom_b, np.array(con[k].position[:]),
+                                 np.array(con[k].impulse[:]), np.array(con[k].dual[:])) for k in range(nc2.value)]
+        return jc, lc, cc
+
+    def set_caches(self, w, joint_cache: JointReactionCache, limit_cache: dict, contact_cache):
+        self._ensure()
+        lam = np.ascontiguousarray(joint_cache.lambda_, dtype=np.float64).reshape(-1)
+        z = np.ascontiguousarray(joint_cache.z, dtype=np.float64).reshape(-1)
+        keys = sorted(limit_cache)
+        lim = (_capi.kd_limit_cache_entry * max(1, len(keys)))()
+        for k, key in enumerate(keys):
+            lim[k].joint, lim[k].bound = int(key[0]), int(key[1])
+            lim[k].lambda_, lim[k].z = float(limit_cache[key][0]), float(limit_cache[key][1])
+        con = (_capi.kd_contact_cache_entry * max(1, len(contact_cache)))()
+        for k, e in enumerate(contact_cache):
+            con[k].geom_a, con[k].geom_b = int(e.geom_a), int(e.geom_b)
+            for d in range(3):
+                con[k].position[d] = float(e.position[d])
+                con[k].impulse[d] = float(e.impulse[d])
+                con[k].dual[d] = float(e.dual[d])
+        _check(lib().kd_batch_set_caches(self.handle, int(w), _capi.dptr(lam if len(lam) else np.zeros(1)),
+                                         _capi.dptr(z if len(z) else np.zeros(1)), len(lam),
+                                         int(bool(joint_cache.valid)), lim, len(keys), con, len(contact_cache)))
 
     def set_active(self, w, active: bool):
         self._ensure()
@@ -433,6 +503,20 @@ def _rows_to_numpy(rows, n):
                       ("lambda", "lambda_"), ("z", "z")):
         out[key] = np.array([getattr(rows[i], attr) for i in range(n)])
     return out
+
+
+def step(model: Model, state: WorldState, config: StepConfig, device: int = 0):
+    """step (stepper.hpp:84, stepper.cpp:134-236) for one world: a one-world
+    device batch warm-started from `state`'s caches; `state` is updated in
+    place (poses, twists, time and caches) and the step's diagnostics are
+    returned.  For many worlds use WorldBatch + batch_step."""
+    b = WorldBatch(device)
+    b.add_world(model, state)
+    b.step(config)
+    s = b.extract_state(0)
+    state.poses, state.twists, state.time = s.poses, s.twists, s.time
+    state.joint_cache, state.limit_cache, state.contact_cache = s.joint_cache, s.limit_cache, s.contact_cache
+    return b.diagnostics()[0]
 
 
 def batch_step(batch: WorldBatch, config: StepConfig, n_threads: int = 0):

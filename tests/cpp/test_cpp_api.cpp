@@ -93,6 +93,24 @@ int main(int argc, char** argv) {
     WorldBatch scratch;
     for (int k = 0; k < 10; ++k) step(fourbar, st, cfg, &scratch);
     CHECK(std::abs(st.time - 10 * cfg.dt) < 1e-12);
+    // the reference signature step(const MechanismModel&, WorldState&, cfg)
+    // warm-starts from the state's caches: a fresh one-world batch per call
+    // tracks a persistent batch bit for bit (checkpoint/restore keeps the
+    // trajectory, stepper.cpp:181-187)
+    WorldState a = initial_state(*sphere);
+    WorldBatch persistent;
+    persistent.add_world(sphere);
+    bool same = true;
+    for (int k = 0; k < 30; ++k) {
+      const StepDiagnostics da = step(*sphere, a, cfg);
+      batch_step(persistent, cfg);
+      const WorldState b = persistent.extract_state(0);
+      same = same && da.solver.iterations == persistent.diagnostics(0).solver.iterations;
+      for (int q = 0; q < 3; ++q) same = same && a.poses[0].position[q] == b.poses[0].position[q];
+      for (int q = 0; q < 3; ++q) same = same && a.twists[0].linear[q] == b.twists[0].linear[q];
+    }
+    CHECK(same);
+    CHECK(a.joint_cache.valid && a.contact_cache.entries.size() == 1);
   }
   std::printf("%s: %d failures\n", gpu ? "cpp api (gpu)" : "cpp api (cpu)", failures);
   return failures;

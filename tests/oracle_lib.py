@@ -36,6 +36,7 @@ def lib():
                                        C.POINTER(C.c_void_p)]),
             "batch_step": (C.c_int, [C.c_void_p, C.POINTER(_capi.kd_step_config), C.c_int32, C.c_int32]),
             "batch_set_trace": (C.c_int, [C.c_void_p, C.c_int32]),
+            "batch_get_caches": _capi.KD_ONLY["batch_get_caches"],
             "batch_get_history": (C.c_int, [C.c_void_p, C.c_int32, _capi.c_double_p]),
             "batch_energy": (C.c_int, [C.c_void_p, C.c_int32, _capi.c_double_p, _capi.c_double_p]),
             "fd_check": (C.c_double, [C.c_void_p, _capi.c_double_p, C.c_double]),
@@ -188,6 +189,20 @@ class OracleBatch:
         n = C.c_int32()
         _check(lib().or_batch_dump_limits(self.handle, w, _capi.i32ptr(k), cap, C.byref(n)))
         return k[: 2 * n.value].reshape(-1, 2)
+
+    def caches(self, w, cap=4096):
+        """(joint lambda, joint z, joint valid, {(joint, bound): (lambda, z)},
+        [(geom_a, geom_b, position, impulse, dual)]) of world w."""
+        lam, z = np.zeros(cap), np.zeros(cap)
+        jv, nl, nc = C.c_int32(), C.c_int32(), C.c_int32()
+        lim = (_capi.kd_limit_cache_entry * cap)()
+        con = (_capi.kd_contact_cache_entry * cap)()
+        _check(lib().or_batch_get_caches(self.handle, int(w), _capi.dptr(lam), _capi.dptr(z), C.byref(jv), lim, cap,
+                                         C.byref(nl), con, cap, C.byref(nc)))
+        lc = {(lim[k].joint, lim[k].bound): (lim[k].lambda_, lim[k].z) for k in range(nl.value)}
+        cc = [(con[k].geom_a, con[k].geom_b, np.array(con[k].position[:]), np.array(con[k].impulse[:]),
+               np.array(con[k].dual[:])) for k in range(nc.value)]
+        return lam, z, bool(jv.value), lc, cc
 
     def energy(self, w):
         ke, pe = C.c_double(), C.c_double()

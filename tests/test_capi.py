@@ -31,11 +31,12 @@ def test_library_exports_every_header_symbol():
 
 def test_struct_layouts_match_compiled_abi():
     lib = C.CDLL(K.LIB_PATH)
-    out = (C.c_int32 * 8)()
-    assert lib.kd_abi_sizes(out, 8) == 8
+    out = (C.c_int32 * 10)()
+    assert lib.kd_abi_sizes(out, 10) == 10
     mine = [C.sizeof(t) for t in (_capi.kd_body_desc, _capi.kd_joint_desc, _capi.kd_geom_desc,
                                    _capi.kd_scene_desc, _capi.kd_step_config, _capi.kd_step_diag,
-                                   _capi.kd_model_info, _capi.kd_row_dump)]
+                                   _capi.kd_model_info, _capi.kd_row_dump, _capi.kd_limit_cache_entry,
+                                   _capi.kd_contact_cache_entry)]
     assert list(out) == mine
 
 
