@@ -27,16 +27,25 @@ iterations; settled steps ~35).
 Other BASELINE configs (`--workload`, each its own JSON line; the default line
 is dr_legs): fourbar (configs[0]'s scene batched, 16384 worlds), hetero
 (configs[2]: four-bar / DR-Legs / serial_chain_10 by w % 3, 16384 worlds),
-closed_chain (configs[3]: 1024 ladder worlds, n = 340 -> matrix-free CR),
-sphere_pile (configs[4] substitute: 100 spheres in a bin, 8192 worlds per GPU,
+stewart_tower (configs[3] as SURVEY §8d specifies it: a spatial parallel
+manipulator, 12 stacked Stewart platforms, 156 bodies, spherical + prismatic
+legs, n = 942 -> matrix-free CR, 1024 worlds), closed_chain (a planar
+parallelogram ladder, 22 cells, 88 joints, n = 440 -> CR, 1024 worlds), sphere_pile (configs[4] substitute: 100 spheres in a bin, 8192 worlds per GPU,
 CR), box_pile (configs[4] as written: 64 boxes in a bin with the opt-in box-box
 narrow phase, 8192 worlds per GPU, CR).  The roofline object then describes the
 workload's dominant kernel family.
 
-Multi-GPU: one process per GPU (torchrun); rank r owns global worlds
-[r*W, (r+1)*W): worlds are independent, so there is no collective on the data
-path ("scaling": "weak"); one all-reduce of the elapsed time at the end.
-`--impl reference` times the CPU oracle path instead (rank 0 only).
+Multi-GPU: one process per GPU.  Under torchrun the ranks come from the
+environment; `--gpus N` without WORLD_SIZE re-launches this script under
+torch.distributed.run with N ranks (127.0.0.1 rendezvous).  The global batch is
+W x N worlds in the reference order; `sharding.deal` bins them by model and
+deals every bin round-robin over the ranks, so each GPU gets the same mix.
+Worlds are independent, so there is no collective on the data path ("scaling":
+"weak"); one all-reduce of the elapsed time and of the run statistics at the
+end.  `--plan-only` runs the launcher and the sharding/statistics logic
+without stepping (any backend: gloo on a CPU host; tests/test_multiproc.py).
+`--impl reference` times the CPU oracle path instead (rank 0 only; it never
+loads the product library).
 """
 import argparse
 import ctypes as C
@@ -60,7 +69,7 @@ UNIT = "world-steps/s"
 def workloads():
     """name -> (scene builders, world -> model index, default worlds per GPU, BASELINE config)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from paper_2603_16536_b200.scenes import box_pile, closed_chain, dr_legs, sphere_pile
+    from paper_2603_16536_b200.scenes import box_pile, closed_chain, dr_legs, sphere_pile, stewart_tower
 
     def bundled(name):
         def make():
@@ -73,8 +82,12 @@ def workloads():
         "fourbar": ([bundled("fourbar")], lambda w: 0, 16384, "configs[0]: the four-bar scene, batched"),
         "hetero": ([bundled("fourbar"), dr_legs, bundled("serial_chain_10")], lambda w: w % 3, 16384,
                    "configs[2]: four-bar / DR Legs / serial_chain_10 by world % 3 (main.cpp:202)"),
+        "stewart_tower": ([stewart_tower], lambda w: 0, 1024,
+                          "configs[3]: spatial parallel manipulator (12 stacked 6-6 Stewart platforms, 156 bodies, "
+                          "216 spherical/prismatic joints, n = 942 rows) -> matrix-free CR"),
         "closed_chain": ([lambda: closed_chain(22)], lambda w: 0, 1024,
-                         "configs[3]: 22-cell parallelogram ladder, n = 340 rows -> matrix-free CR"),
+                         "configs[3] (planar variant): 22-cell parallelogram ladder, 88 revolute joints, "
+                         "n = 440 rows -> matrix-free CR"),
         "sphere_pile": ([lambda: sphere_pile(100)], lambda w: 0, 8192,
                         "configs[4] substitute: 100 spheres in a 5-plane bin (box-box is rejected, "
                         "model.cpp:56-62), matrix-free CR"),
@@ -93,12 +106,30 @@ def parse():
     ap.add_argument("--settle", type=int, default=50)
     ap.add_argument("--worlds-per-gpu", type=int, default=0, help="0: the workload's default")
     ap.add_argument("--workload", default="dr_legs",
-                    choices=["dr_legs", "fourbar", "hetero", "closed_chain", "sphere_pile", "box_pile"])
+                    choices=["dr_legs", "fourbar", "hetero", "stewart_tower", "closed_chain", "sphere_pile",
+                             "box_pile"])
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="launch the ranks, shard the global batch and reduce the statistics, without stepping")
     return ap.parse_args()
+
+
+def relaunch(args):
+    """`--gpus N` (N > 1) outside torchrun: re-run this script as N ranks under
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous) and
+    return its exit code; rank 0's JSON line is the output."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 def dist_env():
@@ -195,57 +226,78 @@ def algorithmic_flops(n, iters):
     return n ** 3 / 3 + np.asarray(iters) * (2 * n * n + 20 * n)
 
 
-def build_world_batch(K, scenes, mix, n_local, rank, seed, device):
+def global_plan(wl, W, ws, rank):
+    """(global model keys, this rank's global world ids): the global batch is
+    W x ws worlds in the reference order; sharding.deal gives every rank the
+    same mix of models."""
     from paper_2603_16536_b200 import sharding
+    keys = [wl[1](w) for w in range(W * ws)]
+    return keys, sharding.deal(keys, ws, rank)
+
+
+def initial_twists(models_init, keys, worlds, seed, jitter=None):
+    """Jittered initial twists of the listed global worlds (main.cpp:199-211,
+    world-major over the global batch)."""
+    from paper_2603_16536_b200 import sharding
+    return sharding.jitter_worlds(lambda w: models_init[keys[w]], worlds, seed, jitter=jitter)
+
+
+def build_world_batch(K, scenes, keys, worlds, seed, device):
     models = [K.build_model(sc) for sc in scenes]
-    worlds = sharding.world_range(n_local, rank)
     b = K.WorldBatch(device=device)
     for w in worlds:
-        b.add_world(models[mix(w)])
+        b.add_world(models[keys[w]])
     p, _, tm = b.get_state()
-    # The jitter stream is global and world-major (main.cpp:199-211): rank r
-    # keeps the slice of global worlds [r*W, (r+1)*W).
-    if len(models) == 1:
-        t = sharding.jitter_slice(models[0].initial_state().twists, models[0].n_bodies, worlds, seed)
-    else:
-        init = [m.initial_state().twists for m in models]
-        t = sharding.jitter_slice_mixed(lambda w: init[mix(w)], worlds, seed)
+    t = initial_twists([m.initial_state().twists for m in models], keys, worlds, seed)
     b.set_state(p, t, tm)
     return b, models
 
 
-def cpu_baseline(args, wl, cfg, quick=False):
-    """The CPU oracle (restated reference solver) on this host's cores, on a
-    bounded sample of the workload's global world list."""
+def cpu_sample_size(workload, W, cores, full=False):
+    """Worlds the CPU oracle steps: the whole per-GPU batch when it fits a few
+    minutes of host time (`full`, the reference arm of the default line),
+    else a bounded sample of the global batch's first worlds."""
+    if full:
+        return W
+    heavy = workload in ("stewart_tower", "closed_chain", "sphere_pile", "box_pile")
+    return min(W, 2 * cores) if heavy else min(W, max(64, 32 * cores))
+
+
+def cpu_baseline(args, wl, cfg, n_worlds=None):
+    """The CPU oracle (restated reference solver, the reference itself cannot
+    be built: no Eigen) on this host's cores, at the GPU arm's trajectory
+    point: the same global worlds' jittered initial state, the same settle and
+    warm-up steps, then args.steps timed steps.  Never loads the product
+    library (the jitter stream comes from the oracle library)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib
-    import paper_2603_16536_b200 as K
     scenes, mix, W, _ = wl
     cores = os.cpu_count() or 1
-    heavy = args.workload in ("closed_chain", "sphere_pile")
-    if heavy:
-        n = min(W, 2 * cores if quick else 8 * cores)
-    else:
-        n = min(W, max(32, 8 * cores)) if quick else min(W, max(64, 32 * cores))
+    n = n_worlds or cpu_sample_size(args.workload, W, cores)
     sc = [f() for f in scenes]
     oms = [oracle_lib.OracleModel(x) for x in sc]
-    wm = [mix(w) for w in range(n)]
-    ob = oracle_lib.OracleBatch(oms, wm, n_threads=cores)
+    keys = [mix(w) for w in range(n)]
+    ob = oracle_lib.OracleBatch(oms, keys, n_threads=cores)
     p, t, tm = ob.get_state()
-    t = K.bench_jitter(t, [oms[m].n_bodies for m in wm], seed=args.seed)
+    init = []
+    for k in range(len(oms)):
+        probe = oracle_lib.OracleBatch([oms[k]], [0], n_threads=1)
+        init.append(probe.get_state()[1].copy())
+        del probe
+    t = initial_twists(init, keys, range(n), args.seed, jitter=oracle_lib.bench_jitter)
     ob.set_state(p, t, tm)
-    settle = min(args.settle, 20) if (quick or heavy) else args.settle
-    ob.step(cfg, settle + (1 if (quick or heavy) else args.warmup))
-    steps = 3 if (quick or heavy) else args.steps
+    ob.step(cfg, args.settle + max(3, args.warmup))
     t0 = time.perf_counter()
-    ob.step(cfg, steps)
+    ob.step(cfg, args.steps)
     dt = time.perf_counter() - t0
     d = ob.diagnostics()
     its = float(np.mean([d[w].iterations for w in range(n)]))
-    return {"value": n * steps / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{n} {args.workload} worlds (first {n} of the global batch, same jitter), {settle} settle "
-                      f"steps, {steps} timed steps, std::thread pool of {cores} threads (batch_step, batch.cpp:74-110)",
-            "mean_padmm_iterations": its}
+    conv = float(np.mean([d[w].converged for w in range(n)]))
+    return {"value": n * args.steps / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n} of the {W} {args.workload} worlds per GPU (global worlds 0..{n - 1}, same jitter), "
+                      f"{args.settle} settle + {max(3, args.warmup)} warm-up steps as the GPU arm, {args.steps} "
+                      f"timed steps, std::thread pool of {cores} threads (batch_step, batch.cpp:74-110)",
+            "same_config": n == W, "mean_padmm_iterations": its, "converged_fraction": conv}
 
 
 def metric_for(workload):
@@ -256,17 +308,22 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
-    import paper_2603_16536_b200 as K
+    from paper_2603_16536_b200.scene import config_for  # pure Python: no product library
     wl = workloads()[args.workload]
     if args.worlds_per_gpu:
         wl = (wl[0], wl[1], args.worlds_per_gpu, wl[3])
-    cfg = K.config_for(wl[0][0]())
-    cb = cpu_baseline(args, wl, cfg)
+    cfg = config_for(wl[0][0]())
+    cores = os.cpu_count() or 1
+    # the default line's whole batch (4096 DR-Legs worlds) fits a few minutes
+    # of host time: same worlds, same steps as the GPU arm
+    full = args.workload == "dr_legs"
+    cb = cpu_baseline(args, wl, cfg, n_worlds=cpu_sample_size(args.workload, wl[2], cores, full))
     out = {"metric": metric_for(args.workload), "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": args.workload, "baseline_config": wl[3], "worlds_sampled": cb["sample"],
-                      "dt": cfg.dt, "integrator": cfg.integrator, "settle_steps": args.settle},
+                      "same_config": cb["same_config"], "dt": cfg.dt, "integrator": cfg.integrator,
+                      "settle_steps": args.settle},
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -300,7 +357,7 @@ def make_chunks(K, torch, b, models, wmodel, W, local, workload):
     best that way (measured); KD_E2E_CHUNKS overrides."""
     p_all, t_all, tm_all = b.get_state()
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
-    cr_workload = workload in ("closed_chain", "sphere_pile", "box_pile")
+    cr_workload = workload in ("stewart_tower", "closed_chain", "sphere_pile", "box_pile")
     nch = int(os.environ.get("KD_E2E_CHUNKS", "0")) or (1 if cr_workload else min(3, max(1, W // (8 * nsm))))
     H = (W + nch - 1) // nch
     out = []
@@ -319,14 +376,76 @@ def make_chunks(K, torch, b, models, wmodel, W, local, workload):
     return out
 
 
+def smem_bytes_per_world(kind, n, iters, applies, plan_slots, solve_terms):
+    """Algorithmic shared-memory bytes of one world's solve on its kernel
+    (DESIGN.md §4): the explicit-inverse PADMM reads X = L^-1 (m(m+1)/2
+    doubles, m = n or the plan's slot count for the hand-off) twice per
+    iteration; the supernodal kernel reads its factor terms (value + vector
+    operand) once per iteration; the incidence-owner CR operator moves 4
+    doubles per incidence (2 per row) per apply."""
+    if kind in ("dense", "supernodal+dense"):
+        m = plan_slots if kind == "supernodal+dense" else n
+        return 16.0 * iters * m * (m + 1) / 2
+    if kind == "supernodal":
+        return 16.0 * iters * solve_terms
+    if kind == "cr":
+        return 64.0 * applies * n
+    return 0.0
+
+
+def plan_only(args, ws, rank, dist):
+    """The launcher + sharding + statistics path without stepping: every rank
+    derives its global worlds and their jittered initial twists, reduces the
+    statistics, and rank 0 prints what each rank owns (checksums)."""
+    wl = workloads()[args.workload]
+    W = args.worlds_per_gpu or wl[2]
+    keys, mine = global_plan(wl, W, ws, rank)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib
+    from paper_2603_16536_b200 import sharding
+    oms = [oracle_lib.OracleModel(f()) for f in wl[0]]
+    init = [oracle_lib.OracleBatch([m], [0], n_threads=1).get_state()[1].copy() for m in oms]
+    t = initial_twists(init, keys, mine, args.seed, jitter=oracle_lib.bench_jitter)
+
+    class D:  # per-world diagnostics stand-in: iterations = global id % 7
+        def __init__(self, w):
+            self.iterations, self.converged, self.kkt_momentum_inf = w % 7, int(w % 2 == 0), 1e-9 * (w % 5)
+            self.r_p = self.r_d = self.r_c = 1e-8 * (w % 3)
+
+    st = sharding.reduce_stats(dist, sharding.local_stats([D(w) for w in mine], len(mine)))
+    rec = {"rank": rank, "worlds": mine, "twist_sum": float(np.sum(t)), "twist_len": int(t.size),
+           "models": [sum(1 for w in mine if keys[w] == k) for k in range(len(oms))]}
+    got = [None] * ws
+    if dist is not None:
+        dist.all_gather_object(got, rec)
+    else:
+        got = [rec]
+    if rank == 0:
+        print(json.dumps({"plan_only": True, "n_gpus": ws, "workload": args.workload, "worlds_per_gpu": W,
+                          "ranks": got, "run_stats": st}), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     if args.impl == "reference":
         return run_reference(args)
-    ws, rank, local = dist_env()
     import torch
-    torch.cuda.set_device(local)
     dist = None
+    if args.plan_only:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        rc = plan_only(args, ws, rank, dist)
+        if dist is not None:
+            dist.destroy_process_group()
+        return rc
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the B200 solver has no CPU fallback)")
+    torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -336,14 +455,18 @@ def main():
     wl = (wl[0], wl[1], W, wl[3])
     scenes = [f() for f in wl[0]]
     cfg = K.config_for(scenes[0])  # one StepConfig, from the first scene (main.cpp:194)
-    b, models = build_world_batch(K, scenes, wl[1], W, rank, args.seed, local)
-    wmodel = [wl[1](w) for w in range(rank * W, (rank + 1) * W)]
+    keys, mine = global_plan(wl, W, ws, rank)
+    b, models = build_world_batch(K, scenes, keys, mine, args.seed, local)
+    Wl = len(mine)  # this rank's worlds (W, up to the per-bin rounding of the deal)
+    wmodel = [keys[w] for w in mine]
     nb_w = np.array([models[m].n_bodies for m in wmodel])
+    plan_slots = [((m.sparse_plan_info() or {}).get("slots", 0)) for m in models]
+    plan_terms = [((m.sparse_plan_info() or {}).get("solve_terms", 0)) for m in models]
     # e2e chunks: separate WorldBatches built from the same initial state and
     # stepped through the same settle/warm-up, so the e2e pass times exactly the
     # trajectory segment (and warm-start caches) of the device-timed pass
     # (worlds are independent; results do not depend on the batch split)
-    chunks = [] if args.no_e2e else make_chunks(K, torch, b, models, wmodel, W, local, args.workload)
+    chunks = [] if args.no_e2e else make_chunks(K, torch, b, models, wmodel, Wl, local, args.workload)
     # settle + warm-up (untimed)
     for bb in [b] + [c[0] for c in chunks]:
         bb.step(cfg, args.settle)
@@ -390,24 +513,28 @@ def main():
             c[0].step(cfg, args.steps)
     clocks["remeasured"] = remeasured
     t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    n_all = torch.tensor([float(Wl)], dtype=torch.float64, device=f"cuda:{local}")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(n_all, op=dist.ReduceOp.SUM)
     ms_max = float(t.item())
-    total_worlds = W * ws
+    total_worlds = int(n_all.item())
     value = total_worlds * args.steps / (ms_max / 1e3)
 
     # ---- roofline pass: per-world n, iterations and kernel of a few more
-    # (statistically identical) steps for the algorithmic byte model
+    # (statistically identical) steps for the algorithmic models
     rsteps = max(5, min(10, args.steps))
-    bytes_dense = bytes_cr = bytes_path = flops = 0.0
+    bytes_dense = bytes_cr = bytes_path = flops = smem_dense = smem_cr = 0.0
     kern_count = {}
+    conv_frac = []
     for _ in range(rsteps):
         b.step(cfg, 1)
         d = b.diagnostics()
         kinds = b.kernels()
-        n = np.array([d[w].n_rows for w in range(W)])
-        it = np.array([d[w].iterations for w in range(W)])
-        cri = np.array([d[w].cr_iterations for w in range(W)])
+        n = np.array([d[w].n_rows for w in range(Wl)])
+        it = np.array([d[w].iterations for w in range(Wl)])
+        cri = np.array([d[w].cr_iterations for w in range(Wl)])
+        conv_frac.append(float(np.mean([d[w].converged for w in range(Wl)])))
         on_cr = np.array([k == "cr" for k in kinds])
         on_dense = np.array([k in ("dense", "supernodal", "supernodal+dense") for k in kinds])
         for k in kinds:
@@ -416,22 +543,33 @@ def main():
         bytes_cr += float((algorithmic_bytes_cr(n, nb_w, it, 2 * it + cri) * on_cr).sum())
         bytes_path += float((algorithmic_bytes_path(n, nb_w, it) * on_dense).sum())
         flops += float(algorithmic_flops(n, it).sum())
+        for w in range(Wl):
+            sb = smem_bytes_per_world(kinds[w], n[w], it[w], 2 * it[w] + cri[w], plan_slots[wmodel[w]],
+                                      plan_terms[wmodel[w]])
+            if kinds[w] == "cr":
+                smem_cr += sb
+            else:
+                smem_dense += sb
     # kernel-family times per step from the timed region itself
     tim = tim_timed
     launches_per_step = tim["launches"] / args.steps
     dense_ms = tim["dense_ms"] / args.steps
     cr_ms = tim["matrix_free_ms"] / args.steps
     step_ms_fam = (tim["assemble_ms"] + tim["dense_ms"] + tim["matrix_free_ms"] + tim["recover_ms"]) / args.steps
-    peak, peak_kind = measured_peaks()
+    hbm_peak, hbm_peak_kind = measured_peaks()
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    smem_peak = 128.0 * nsm * sm_mhz * 1e6 / 1e9  # GB/s: 128 B/clk/SM shared-memory pipe
     if cr_ms > dense_ms:
-        fam, fam_ms, fam_bytes = "cr", cr_ms, bytes_cr / rsteps
+        fam, fam_ms, fam_bytes, fam_smem = "cr", cr_ms, bytes_cr / rsteps, smem_cr / rsteps
         kname = ("cr_op_kernel (K2b: PADMM + warm-started Conjugate Residual over the matrix-free Delassus "
                  "operator, P J register-resident)")
-        note = ("SURVEY.md §8d matrix-free model with the applies executed (the reference re-reads the baked "
-                "rows every apply); the device keeps P J in registers and the n-vectors in shared memory, so "
-                "HBM is not the binding roof (see DESIGN.md)")
+        note = ("bound by shared memory and block-barrier latency: P J lives in registers, the CR vectors in "
+                "registers and shared memory; achieved = 4 doubles per incidence per apply (IncOp) / the K2b "
+                "event time; operand_touch = the SURVEY §8d HBM model (the reference re-reads the baked rows "
+                "every apply), which the device does not stream from HBM")
     else:
-        fam, fam_ms, fam_bytes = "dense", dense_ms, bytes_dense / rsteps
+        fam, fam_ms, fam_bytes, fam_smem = "dense", dense_ms, bytes_dense / rsteps, smem_dense / rsteps
         nd, nh, ns = (kern_count.get(k, 0) for k in ("dense", "supernodal+dense", "supernodal"))
         if nh >= max(nd, ns):
             kname = ("dense_kernel (K2 after the K2f supernodal factor kernel: L^-1 + explicit-inverse PADMM, "
@@ -440,15 +578,19 @@ def main():
             kname = "dense_kernel (K2: Delassus assembly + Cholesky + explicit-inverse PADMM, smem-resident)"
         else:
             kname = "sparse_kernel (K2s: supernodal sparse LLT + PADMM, one warp per world)"
-        note = ("operand-touch model of SURVEY.md §8d (the reference's dense algorithm); the factor and X are "
-                "shared-memory resident, so HBM is not the binding roof (see DESIGN.md)")
-    achieved = fam_bytes / (fam_ms / 1e3) / 1e9
+        note = ("the factor and X = L^-1 are shared-memory resident: achieved = the PADMM solve passes' shared-"
+                "memory bytes (X read twice per iteration) / the family event time, against the 128 B/clk/SM "
+                "shared-memory pipe at the sampled SM clock; operand_touch = the SURVEY §8d HBM operand-touch "
+                "model of the reference's dense algorithm (not DRAM traffic: ncu DRAM bytes are in `traffic`)")
+    achieved_smem = fam_smem / (fam_ms / 1e3) / 1e9
+    operand_touch = fam_bytes / (fam_ms / 1e3) / 1e9
     worlds_in_launch = sum(v for k, v in kern_count.items() if (k == "cr") == (fam == "cr") and k != "none") / rsteps
     traffic, traffic_src, onchip = ncu_traffic(kname.split(" ")[0], args.workload, worlds_in_launch)
     d = b.diagnostics()
-    rows_mean = float(np.mean([d[w].n_rows for w in range(W)]))
+    rows_mean = float(np.mean([d[w].n_rows for w in range(Wl)]))
     from paper_2603_16536_b200 import sharding
-    run_stats = sharding.reduce_stats(dist, sharding.local_stats(d, W), device=f"cuda:{local}")
+    run_stats = sharding.reduce_stats(dist, sharding.local_stats(d, Wl), device=f"cuda:{local}")
+    run_stats["converged_fraction"] = run_stats["converged"] / max(1.0, run_stats["worlds"])
     iters_mean = run_stats["mean_iterations"]
 
     # ---- end-to-end through the C-ABI with host (pinned) state buffers.  The
@@ -484,11 +626,12 @@ def main():
         barrier()
         e2e_ms = f0.elapsed_time(f1)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        nbytes = torch.tensor([8.0 * (b.pose_len + b.twist_len)], dtype=torch.float64, device=f"cuda:{local}")
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            dist.all_reduce(nbytes, op=dist.ReduceOp.SUM)
         e2e = {"value": total_worlds * args.steps / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": 8 * (b.pose_len + b.twist_len) * ws,
-               "d2h_bytes_per_step": 8 * (b.pose_len + b.twist_len) * ws,
+               "h2d_bytes_per_step": int(nbytes.item()), "d2h_bytes_per_step": int(nbytes.item()),
                "what": "per step and per chunk (a WorldBatch per chunk, one stream each; up to three chunks "
                        "that each fill the GPU 8x over for the dense workloads, one for the matrix-free ones): "
                        "H2D poses+twists from pinned host memory, batch step, D2H poses+twists; one chunk's "
@@ -496,11 +639,13 @@ def main():
         del halves
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         try:
-            cpu = cpu_baseline(args, wl, cfg, quick=True)
+            cpu = cpu_baseline(args, wl, cfg)
         except Exception as ex:  # the oracle is test infrastructure; report, don't fail the bench
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
+    if dist is not None:
+        dist.barrier()  # the other ranks wait here while rank 0 times the CPU sample
 
     if rank == 0:
         out = {
@@ -511,19 +656,25 @@ def main():
                        "global_worlds": total_worlds, "models": [m.name for m in models],
                        "bodies": [m.n_bodies for m in models], "joints": [m.info.n_joints for m in models],
                        "loops": [m.n_loops for m in models],
-                       "rows_mean": rows_mean, "padmm_iterations_mean": iters_mean, "dt": cfg.dt,
+                       "rows_mean": rows_mean, "padmm_iterations_mean": iters_mean,
+                       "converged_fraction": float(np.mean(conv_frac)), "dt": cfg.dt,
                        "integrator": cfg.integrator, "backend": cfg.backend, "settle_steps": args.settle,
                        "kernels": {k: v / rsteps for k, v in kern_count.items()},
                        "jitter": "mt19937_64(seed=1), normal(0,1e-3) (main.cpp:199-211)",
                        "l2": "not flushed: per-step scratch (rows, factors, caches) of all worlds exceeds the "
                              "126 MB L2",
-                       "parallelism": f"worlds sharded over {ws} GPU(s), no data-path collective"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_kind": peak_kind, "kernel": kname, "onchip": onchip,
+                       "parallelism": f"worlds dealt over {ws} GPU(s) by model (sharding.deal), no data-path "
+                                      f"collective"},
+            "roofline": {"bound": "smem", "achieved": achieved_smem, "peak": smem_peak, "unit": "GB/s",
+                         "frac": achieved_smem / smem_peak,
+                         "peak_kind": f"128 B/clk/SM x {nsm} SMs x {sm_mhz:.0f} MHz (sampled SM clock)",
+                         "traffic": traffic, "traffic_source": traffic_src, "kernel": kname, "onchip": onchip,
                          "kernel_ms_per_launch": fam_ms, "kernel_share_of_step": fam_ms / step_ms_fam,
-                         "algorithmic_bytes_per_launch": fam_bytes,
-                         "path_bytes_per_step": bytes_path / rsteps if fam == "dense" else None,
+                         "algorithmic_smem_bytes_per_launch": fam_smem,
+                         "operand_touch": {"achieved": operand_touch, "peak": hbm_peak, "unit": "GB/s",
+                                           "frac": operand_touch / hbm_peak, "peak_kind": hbm_peak_kind,
+                                           "bytes_per_launch": fam_bytes,
+                                           "path_bytes_per_step": bytes_path / rsteps if fam == "dense" else None},
                          "note": note,
                          "fp64": {"achieved_tflops": flops / rsteps / (step_ms_fam / 1e3) / 1e12,
                                   "peak_tflops": 37.0, "peak_kind": "nominal B200 FP64"}},

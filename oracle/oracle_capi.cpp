@@ -5,6 +5,7 @@
 // implementations through the same calls.  Loaded with ctypes from tests/,
 // __graft_entry__.smoke() and bench.py's cpu_baseline leg only.
 #include <cstring>
+#include <random>
 #include <string>
 
 #include "../include/kamino_b200.h"
@@ -353,6 +354,26 @@ int or_batch_get_caches(void* bp, int32_t w, double* jlam, double* jz, int32_t* 
     }
   }
   return (k > lcap || n > ccap) ? KD_ERR_CAPACITY : KD_OK;
+}
+
+// The reference bench's initial-twist jitter (tools/main.cpp:199-211): one
+// std::mt19937_64(seed) stream and normal_distribution<double>(0, sigma) for
+// the whole batch, world-major, per body, k = 0..2: linear[k] then angular[k];
+// applied only when seed != 0.  (The bench's reference arm uses this, so it
+// never loads the product library.)
+int or_bench_jitter(uint64_t seed, double sigma, int32_t n_worlds, const int32_t* n_bodies, double* twists6) {
+  if (!n_bodies || !twists6) return KD_ERR_INVALID_ARGUMENT;
+  if (seed == 0) return KD_OK;
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> jitter(0.0, sigma);
+  int64_t off = 0;
+  for (int w = 0; w < n_worlds; ++w)
+    for (int b = 0; b < n_bodies[w]; ++b, off += 6)
+      for (int k = 0; k < 3; ++k) {
+        twists6[off + k] += jitter(rng);
+        twists6[off + 3 + k] += jitter(rng);
+      }
+  return KD_OK;
 }
 
 int or_batch_set_active(void* bp, const uint8_t* active) {

@@ -14,6 +14,15 @@ description drives the device path and the CPU oracle.
 * `closed_chain(n_cells)` — config 4: a ladder of parallelogram cells hanging
   from the world (n > 300 rows -> matrix-free CR path).
 * `sphere_pile(n)` — config 5 substitute: spheres in a bin of 5 planes.
+* `stewart_tower(stages)` — config 4 as SURVEY §8d specifies it: a spatial
+  parallel manipulator, a stack of 6-6 Stewart platforms with
+  spherical-prismatic-spherical legs (PD + damping on every leg, limits on the
+  bottom stage).  12 stages: 156 bodies, 216 joints, 936 rows + 12 limit-row
+  capacity -> matrix-free CR path.
+* `mixed_joints()` — every joint type and joint-dynamics row kind in one
+  small world: fixed, spherical, revolute and prismatic joints, PD, armature
+  and damping rows, and a prismatic limit that is active from the start
+  (the linear 0.001 m margin, constraints.cpp:218-229).
 """
 from __future__ import annotations
 
@@ -156,6 +165,79 @@ def closed_chain(n_cells=22, link=0.2, mass=0.1) -> SceneDescription:
         prev_l, prev_r = l, r
     # give the ladder a push so it swings
     b.root["bodies"][-1]["linear_velocity"] = [0.5, 0.0, 0.0]
+    return b.scene()
+
+
+def stewart_tower(stages=12, radius_base=0.3, radius_top=0.25, height=0.4, kp=3000.0, kd=60.0, damping=5.0,
+                  platform_mass=1.0, leg_mass=0.1) -> SceneDescription:
+    """Config 4 ("a multi-leg parallel manipulator with spherical
+    joints", n ~ 1000, ~150 bodies): `stages` 6-6 Stewart platforms stacked on
+    the ground.  Every leg is two bodies (cylinder, piston) joined by a
+    prismatic joint along the leg (PD-held at its build length, plus a damping
+    row), with spherical joints to the platform below (or the world) and the
+    platform above.  Bottom-stage legs have a [-0.0005, 0.05] m stroke limit,
+    so their lower limit sits inside the 0.001 m margin from the start.  Per
+    stage: 13 bodies, 18 joints, 6 x (3 + 5 + 3) + 12 = 78 rows."""
+    b = _Builder("stewart_tower")
+    lower = "world"
+    zl = 0.0
+    for k in range(stages):
+        zu = zl + height
+        plat = f"plat{k}"
+        b.body(plat, platform_mass, (2 * radius_top, 2 * radius_top, 0.04), [0.0, 0.0, zu])
+        for i in range(6):
+            a = math.radians(60.0 * i)
+            t = math.radians(60.0 * i + (30.0 if i % 2 == 0 else -30.0))
+            B = [radius_base * math.cos(a), radius_base * math.sin(a), zl]
+            T = [radius_top * math.cos(t), radius_top * math.sin(t), zu]
+            d = _sub(T, B)
+            length = math.sqrt(sum(x * x for x in d))
+            u = [x / length for x in d]
+            M = [B[q] + 0.5 * d[q] for q in range(3)]
+            cyl, pis = f"leg{k}_{i}_cyl", f"leg{k}_{i}_pis"
+            b.body(cyl, leg_mass, (0.03, 0.03, 0.5 * length), [B[q] + 0.25 * d[q] for q in range(3)])
+            b.body(pis, leg_mass, (0.02, 0.02, 0.5 * length), [B[q] + 0.75 * d[q] for q in range(3)])
+            b.joint(f"s{k}_{i}_lo", lower, cyl, B, X, type="spherical")
+            kw = dict(type="prismatic", kp=kp, kd=kd, damping=damping)
+            if k == 0:
+                kw["limits"] = [-0.0005, 0.05]
+            b.joint(f"p{k}_{i}", cyl, pis, M, u, **kw)
+            b.joint(f"s{k}_{i}_hi", pis, plat, T, X, type="spherical")
+        lower, zl = plat, zu
+    # a slow twist of the top platform sets the tower moving
+    b.root["bodies"][-13]["angular_velocity"] = [0.0, 0.0, 0.2]
+    return b.scene()
+
+
+def mixed_joints() -> SceneDescription:
+    """Every joint type and joint-dynamics row in one world (constraints.cpp:
+    90-108 fixed / prismatic / spherical rows, 160-187 coordinate-rate rows,
+    256-274 PD / armature / damping, 218-229 limits with the linear margin).
+
+    carriage --prismatic x (PD to 0.02, limits +-0.1)--> world
+    cap      --fixed--> carriage
+    arm1     --spherical--> carriage          (swinging in 3D)
+    arm2     --revolute y (armature 0.05, damping 0.1, limits)--> arm1
+    plunger  --prismatic along arm2 (armature 0.2, damping 0.5, limits [-0.0005, 0.05])--> arm2
+    slider   --prismatic y (limits [-0.0008, 0.05], pushed into its lower limit)--> world
+    """
+    b = _Builder("mixed_joints")
+    b.body("carriage", 1.0, (0.2, 0.1, 0.05), [0.0, 0.0, 1.0])
+    b.joint("slide_x", "world", "carriage", [0.0, 0.0, 1.0], X, type="prismatic", kp=20.0, kd=1.0, target=0.02,
+            limits=[-0.1, 0.1])
+    b.body("cap", 0.3, (0.05, 0.05, 0.05), [0.0, 0.0, 1.05])
+    b.joint("weld", "carriage", "cap", [0.0, 0.0, 1.03], X, type="fixed")
+    b.body("arm1", 0.5, (0.03, 0.03, 0.4), [0.0, 0.0, 0.8])
+    b.joint("ball", "carriage", "arm1", [0.0, 0.0, 1.0], X, type="spherical")
+    b.body("arm2", 0.4, (0.03, 0.03, 0.3), [0.0, 0.0, 0.45])
+    b.joint("elbow", "arm1", "arm2", [0.0, 0.0, 0.6], Y, armature=0.05, damping=0.1, limits=[-1.0, 1.0])
+    b.body("plunger", 0.2, (0.02, 0.02, 0.1), [0.0, 0.0, 0.25])
+    b.joint("plunge", "arm2", "plunger", [0.0, 0.0, 0.3], Z, type="prismatic", armature=0.2, damping=0.5,
+            limits=[-0.0005, 0.05])
+    b.body("slider", 0.5, (0.1, 0.1, 0.1), [0.5, 0.0, 0.5])
+    b.joint("slide_y", "world", "slider", [0.5, 0.0, 0.5], Y, type="prismatic", limits=[-0.0008, 0.05])
+    b.root["bodies"][2]["angular_velocity"] = [1.0, 0.5, 0.0]   # arm1
+    b.root["bodies"][5]["linear_velocity"] = [0.0, -0.1, 0.0]   # slider into its lower limit
     return b.scene()
 
 

@@ -1,11 +1,15 @@
 """World sharding across GPUs (one process per GPU) — SURVEY.md §8e.
 
-Worlds are independent, so the data path has no collective: rank r owns a
-contiguous block of global world ids and steps it on its own device.  The
-global world order, and therefore every world's initial state (including the
-reference bench jitter stream, main.cpp:199-211, which is drawn world-major
-over the whole batch), is independent of the GPU count.  The only collective
-is the end-of-run reduction of a few statistics (`reduce_stats`).
+Worlds are independent, so the data path has no collective.  The global world
+list is built in the reference order (main.cpp:199-211: one jitter stream,
+world-major over the whole batch), so every world's initial state is
+independent of the GPU count.  `deal` bins the global worlds by a key (the
+model, i.e. the device capacity class) and deals every bin round-robin over
+the ranks, so each GPU gets the same mix of world sizes (for the
+heterogeneous config, a contiguous block would depend on where the block
+boundary falls in the w % 3 cycle; a plain w % ranks deal would give rank r
+only model r % 3 when the rank count is a multiple of 3).  The only
+collective is the end-of-run reduction of a few statistics (`reduce_stats`).
 """
 from __future__ import annotations
 
@@ -22,6 +26,39 @@ def split_range(n_global: int, rank: int, world_size: int) -> range:
     base, extra = divmod(n_global, world_size)
     start = rank * base + min(rank, extra)
     return range(start, start + base + (1 if rank < extra else 0))
+
+
+def deal(keys, world_size: int, rank: int) -> list:
+    """Global world ids of `rank`: worlds grouped by keys[w] (bins in order of
+    first appearance), each bin dealt round-robin over the ranks.  Every rank
+    gets floor or ceil of |bin| / world_size worlds of every bin; the ids are
+    returned ascending (the rank's batch keeps the global order)."""
+    bins = {}
+    for w, k in enumerate(keys):
+        bins.setdefault(k, []).append(w)
+    mine = []
+    for ids in bins.values():
+        mine.extend(ids[rank::world_size])
+    return sorted(mine)
+
+
+def jitter_worlds(world_twists, worlds, seed: int = 1, sigma: float = 1e-3, jitter=None):
+    """Twists of the global worlds `worlds` (any ascending id list) after the
+    reference bench jitter (main.cpp:199-211): the stream runs world-major over
+    global worlds [0, max id] and each listed world keeps its own block.
+    `world_twists(w)` gives global world w's initial twists; `jitter` is the
+    stream implementation (default: the product library's kd_bench_jitter)."""
+    if jitter is None:
+        from .loopdyn import bench_jitter as jitter
+    worlds = list(worlds)
+    if not worlds:
+        return np.zeros(0)
+    top = max(worlds) + 1
+    per = [np.asarray(world_twists(w), dtype=np.float64).reshape(-1) for w in range(top)]
+    nb = [p.size // 6 for p in per]
+    full = jitter(np.concatenate(per), nb, seed=seed, sigma=sigma)
+    off = np.concatenate([[0], np.cumsum([6 * n for n in nb])])
+    return np.concatenate([full[off[w]: off[w + 1]] for w in worlds])
 
 
 def jitter_slice(initial_twists: np.ndarray, n_bodies: int, worlds: range, seed: int = 1, sigma: float = 1e-3):

@@ -37,6 +37,7 @@ def lib():
             "batch_step": (C.c_int, [C.c_void_p, C.POINTER(_capi.kd_step_config), C.c_int32, C.c_int32]),
             "batch_set_trace": (C.c_int, [C.c_void_p, C.c_int32]),
             "batch_get_caches": _capi.KD_ONLY["batch_get_caches"],
+            "bench_jitter": _capi.KD_ONLY["bench_jitter"],
             "batch_get_history": (C.c_int, [C.c_void_p, C.c_int32, _capi.c_double_p]),
             "batch_energy": (C.c_int, [C.c_void_p, C.c_int32, _capi.c_double_p, _capi.c_double_p]),
             "fd_check": (C.c_double, [C.c_void_p, _capi.c_double_p, C.c_double]),
@@ -208,6 +209,16 @@ class OracleBatch:
         ke, pe = C.c_double(), C.c_double()
         lib().or_batch_energy(self.handle, w, C.byref(ke), C.byref(pe))
         return ke.value, pe.value
+
+
+def bench_jitter(twists, n_bodies_per_world, seed=1, sigma=1e-3):
+    """The reference bench jitter stream (main.cpp:199-211) from the oracle
+    library (same arithmetic as kd_bench_jitter; the reference arm of bench.py
+    uses this one so that it never loads the product library)."""
+    t = np.ascontiguousarray(twists, dtype=np.float64).copy()
+    nb = np.ascontiguousarray(n_bodies_per_world, dtype=np.int32)
+    _check(lib().or_bench_jitter(int(seed), float(sigma), len(nb), _capi.i32ptr(nb), _capi.dptr(t)))
+    return t
 
 
 def rows_to_numpy(rows, n):
