@@ -524,7 +524,7 @@ def main():
     # ---- roofline pass: per-world n, iterations and kernel of a few more
     # (statistically identical) steps for the algorithmic models
     rsteps = max(5, min(10, args.steps))
-    bytes_dense = bytes_cr = bytes_path = flops = smem_dense = smem_cr = 0.0
+    bytes_dense = bytes_cr = bytes_path = flops_dense = flops_cr = smem_dense = smem_cr = 0.0
     kern_count = {}
     conv_frac = []
     for _ in range(rsteps):
@@ -542,7 +542,8 @@ def main():
         bytes_dense += float((algorithmic_bytes_k2(n, nb_w, it) * on_dense).sum())
         bytes_cr += float((algorithmic_bytes_cr(n, nb_w, it, 2 * it + cri) * on_cr).sum())
         bytes_path += float((algorithmic_bytes_path(n, nb_w, it) * on_dense).sum())
-        flops += float(algorithmic_flops(n, it).sum())
+        flops_dense += float((algorithmic_flops(n, it) * on_dense).sum())
+        flops_cr += float((48.0 * n * (2 * it + cri) * on_cr).sum())
         for w in range(Wl):
             sb = smem_bytes_per_world(kinds[w], n[w], it[w], 2 * it[w] + cri[w], plan_slots[wmodel[w]],
                                       plan_terms[wmodel[w]])
@@ -676,8 +677,10 @@ def main():
                                            "bytes_per_launch": fam_bytes,
                                            "path_bytes_per_step": bytes_path / rsteps if fam == "dense" else None},
                          "note": note,
-                         "fp64": {"achieved_tflops": flops / rsteps / (step_ms_fam / 1e3) / 1e12,
-                                  "peak_tflops": 37.0, "peak_kind": "nominal B200 FP64"}},
+                         "fp64": {"achieved_tflops": (flops_cr if fam == "cr" else flops_dense) / rsteps
+                                  / (fam_ms / 1e3) / 1e12, "peak_tflops": 37.0, "peak_kind": "nominal B200 FP64",
+                                  "model": "CR: 48 n flops per apply (SURVEY §8d)" if fam == "cr" else
+                                  "dense: n^3/3 + I (2 n^2 + 20 n) (SURVEY §8d)"}},
             "clocks": clocks,
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "e2e": e2e,

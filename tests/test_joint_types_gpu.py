@@ -53,13 +53,13 @@ def _pair(sc, n_worlds, monkeypatch, sparse_env=None, seed=5):
     return gb, ob
 
 
-def _rows_match(gb, ob, w):
+def _rows_match(gb, ob, w, tol=1e-12):
     rg, ro = gb.dump_rows(w), ob.dump_rows(w)
     assert len(rg["kind"]) == len(ro["kind"])
     assert (rg["body"] == ro["body"]).all()
     assert (rg["kind"] == ro["kind"]).all()
     for key in ("J", "bias", "reg", "scale", "vf"):
-        assert rel(rg[key], ro[key]) < 1e-12, key
+        assert rel(rg[key], ro[key]) < tol, key
     for key in ("lambda", "z"):
         assert rel(rg[key], ro[key]) < 1e-9, key
     assert (gb.dump_limits(w) == ob.dump_limits(w)).all()
@@ -128,8 +128,8 @@ def test_stewart_tower_cr_parity(monkeypatch):
             assert dg[w].n_rows == do[w].n_rows and dg[w].n_limits == do[w].n_limits
             assert dg[w].iterations == do[w].iterations, (k, w)
             assert abs(dg[w].cr_iterations - do[w].cr_iterations) <= 2
-        if k < 2:
-            _rows_match(gb, ob, 0)
+        if k < 2:  # identical inputs at k = 0; after one step the states differ at rounding level
+            _rows_match(gb, ob, 0, 1e-12 if k == 0 else 1e-10)
     assert gb.kernels() == ["cr", "cr"]
     pg, tg, _ = gb.get_state()
     po, to, _ = ob.get_state()
