@@ -297,6 +297,64 @@ int kd_batch_set_caches(kd_batch* batch, int32_t world, const double* joint_lamb
                         int32_t joint_len, int32_t joint_valid, const kd_limit_cache_entry* limits,
                         int32_t n_limits, const kd_contact_cache_entry* contacts, int32_t n_contacts);
 
+/* ---- solver-level entry points (unit parity on pre-assembled systems) -------- */
+/* One pre-assembled system: ConstraintSet (constraints.hpp:39-65: rows in the
+ * order bilateral + joint-dynamics | limits | contacts, so the cone product is
+ * one Bilateral group, one Nonnegative(1) group per limit row and one
+ * SecondOrder(3, mu) group per contact), the per-body inverse mass data of
+ * world_inertias (BodyInertiaWorld, delassus.hpp:13-18) and the
+ * Preconditioner scale (delassus.hpp:26-29).  All arrays are caller-owned. */
+typedef struct kd_solve_problem {
+  int32_t n_rows;
+  int32_t n_bodies;
+  int32_t n_bilateral;        /* rows in the leading Bilateral group */
+  int32_t n_limits;           /* Nonnegative rows that follow */
+  int32_t n_contacts;         /* SOC triples that follow (3 rows each) */
+  int32_t pad;
+  const int32_t* body;        /* 2 per row: body_a, body_b (-1: none) */
+  const double* jacobian;     /* 12 per row: block_a[6], block_b[6] ([linear; angular]) */
+  const double* reg;          /* n_rows: R */
+  const double* scale;        /* n_rows: P */
+  const double* mu;           /* n_contacts friction coefficients (may be NULL if none) */
+  const double* inv_mass;     /* n_bodies */
+  const double* inv_inertia;  /* 9 per body, world frame, row-major */
+  const double* rhs;          /* n_rows: padmm_solve's v_f (preconditioned), or cr_solve's rhs */
+  const double* x0;           /* n_rows or NULL: PadmmInit::x0 / cr_solve's warm start x */
+  const double* z0;           /* n_rows or NULL: PadmmInit::z0 */
+} kd_solve_problem;
+
+/* build_backend + padmm_solve (delassus.hpp:103-105, padmm.hpp:64-67) for a
+ * batch of systems on device `device`: backend Dense (any n, the dense
+ * kernel: assembly + Cholesky + PADMM), MatrixFree (the CR kernels, cr_budget
+ * per solve) or Auto (Dense iff n <= 300, delassus.cpp:204-206); the operator
+ * is D = P (J M^-1 J^T + R) P + eta_rho I.  cfg supplies PadmmConfig (eta,
+ * rho, eps, max_iters, acceleration, restart, fixed_iteration_mode); other
+ * fields are ignored.  Problem p's lambda (PadmmResult::lambda, preconditioned
+ * y) and z go to lambda[off_p..], z[off_p..] with off_p the prefix sum of
+ * n_rows; diags[p] gets SolveDiagnostics (iterations, restarts, converged,
+ * r_p, r_d, r_c, cr_iterations, cr_breakdown) and n_rows.  history (may be
+ * NULL) is [n_problems][history_capacity]: the combined residual per
+ * iteration, -1 after the last.  A non-SPD dense system -> KD_ERR_SPD_FAILURE
+ * (the reference's runtime_error, delassus.cpp:209-215). */
+int kd_padmm_solve_batched(int32_t device, const kd_solve_problem* problems, int32_t n_problems, double eta_rho,
+                           int32_t backend, int32_t cr_budget, const kd_step_config* cfg, double* lambda,
+                           double* z, kd_step_diag* diags, double* history, int32_t history_capacity);
+/* cr_solve(bake_jacobian(cs, inertias, precond, eta_rho), rhs, x, max_iters,
+ * &history) (delassus.hpp:82-83, delassus.cpp:130-187) per problem: x0 is
+ * the warm start (NULL: zeros), x[off_p..] the result; iterations,
+ * breakdown (CrResult::breakdown, raw) and residual_norm per problem (each
+ * may be NULL); history (may be NULL): [n_problems][history_capacity] of
+ * |r| (initial, then after every update), -1 after the last. */
+int kd_cr_solve_batched(int32_t device, const kd_solve_problem* problems, int32_t n_problems, double eta_rho,
+                        int32_t max_iters, double* x, int32_t* iterations, uint8_t* breakdown, double* residual_norm,
+                        double* history, int32_t history_capacity);
+/* assemble_constraints (constraints.hpp:91-94) for every active world of the
+ * batch at its current state: runs the device assembly (collide, rows,
+ * preconditioner, warm start) without solving or integrating; the rows,
+ * contacts and limit keys are then readable with kd_batch_dump_* and
+ * kd_batch_get_diagnostics (n_rows, contact_count, n_limits). */
+int kd_batch_assemble(kd_batch* batch, const kd_step_config* cfg);
+
 /* ---- one-step introspection for parity (ConstraintSet constraints.hpp:39-65) -- */
 typedef struct kd_row_dump {
   int32_t body_a, body_b;

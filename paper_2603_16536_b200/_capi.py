@@ -186,6 +186,15 @@ class kd_contact_cache_entry(C.Structure):
                 ("impulse", C.c_double * 3), ("dual", C.c_double * 3)]
 
 
+class kd_solve_problem(C.Structure):
+    _fields_ = [("n_rows", C.c_int32), ("n_bodies", C.c_int32), ("n_bilateral", C.c_int32),
+                ("n_limits", C.c_int32), ("n_contacts", C.c_int32), ("pad", C.c_int32),
+                ("body", C.POINTER(C.c_int32)), ("jacobian", C.POINTER(C.c_double)), ("reg", C.POINTER(C.c_double)),
+                ("scale", C.POINTER(C.c_double)), ("mu", C.POINTER(C.c_double)),
+                ("inv_mass", C.POINTER(C.c_double)), ("inv_inertia", C.POINTER(C.c_double)),
+                ("rhs", C.POINTER(C.c_double)), ("x0", C.POINTER(C.c_double)), ("z0", C.POINTER(C.c_double))]
+
+
 _H = C.c_void_p
 SIGNATURES = {
     "model_build": (C.c_int, [C.POINTER(kd_scene_desc), C.POINTER(C.c_void_p)]),
@@ -238,6 +247,12 @@ KD_ONLY = {
     "model_sparse_plan_info": (C.c_int, [_H, c_int64_p]),
     "model_sparse_plan_selftest": (C.c_int, [_H, C.c_uint64, c_double_p]),
     "model_set_contact_capacity": (C.c_int, [_H, C.c_int32]),
+    "padmm_solve_batched": (C.c_int, [C.c_int32, C.POINTER(kd_solve_problem), C.c_int32, C.c_double, C.c_int32,
+                                      C.c_int32, C.POINTER(kd_step_config), c_double_p, c_double_p,
+                                      C.POINTER(kd_step_diag), c_double_p, C.c_int32]),
+    "cr_solve_batched": (C.c_int, [C.c_int32, C.POINTER(kd_solve_problem), C.c_int32, C.c_double, C.c_int32,
+                                   c_double_p, c_int32_p, c_uint8_p, c_double_p, c_double_p, C.c_int32]),
+    "batch_assemble": (C.c_int, [_H, C.POINTER(kd_step_config)]),
     "batch_get_cache_sizes": (C.c_int, [_H, C.c_int32, c_int32_p, c_int32_p, c_int32_p, c_int32_p]),
     "batch_get_caches": (C.c_int, [_H, C.c_int32, c_double_p, c_double_p, c_int32_p,
                                    C.POINTER(kd_limit_cache_entry), C.c_int32, c_int32_p,

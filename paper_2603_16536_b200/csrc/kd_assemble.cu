@@ -666,44 +666,10 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
   }
   __syncwarp();
 
-  // ---- 7. per-body row lists in ascending row order (for J^T lambda and the CR scatter):
-  // a counting sort over the incidence codes 2r + side, 32 codes per pass; lanes
-  // holding the same body in a pass are grouped by __match_any_sync, so every
-  // body's list comes out in ascending code (= row) order.
+  // ---- 7. per-body row lists in ascending row order (for J^T lambda and the CR scatter)
   int32_t* cptr = bv.csr_ptr + W.body_off + w;
   int32_t* clist = bv.csr + 2 * R0;
-  const int ncode = 2 * n;
-  for (int b = lane; b <= M.nb; b += 32) cptr[b] = 0;
-  __syncwarp();
-  for (int c0 = 0; c0 < ncode; c0 += 32) {  // counts into cptr[b + 1]
-    const int code = c0 + lane;
-    const int body = code < ncode ? rb[code] : -1;
-    const unsigned grp = __match_any_sync(0xffffffffu, body);
-    if (body >= 0 && lane == __ffs(grp) - 1) cptr[body + 1] += __popc(grp);
-    __syncwarp();
-  }
-  int run = 0;  // exclusive scan over indices 1..nb: cptr[b + 1] = start of body b
-  for (int base = 1; base <= M.nb; base += 32) {
-    const int b = base + lane;
-    const int cnt = b <= M.nb ? cptr[b] : 0;
-    int excl;
-    const int tot = warp_exclusive_sum(cnt, lane, excl);
-    __syncwarp();
-    if (b <= M.nb) cptr[b] = run + excl;
-    run += tot;
-  }
-  __syncwarp();
-  // cptr[b + 1] is body b's cursor while filling: it ends at the start of body
-  // b + 1, which is its final value (cptr[0] = 0)
-  for (int c0 = 0; c0 < ncode; c0 += 32) {
-    const int code = c0 + lane;
-    const int body = code < ncode ? rb[code] : -1;
-    const unsigned grp = __match_any_sync(0xffffffffu, body);
-    if (body >= 0) clist[cptr[body + 1] + __popc(grp & ((1u << lane) - 1))] = code;
-    __syncwarp();
-    if (body >= 0 && lane == __ffs(grp) - 1) cptr[body + 1] += __popc(grp);
-    __syncwarp();
-  }
+  const int run = warp_incidence_lists(rb, n, M.nb, cptr, clist, lane);
   bool sn_ok = sp.sparse && M.sn;
   if (sn_ok) {
     const int32_t* pslot = bv.sn_pair_slot + bv.snplan[W.model].pair_off;

@@ -101,6 +101,8 @@ constexpr int kSnAutoMaxSlots = 32;     // supernodal kernel by default up to on
 
 }  // namespace
 
+int kd::set_last_error(int code, const std::string& msg) { return fail(code, msg); }
+
 struct kd_batch;
 namespace {
 cudaError_t to_dev(kd_batch* b, void* dst, const void* src, size_t bytes);
@@ -929,6 +931,7 @@ static StepParams step_params(const kd_batch* b, const kd_step_config* c) {
   sp.backend = c->backend;
   sp.sparse = b->sparse ? 1 : 0;
   sp.sn_handoff = b->sn_handoff ? 1 : 0;
+  sp.eta_rho = c->eta + c->rho;
   sp.nest_beta = b->d_nest;
   return sp;
 }
@@ -1150,6 +1153,20 @@ int kd_batch_step(kd_batch* b, const kd_step_config* c, int32_t n_steps) {
   const int rc = enqueue_steps(b, c, n_steps);
   if (rc != KD_OK) return rc;
   return kd_batch_sync(b);
+}
+
+int kd_batch_assemble(kd_batch* b, const kd_step_config* c) {
+  if (!b || !c) return fail(KD_ERR_INVALID_ARGUMENT, "null argument");
+  if (b->n_worlds == 0) return KD_OK;
+  KD_CK(cudaSetDevice(b->device));
+  const int nrc = ensure_nest_table(b, c->max_iters);
+  if (nrc != KD_OK) return nrc;
+  const StepParams sp = step_params(b, c);
+  KD_CK(cudaMemsetAsync(b->d_err, 0, 16, b->stream));
+  launch_assemble(b->view, sp, b->stream);
+  KD_CK(cudaGetLastError());
+  KD_CK(cudaStreamSynchronize(b->stream));
+  return KD_OK;
 }
 
 int kd_batch_stream(kd_batch* b, void** stream) {

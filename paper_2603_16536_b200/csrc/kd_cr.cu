@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
   int32_t* cl_s = cp_s + nb + 1;
   const bool staged = (ja_s - smem) + 12 * n + (4 * n + nb + 2) / 2 + 1 <= smem_doubles;
 
-  const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
+  const double eta = sp.eta, rho = sp.rho, eta_rho = sp.eta_rho;
   const double inv_rho = 1.0 / rho;  // w = x - z_hat * (1/rho): no division in the loop
   for (int r = tid; r < n; r += NT) {
     const double p = bv.scale[R0 + r];
@@ -210,6 +210,78 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
     c.rbs = rb_s;
     c.cps = cp_s;
     c.cls = cl_s;
+  }
+  if (sp.cr_only) {
+    // ---- one cr_solve(op, rhs, x, max_iters, &history) (delassus.cpp:156-187)
+    // on the operator bake_jacobian(cs, inertias, precond, eta_rho) builds
+    // (kd_cr_solve_batched): rhs in vf, the warm start in x0; x -> lam,
+    // iterations -> cr_iterations, the raw breakdown flag -> cr_breakdown,
+    // |r| -> r_p, the residual-norm history (initial |r|, then after every
+    // update) -> hist.
+    __syncthreads();
+    const int hcap = bv.hist_cap;
+    double* rhs_ = rhs;
+    for (int r = tid; r < n; r += NT) rhs_[r] = vf[r];
+    apply_op<NT>(c, xs, ar);
+    for (int r = tid; r < n; r += NT) rr[r] = rhs_[r] - ar[r];
+    apply_op<NT>(c, rr, ar);
+    double loc = 0.0, loc2 = 0.0, loc3 = 0.0;
+    for (int r = tid; r < n; r += NT) {
+      pp[r] = rr[r];
+      ap[r] = ar[r];
+      loc += rr[r] * ar[r];
+    }
+    double rar = block_sum<NT>(loc, red);
+    for (int r = tid; r < n; r += NT) loc2 += rhs_[r] * rhs_[r];
+    const double rhs2 = block_sum<NT>(loc2, red);
+    for (int r = tid; r < n; r += NT) loc3 += rr[r] * rr[r];
+    double rn = sqrt(block_sum<NT>(loc3, red));
+    int nh = 0;
+    if (tid == 0 && nh < hcap) bv.hist[(int64_t)w * hcap + nh] = rn;
+    ++nh;
+    const double beps = 1e-30 * fmax(1.0, rhs2);
+    int iters = 0;
+    bool brk = false;
+    for (int k = 0; k < sp.cr_iters; ++k) {
+      loc = 0.0;
+      for (int r = tid; r < n; r += NT) loc += ap[r] * ap[r];
+      const double apap = block_sum<NT>(loc, red);
+      if (!(rar > beps) || !(apap > beps)) {
+        brk = true;
+        break;
+      }
+      const double alpha = rar / apap;
+      loc = 0.0;
+      for (int r = tid; r < n; r += NT) {
+        xs[r] += alpha * pp[r];
+        rr[r] -= alpha * ap[r];
+        loc += rr[r] * rr[r];
+      }
+      rn = sqrt(block_sum<NT>(loc, red));
+      if (tid == 0 && nh < hcap) bv.hist[(int64_t)w * hcap + nh] = rn;
+      ++nh;
+      apply_op<NT>(c, rr, ar);
+      loc = 0.0;
+      for (int r = tid; r < n; r += NT) loc += rr[r] * ar[r];
+      const double rar_next = block_sum<NT>(loc, red);
+      const double beta = rar_next / rar;
+      for (int r = tid; r < n; r += NT) {
+        pp[r] = rr[r] + beta * pp[r];
+        ap[r] = ar[r] + beta * ap[r];
+      }
+      rar = rar_next;
+      ++iters;
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += NT) bv.lam[R0 + r] = xs[r];
+    if (tid == 0) {
+      ws.cr_iterations = iters;
+      ws.cr_breakdown = brk ? 1 : 0;
+      ws.r_p = rn;
+      ws.iterations = 0;
+      for (int i = nh; i < hcap; ++i) bv.hist[(int64_t)w * hcap + i] = -1.0;
+    }
+    return;
   }
   const int n_jd = n - ws.n_limits - 3 * ws.n_contacts;
   const int first_contact = n_jd + ws.n_limits;
@@ -824,7 +896,7 @@ __global__ void __launch_bounds__(NT, MINB) cr_op_kernel(BatchView bv, StepParam
   double* xs = vf + n;
   double* red = xs + n;  // 2 buffers x 3 x NW
   double* opsm = red + ((2 * 3 * (NT / 32) + 1) & ~1);
-  const double eta = sp.eta, rho = sp.rho, eta_rho = eta + rho;
+  const double eta = sp.eta, rho = sp.rho, eta_rho = sp.eta_rho;
   const double inv_rho = 1.0 / rho;
   Op op;
   const bool ok = op.setup(bv, W, w, n, nb, eta_rho, opsm);
@@ -1070,6 +1142,14 @@ static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const 
   }
   cr_kernel<NT, MINB><<<count, NT, smem, s>>>(bv, sp, worlds, (int)(smem / 8), n_reg);
   return cudaGetLastError();
+}
+
+// The shared-memory CR kernel over every listed world (any n that fits one
+// CTA's shared memory), e.g. for the cr_only mode of kd_cr_solve_batched.
+cudaError_t launch_cr_shared(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap,
+                             int nbcap, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  return launch_cr_t<256, 1>(bv, sp, worlds, count, ncap, nbcap, 0, s);
 }
 
 template <class Op, int NT, int RPT, int MINB, bool PROF, bool MARK>

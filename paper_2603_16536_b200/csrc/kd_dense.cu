@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   const RowJ* rj = bv.rowj + R0;
   const int32_t* rb = bv.rbody + 2 * R0;
   const double* regg = bv.reg + R0;
-  const double eta_rho = sp.eta + sp.rho;
+  const double eta_rho = sp.eta_rho;
 
   long long t_prev = clock64();
   auto stamp = [&](int k) {

@@ -78,6 +78,51 @@ __device__ __forceinline__ int warp_exclusive_sum(int v, int lane, int& excl) {
   return __shfl_sync(0xffffffffu, incl, 31);
 }
 
+// Per-body incidence lists of a world's rows in ascending row order (the
+// accumulation order of apply_jacobian_transpose, constraints.cpp:121-129, and
+// of MatrixFreeDelassus::apply, delassus.cpp:108-113), built by one warp: a
+// counting sort over the incidence codes 2r + side, 32 codes per pass; lanes
+// holding the same body in a pass are grouped by __match_any_sync, so every
+// body's list comes out in ascending code (= row) order.  rb: 2 body ids per
+// row (-1: none).  Writes cptr[0..nb] (cptr[b]..cptr[b+1] = body b's codes in
+// clist) except cptr[nb], which the caller sets to the returned total.
+__device__ __forceinline__ int warp_incidence_lists(const int32_t* rb, int n, int nb, int32_t* cptr, int32_t* clist,
+                                                    int lane) {
+  const int ncode = 2 * n;
+  for (int b = lane; b <= nb; b += 32) cptr[b] = 0;
+  __syncwarp();
+  for (int c0 = 0; c0 < ncode; c0 += 32) {  // counts into cptr[b + 1]
+    const int code = c0 + lane;
+    const int body = code < ncode ? rb[code] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, body);
+    if (body >= 0 && lane == __ffs(grp) - 1) cptr[body + 1] += __popc(grp);
+    __syncwarp();
+  }
+  int run = 0;  // exclusive scan over indices 1..nb: cptr[b + 1] = start of body b
+  for (int base = 1; base <= nb; base += 32) {
+    const int b = base + lane;
+    const int cnt = b <= nb ? cptr[b] : 0;
+    int excl;
+    const int tot = warp_exclusive_sum(cnt, lane, excl);
+    __syncwarp();
+    if (b <= nb) cptr[b] = run + excl;
+    run += tot;
+  }
+  __syncwarp();
+  // cptr[b + 1] is body b's cursor while filling: it ends at the start of body
+  // b + 1, which is its final value (cptr[0] = 0)
+  for (int c0 = 0; c0 < ncode; c0 += 32) {
+    const int code = c0 + lane;
+    const int body = code < ncode ? rb[code] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, body);
+    if (body >= 0) clist[cptr[body + 1] + __popc(grp & ((1u << lane) - 1))] = code;
+    __syncwarp();
+    if (body >= 0 && lane == __ffs(grp) - 1) cptr[body + 1] += __popc(grp);
+    __syncwarp();
+  }
+  return run;
+}
+
 // max is exactly associative/commutative: any reduction order gives the
 // reference's serial lpNorm<Infinity> result bit for bit.
 __device__ __forceinline__ double warp_max(double v) {

@@ -31,6 +31,9 @@ struct HostModel {
   int contact_cap = 0;  // kd_model_set_contact_capacity (0: default)
 };
 
+// Sets kd_last_error()'s thread-local message; returns code.
+int set_last_error(int code, const std::string& msg);
+
 int build_host_model(const kd_scene_desc* d, HostModel& m, std::string& err, uint32_t extensions = 0);
 double host_joint_coordinate(const HostModel& m, int joint, const double* poses7);
 
@@ -40,6 +43,8 @@ cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_
                   bool global_l, cudaStream_t s);
 cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
                int nt, cudaStream_t s);
+cudaError_t launch_cr_shared(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap,
+                             int nbcap, cudaStream_t s);
 cudaError_t launch_sparse(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int per_warp,
                           int wpc, int prog_words, cudaStream_t s);
 cudaError_t launch_snfactor(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, size_t smem,

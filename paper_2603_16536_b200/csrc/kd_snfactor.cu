@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
   {
     const RowJ* rj = bv.rowj + R0;
     const double* reg = bv.reg + R0;
-    const double eta_rho = sp.eta + sp.rho;
+    const double eta_rho = sp.eta_rho;
     const SnGram* gl = bv.sn_gram + P.gram_off;
     // two entries per thread and pass, so their descriptor and J loads overlap
     auto entry = [&](const SnGram g) {

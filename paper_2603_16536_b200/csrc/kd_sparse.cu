@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256, 3) sparse_kernel(BatchView bv, StepParams
     }
     // + R on the diagonal, P scaling, + (eta+rho) I; inactive slots -> identity
     const double* reg = bv.reg + R0;
-    const double eta_rho = sp.eta + sp.rho;
+    const double eta_rho = sp.eta_rho;
     const SnGram* gl = bv.sn_gram + P.gram_off;
     for (int e = lane; e < P.n_gram; e += 32) {
       const SnGram g = gl[e];

@@ -344,6 +344,14 @@ class WorldBatch:
         _check(lib().kd_batch_reset_caches(self.handle))
 
     # -- stepping
+    def assemble(self, cfg: StepConfig):
+        """assemble_constraints (constraints.hpp:91-94) for every active world
+        at its current state, on the device, without solving or integrating;
+        read the result with dump_rows / dump_contacts / dump_limits."""
+        self._ensure()
+        c = cfg.to_ctypes()
+        _check(lib().kd_batch_assemble(self.handle, C.byref(c)))
+
     def step(self, cfg: StepConfig, n_steps: int = 1):
         self._ensure()
         c = cfg.to_ctypes()
@@ -502,6 +510,101 @@ def _rows_to_numpy(rows, n):
     for key, attr in (("bias", "bias"), ("reg", "reg"), ("scale", "scale"), ("vf", "vf_scaled"),
                       ("lambda", "lambda_"), ("z", "z")):
         out[key] = np.array([getattr(rows[i], attr) for i in range(n)])
+    return out
+
+
+@dataclass
+class SolveProblem:
+    """A pre-assembled system for the solver-level entry points
+    (kd_solve_problem): ConstraintSet rows (constraints.hpp:19-65) in the order
+    bilateral | limits | contacts, per-body inverse mass data
+    (BodyInertiaWorld, delassus.hpp:13-18), the Preconditioner scale, the
+    right-hand side (padmm_solve's preconditioned v_f, or cr_solve's rhs) and
+    an optional warm start (PadmmInit x0 / z0, or cr_solve's x)."""
+    body: np.ndarray          # (n, 2) int: body_a, body_b (-1 none)
+    jacobian: np.ndarray      # (n, 12): block_a, block_b
+    reg: np.ndarray           # (n,)
+    scale: np.ndarray         # (n,)
+    inv_mass: np.ndarray      # (nb,)
+    inv_inertia: np.ndarray   # (nb, 3, 3) world frame
+    rhs: np.ndarray           # (n,)
+    n_bilateral: int = -1     # default: every row
+    n_limits: int = 0
+    n_contacts: int = 0
+    mu: Optional[np.ndarray] = None
+    x0: Optional[np.ndarray] = None
+    z0: Optional[np.ndarray] = None
+
+    def _c(self, keep):
+        n = len(self.reg)
+        nbil = n - self.n_limits - 3 * self.n_contacts if self.n_bilateral < 0 else self.n_bilateral
+        f = lambda a, dt=np.float64: np.ascontiguousarray(a, dtype=dt).reshape(-1)  # noqa: E731
+        arrs = dict(body=f(self.body, np.int32), jacobian=f(self.jacobian), reg=f(self.reg), scale=f(self.scale),
+                    inv_mass=f(self.inv_mass), inv_inertia=f(self.inv_inertia), rhs=f(self.rhs),
+                    mu=f(self.mu) if self.mu is not None else None, x0=f(self.x0) if self.x0 is not None else None,
+                    z0=f(self.z0) if self.z0 is not None else None)
+        keep.append(arrs)
+        p = _capi.kd_solve_problem()
+        p.n_rows, p.n_bodies = n, len(arrs["inv_mass"])
+        p.n_bilateral, p.n_limits, p.n_contacts = nbil, self.n_limits, self.n_contacts
+        p.body = _capi.i32ptr(arrs["body"])
+        for k in ("jacobian", "reg", "scale", "inv_mass", "inv_inertia", "rhs", "mu", "x0", "z0"):
+            setattr(p, k, _capi.dptr(arrs[k]))
+        return p
+
+
+def _problems(problems):
+    keep = []
+    arr = (_capi.kd_solve_problem * max(1, len(problems)))(*[q._c(keep) for q in problems])
+    offs = np.concatenate([[0], np.cumsum([len(q.reg) for q in problems])]).astype(np.int64)
+    return arr, keep, offs
+
+
+_BACKENDS = {"dense": _capi.KD_BACKEND_DENSE, "sparse": _capi.KD_BACKEND_MATRIX_FREE,
+             "matrix_free": _capi.KD_BACKEND_MATRIX_FREE, "auto": _capi.KD_BACKEND_AUTO}
+
+
+def padmm_solve(problems, eta_rho: float, config: StepConfig, backend: str = "auto", cr_budget: int = 9,
+                history_capacity: int = 0, device: int = 0):
+    """build_backend + padmm_solve (delassus.hpp:103-105, padmm.hpp:64-67) for
+    every problem, on the device.  Returns per problem a dict with lambda
+    (preconditioned y), z, diag (kd_step_diag) and history (the combined
+    residual per iteration; empty unless history_capacity > 0)."""
+    arr, keep, offs = _problems(problems)
+    lam, z = np.zeros(max(1, offs[-1])), np.zeros(max(1, offs[-1]))
+    diags = (_capi.kd_step_diag * max(1, len(problems)))()
+    hist = np.zeros(max(1, len(problems) * history_capacity))
+    c = config.to_ctypes()
+    _check(lib().kd_padmm_solve_batched(device, arr, len(problems), float(eta_rho), _BACKENDS[backend],
+                                        int(cr_budget), C.byref(c), _capi.dptr(lam), _capi.dptr(z), diags,
+                                        _capi.dptr(hist), int(history_capacity)))
+    out = []
+    for p in range(len(problems)):
+        h = hist[p * history_capacity:(p + 1) * history_capacity]
+        out.append({"lambda": lam[offs[p]:offs[p + 1]].copy(), "z": z[offs[p]:offs[p + 1]].copy(),
+                    "diag": diags[p], "history": h[h != -1.0].copy()})
+    return out
+
+
+def cr_solve(problems, eta_rho: float, max_iters: int, history_capacity: int = 0, device: int = 0):
+    """bake_jacobian + cr_solve (delassus.hpp:82-83) per problem on the device
+    (x0 is the warm start).  Returns per problem a dict with x, iterations,
+    breakdown, residual_norm and history (|r| initially and after every update)."""
+    arr, keep, offs = _problems(problems)
+    n = len(problems)
+    x = np.zeros(max(1, offs[-1]))
+    it = np.zeros(max(1, n), np.int32)
+    brk = np.zeros(max(1, n), np.uint8)
+    rn = np.zeros(max(1, n))
+    hist = np.zeros(max(1, n * history_capacity))
+    _check(lib().kd_cr_solve_batched(device, arr, n, float(eta_rho), int(max_iters), _capi.dptr(x), _capi.i32ptr(it),
+                                     brk.ctypes.data_as(_capi.c_uint8_p), _capi.dptr(rn), _capi.dptr(hist),
+                                     int(history_capacity)))
+    out = []
+    for p in range(n):
+        h = hist[p * history_capacity:(p + 1) * history_capacity]
+        out.append({"x": x[offs[p]:offs[p + 1]].copy(), "iterations": int(it[p]), "breakdown": bool(brk[p]),
+                    "residual_norm": float(rn[p]), "history": h[h != -1.0].copy()})
     return out
 
 
