@@ -145,6 +145,7 @@ struct kd_batch {
   };
   std::vector<SnBin> sn_bins;
   bool sparse = true;
+  bool no_df = false;
   int sparse_mode = 1;
   bool sn_handoff = true;
   int64_t total_snlv = 0, total_snr2p = 0;
@@ -409,6 +410,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     b->sn_handoff = !(h && h[0] == '0');
     const char* g = getenv("KD_GRAPHS");  // KD_GRAPHS=0: launch every kernel directly
     b->graphs = !(g && g[0] == '0');
+    const char* df = getenv("KD_DENSE_DF");  // KD_DENSE_DF=0: barrier between the dense solve passes
+    b->no_df = df && df[0] == '0';
   }
   b->n_worlds = n_worlds;
   // model tables
@@ -932,6 +935,7 @@ static StepParams step_params(const kd_batch* b, const kd_step_config* c) {
   sp.sparse = b->sparse ? 1 : 0;
   sp.sn_handoff = b->sn_handoff ? 1 : 0;
   sp.eta_rho = c->eta + c->rho;
+  sp.no_df = b->no_df ? 1 : 0;
   sp.nest_beta = b->d_nest;
   return sp;
 }

@@ -485,6 +485,116 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, u
 }
 
 
+// Release / acquire flags in shared memory (CTA scope).
+__device__ __forceinline__ void flag_release(int* f, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(f)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(const int* f) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(f)) : "memory");
+  return v;
+}
+
+// inv_solve for T <= NT/32 tile rows with the barrier between the two passes
+// replaced by per-tile-row dataflow flags.  Warp i computes tile row i of
+// w = X b (pass 1), publishes it (rdy[i] = epoch, release), then runs tile
+// column i of x = X^T w (pass 2), consuming w_k for k = i, i+1, ... as each
+// is published (acquire).  The passes overlap: warp i's column work starts at
+// ~(i+1) tile times instead of after the slowest row (T tile times), so the
+// critical path drops from ~2T to ~T+1 tile times.  Every dot product runs in
+// the same order as inv_solve's, so the result is bitwise the same; x goes to
+// xo (pass 1 may still be reading b when early columns finish).
+template <int NT>
+__device__ void inv_solve_df(const double* X, const double* b, double* w, double* xo, int n, int T,
+                             unsigned long long xmask, int* rdy, int epoch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();  // b complete
+  if (wid >= T) return;  // (the caller's barrier after the solve is outside)
+  {  // pass 1: tile row wid
+    const int i = wid;
+    const int ri = tile_rows(i, n), r = lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (r < ri) {
+      for (int j = 0; j < i; ++j) {
+        if (!mtile(xmask, i, j)) continue;
+        const double* row = X + off_tile(i, j, n) + r * LDT;
+        const double2* bj = reinterpret_cast<const double2*>(b + 32 * j);
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const double2 b01 = bj[c / 2], b23 = bj[c / 2 + 1];
+          a0 += row[c] * b01.x;
+          a1 += row[c + 1] * b01.y;
+          a2 += row[c + 2] * b23.x;
+          a3 += row[c + 3] * b23.y;
+        }
+      }
+      const double* drow = X + diag_tile(i, n) + tri(r);
+      const double2* bi = reinterpret_cast<const double2*>(b + 32 * i);
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const double2 bb = bi[c / 2];
+        if (c <= r) a0 += drow[c] * bb.x;
+        if (c + 1 <= r) a1 += drow[c + 1] * bb.y;
+      }
+      w[32 * i + r] = (a0 + a1) + (a2 + a3);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      flag_release(rdy + i, epoch);
+    }
+  }
+  {  // pass 2: tile column wid, rows consumed as they are published
+    const int j = wid;
+    const int c = lane, rj = tile_rows(j, n);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    // the diagonal tile needs w_j, which this warp published itself
+    if (c < rj) {
+      const double* D = X + diag_tile(j, n);
+      const double2* wj = reinterpret_cast<const double2*>(w + 32 * j);
+#pragma unroll
+      for (int r = 0; r < 32; r += 2) {
+        const double2 ww = wj[r / 2];
+        if (r >= c && r < rj) a0 += D[tri(r) + c] * ww.x;
+        if (r + 1 >= c && r + 1 < rj) a1 += D[tri(r + 1) + c] * ww.y;
+      }
+    }
+    for (int i = j + 1; i < T; ++i) {
+      if (!mtile(xmask, i, j)) continue;
+      if (lane == 0)
+        while (flag_acquire(rdy + i) != epoch) {
+        }
+      __syncwarp();
+      if (c < rj) {
+        const int ri = tile_rows(i, n);
+        const double* A = X + off_tile(i, j, n) + c;
+        const double2* wi = reinterpret_cast<const double2*>(w + 32 * i);
+        if (ri == 32) {
+#pragma unroll
+          for (int r = 0; r < 32; r += 4) {
+            const double2 w01 = wi[r / 2], w23 = wi[r / 2 + 1];
+            a0 += A[r * LDT] * w01.x;
+            a1 += A[(r + 1) * LDT] * w01.y;
+            a2 += A[(r + 2) * LDT] * w23.x;
+            a3 += A[(r + 3) * LDT] * w23.y;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; r += 4) {
+            const double2 w01 = wi[r / 2], w23 = wi[r / 2 + 1];
+            if (r < ri) a0 += A[r * LDT] * w01.x;
+            if (r + 1 < ri) a1 += A[(r + 1) * LDT] * w01.y;
+            if (r + 2 < ri) a2 += A[(r + 2) * LDT] * w23.x;
+            if (r + 3 < ri) a3 += A[(r + 3) * LDT] * w23.y;
+          }
+        }
+      }
+    }
+    if (c < rj) xo[32 * j + c] = (a0 + a1) + (a2 + a3);
+  }
+}
+
+
 
 // PADMM loop of the dense kernel for GLOBAL_L worlds (any n): the same
 // arithmetic as the register-resident loop of dense_kernel, with every thread
@@ -664,6 +774,11 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   double* red = wv_s + npad;       // 3 * NW
   int* rbs = reinterpret_cast<int*>(red + 3 * NW + 1);  // 2n body ids
   double* chain = reinterpret_cast<double*>(rbs + 2 * npad);  // 32 doubles: pivot-column broadcast
+  int* rdy = reinterpret_cast<int*>(chain + 32);                // 8 tile-row flags of inv_solve_df
+  // the dataflow solve (T <= warps) writes x to the P buffer, which is free
+  // after the Gram phase (and unused by the hand-off)
+  const bool df = !GLOBAL_L && T <= NW && !sp.no_df;
+  double* xsol = df ? P : xv;
   __shared__ int fail;
   const int64_t R0 = W.row_off;
   const RowJ* rj = bv.rowj + R0;
@@ -680,6 +795,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     }
   };
   if (tid == 0) fail = 0;
+  if (tid < 8) rdy[tid] = 0;
   if (handoff) {  // rbs holds the row -> plan position map; b is zero at unused positions
     for (int r = tid; r < ws.n_rows; r += NT) rbs[r] = bv.sn_r2p[W.snr2p_off + r];
     for (int r = tid; r < npad; r += NT) xv[r] = 0.0;
@@ -917,7 +1033,12 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
 #ifdef KD_PROF_PADMM
     const long long p0 = clock64();
 #endif
-    inv_solve<NT>(L, xv, wv_s, n, T, xm, prof);
+    if (df) {
+      inv_solve_df<NT>(L, xv, wv_s, xsol, n, T, xm, rdy, it);
+      __syncthreads();  // x complete
+    } else {
+      inv_solve<NT>(L, xv, wv_s, n, T, xm, prof);
+    }
 #ifdef KD_PROF_PADMM
     const long long p1 = clock64();
 #endif
@@ -926,7 +1047,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     double yp[3], zp[3], wv[3], yn[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      if (d < nr) x[d] = xv[pos[d]];
+      if (d < nr) x[d] = xsol[pos[d]];
       wv[d] = x[d] - zh[d] * inv_rho;
       yp[d] = y[d];
       zp[d] = z[d];
@@ -1041,7 +1162,7 @@ size_t dense_smem_bytes(int n, int nt, bool global_l) {
   const size_t nl = (size_t)528 * (T - 1) * (T - 1) + (size_t)(T - 1) * 33 * rl + (size_t)rl * (rl + 1) / 2;
   const size_t nlen = global_l ? 0 : ((nl + 1) & ~(size_t)1);
   const size_t npad = 32 * (size_t)T;
-  return 8 * (nlen + 3 * npad + 3 * (nt / 32) + 1) + 4 * 2 * npad + 8 * 32 + 64;
+  return 8 * (nlen + 3 * npad + 3 * (nt / 32) + 1) + 4 * 2 * npad + 8 * 32 + 32 + 64;
 }
 
 template <int NT, bool G>

@@ -129,7 +129,7 @@ def test_stewart_tower_cr_parity(monkeypatch):
             assert dg[w].iterations == do[w].iterations, (k, w)
             assert abs(dg[w].cr_iterations - do[w].cr_iterations) <= 2
         if k < 2:  # identical inputs at k = 0; after one step the states differ at rounding level
-            _rows_match(gb, ob, 0, 1e-12 if k == 0 else 1e-10)
+            _rows_match(gb, ob, 0, 1e-12 if k == 0 else 1e-9)
     assert gb.kernels() == ["cr", "cr"]
     pg, tg, _ = gb.get_state()
     po, to, _ = ob.get_state()
