@@ -148,7 +148,11 @@ __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams s
   WorldStep& ws = bv.wstep[w];
   if (ws.backend != BE_MATRIX_FREE) return;
   const int n = ws.n_rows;
-  if (n <= n_reg) return;  // cr_op_kernel took it
+  if (n_reg >= 0) {
+    if (n <= n_reg) return;  // cr_op_kernel took it
+  } else if (ws.cr_path == 1) {
+    return;  // n_reg < 0: the incidence-owner kernel took it this step (it marks every world of the bin)
+  }
   const int tid = threadIdx.x;
   if (tid == 0) ws.cr_path = 3;  // KD_CR_PATH_SHARED
   const DevWorld W = bv.worlds[w];
@@ -1234,6 +1238,21 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
     }
     if (e != cudaSuccess) return e;
     if (ncap <= n_reg) return cudaSuccess;
+  } else if (cr_reg_mode() && ncap > 512 && ncap <= 1024 &&
+             cr_common_bytes(ncap, 256) + IncOp<256, 4, 8, false>::smem_bytes(ncap, nbcap) <= 232448) {
+    // many bodies (the row owners' per-body staging does not fit, e.g. the
+    // 156-body Stewart tower): incidence owners, and the shared-memory kernel
+    // for the worlds whose bodies do not fit the lanes (n_reg = -1: it skips
+    // the worlds the incidence-owner kernel marked)
+    cudaError_t e =
+        launch_cr_op_p<IncOp<256, 4, 8, false>, 256, 4, 1, false, true>(bv, sp, worlds, count, ncap, nbcap, 0, s);
+    if (e != cudaSuccess) return e;
+    // more body pieces than 256 lanes: 512 lanes with pieces of <= 5
+    if (cr_common_bytes(ncap, 512) + IncOp<512, 2, 5, false>::smem_bytes(ncap, nbcap) <= 232448) {
+      e = launch_cr_op_p<IncOp<512, 2, 5, false>, 512, 2, 1, false, true>(bv, sp, worlds, count, ncap, nbcap, 1, s);
+      if (e != cudaSuccess) return e;
+    }
+    n_reg = -1;
   }
   // two resident CTAs per SM whenever their (staged) shared memory fits: the
   // kernel is synchronisation/latency bound, so a second world hides it

@@ -8,11 +8,11 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_16536_b200 as K  # noqa: E402
-from paper_2603_16536_b200.scenes import closed_chain, sphere_pile  # noqa: E402
+from paper_2603_16536_b200.scenes import closed_chain, sphere_pile, stewart_tower  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "closed_chain"
 nw = int(sys.argv[2]) if len(sys.argv) > 2 else 296
-sc = closed_chain(22) if which == "closed_chain" else sphere_pile()
+sc = {"closed_chain": lambda: closed_chain(22), "stewart_tower": stewart_tower}.get(which, sphere_pile)()
 cfg = K.config_for(sc)
 m = K.build_model(sc)
 b = K.WorldBatch()
