@@ -1171,6 +1171,9 @@ static cudaError_t launch_cr_op_p(const BatchView& bv, const StepParams& sp, con
 }
 
 static int cr_reg_mode();
+#ifndef KD_INC512_P
+#define KD_INC512_P 5
+#endif
 
 // KD_CR_REG: 0 = shared-memory kernel only, 1 (default) = incidence-owner then
 // register-row kernels, 2 = the same with phase clocks, 3 = register-row only,
@@ -1248,8 +1251,8 @@ cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* 
         launch_cr_op_p<IncOp<256, 4, 8, false>, 256, 4, 1, false, true>(bv, sp, worlds, count, ncap, nbcap, 0, s);
     if (e != cudaSuccess) return e;
     // more body pieces than 256 lanes: 512 lanes with pieces of <= 5
-    if (cr_common_bytes(ncap, 512) + IncOp<512, 2, 5, false>::smem_bytes(ncap, nbcap) <= 232448) {
-      e = launch_cr_op_p<IncOp<512, 2, 5, false>, 512, 2, 1, false, true>(bv, sp, worlds, count, ncap, nbcap, 1, s);
+    if (cr_common_bytes(ncap, 512) + IncOp<512, 2, KD_INC512_P, false>::smem_bytes(ncap, nbcap) <= 232448) {
+      e = launch_cr_op_p<IncOp<512, 2, KD_INC512_P, false>, 512, 2, 1, false, true>(bv, sp, worlds, count, ncap, nbcap, 1, s);
       if (e != cudaSuccess) return e;
     }
     n_reg = -1;

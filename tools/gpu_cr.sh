@@ -10,5 +10,5 @@ KD_CR_REG=0 timeout 600 python bench.py --workload closed_chain --steps 10 --war
 tail -3 gpurun_out/${TAG}_pytest_gpu.txt
 for f in gpurun_out/${TAG}_bench_*.json; do echo "$f: $(cut -c1-180 $f)"; done
 if [ "$2" = "ncu" ]; then
-  timeout 800 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-cr_op_kernel} -s 10 -c 1 -o gpurun_out/${TAG}_crreg python tests/ncu_target_cr.py 296 12 > gpurun_out/${TAG}_ncu.log 2>&1
+  timeout 800 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-cr_op_kernel} -s 10 -c 1 -o gpurun_out/${TAG}_crreg python tools/ncu_target_cr.py 296 12 > gpurun_out/${TAG}_ncu.log 2>&1
 fi

@@ -1,12 +1,12 @@
 """A/B throughput of the fused dense kernel vs the supernodal kernel per model
-(diagnostic): python tests/kernel_ab.py  (run twice: KD_SPARSE=0 and default)."""
+(diagnostic): python tools/kernel_ab.py  (run twice: KD_SPARSE=0 and default)."""
 import json
 import os
 import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import oracle_lib  # noqa: E402
 import paper_2603_16536_b200 as K  # noqa: E402
 from paper_2603_16536_b200.scenes import dr_legs  # noqa: E402
