@@ -241,9 +241,10 @@ int kd_batch_device_state(kd_batch* batch, double** poses, double** twists, doub
  * are overwritten with the result (twists and time untouched).  joints /
  * values are n_worlds x n_targets (joint index, target coordinate) per world;
  * tolerance / max_iters / lm_initial are FkConfig (fk.hpp:19-23).  Per-world
- * outputs (each may be NULL): iterations, residual_inf, converged.  Models with
- * more than 36 bodies return KD_ERR_CAPACITY (the normal matrix must fit in
- * one CTA's shared memory). */
+ * outputs (each may be NULL): iterations, residual_inf, converged.  Any model
+ * size: the normal matrix lives in shared memory when it fits (<= 36 bodies),
+ * else in a per-world HBM scratch slab (KD_ERR_CAPACITY only if that slab does
+ * not fit device memory). */
 int kd_batch_fk(kd_batch* batch, const int32_t* joints, const double* values, int32_t n_targets, double tolerance,
                 int32_t max_iters, double lm_initial, int32_t* iterations, double* residual_inf, uint8_t* converged);
 /* Async state copies with caller-provided (pinned) host buffers, on the batch stream. */

@@ -1204,7 +1204,16 @@ int kd_batch_fk(kd_batch* b, const int32_t* joints, const double* values, int32_
     }
     smem = std::max(smem, fk_smem_bytes((int)m.bodies.size(), m.n_bil + nt));
   }
-  if (smem > 232448) return fail(KD_ERR_CAPACITY, "forward kinematics: model too large for one CTA's shared memory");
+  // models too large for one CTA's shared memory: a per-world HBM scratch slab
+  double* d_scr = nullptr;
+  if (smem > 232448) {
+    const size_t per = (smem + 15) / 16 * 16;
+    if (cudaMalloc(&d_scr, per * (size_t)b->n_worlds) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(KD_ERR_CAPACITY, "forward kinematics: the normal-matrix scratch (" +
+                                       std::to_string(per * (double)b->n_worlds / 1e9) + " GB) does not fit device memory");
+    }
+  }
   const size_t n = (size_t)b->n_worlds * std::max(1, nt);
   int32_t* d_j = nullptr;
   double* d_v = nullptr;
@@ -1221,7 +1230,7 @@ int kd_batch_fk(kd_batch* b, const int32_t* joints, const double* values, int32_
     KD_CK(cudaMemcpyAsync(d_j, joints, 4 * (size_t)b->n_worlds * nt, cudaMemcpyHostToDevice, b->stream));
     KD_CK(cudaMemcpyAsync(d_v, values, 8 * (size_t)b->n_worlds * nt, cudaMemcpyHostToDevice, b->stream));
   }
-  cudaError_t e = launch_fk(b->view, d_j, d_v, nt, tol, max_iters, lm0, d_it, d_res, d_conv, smem, b->stream);
+  cudaError_t e = launch_fk(b->view, d_j, d_v, nt, tol, max_iters, lm0, d_it, d_res, d_conv, smem, b->stream, d_scr);
   if (e == cudaSuccess) e = cudaStreamSynchronize(b->stream);
   if (e == cudaSuccess && iterations) e = to_host(b, iterations, d_it, 4 * (size_t)b->n_worlds);
   if (e == cudaSuccess && residual_inf)
@@ -1233,6 +1242,7 @@ int kd_batch_fk(kd_batch* b, const int32_t* joints, const double* values, int32_
   cudaFree(d_it);
   cudaFree(d_res);
   cudaFree(d_conv);
+  if (d_scr) cudaFree(d_scr);
   return rc;
 }
 

@@ -44,8 +44,12 @@ struct FkRows {
 
 __global__ void __launch_bounds__(kFkThreads, 1) fk_kernel(BatchView bv, const int32_t* tj, const double* tv, int nt,
                                                            double tol, int max_iters, double lm0, int32_t* out_iters,
-                                                           double* out_res, uint8_t* out_conv) {
-  extern __shared__ __align__(16) double smem[];
+                                                           double* out_res, uint8_t* out_conv, double* gscratch,
+                                                           int64_t scratch_doubles) {
+  extern __shared__ __align__(16) double smem_[];
+  // models whose normal matrix does not fit one CTA's shared memory work in a
+  // per-world HBM scratch slab instead (same layout, same arithmetic)
+  double* smem = gscratch ? gscratch + (int64_t)blockIdx.x * scratch_doubles : smem_;
   constexpr int NT = kFkThreads;
   const int w = blockIdx.x, tid = threadIdx.x;
   if (!bv.active[w]) {
@@ -254,14 +258,20 @@ size_t fk_smem_bytes(int nb, int nr) {
 }
 
 cudaError_t launch_fk(const BatchView& bv, const int32_t* tj, const double* tv, int nt, double tol, int max_iters,
-                      double lm0, int32_t* iters, double* res, uint8_t* conv, size_t smem, cudaStream_t s) {
+                      double lm0, int32_t* iters, double* res, uint8_t* conv, size_t smem, cudaStream_t s,
+                      double* gscratch) {
   if (bv.n_worlds <= 0) return cudaSuccess;
+  if (gscratch) {
+    fk_kernel<<<bv.n_worlds, kFkThreads, 0, s>>>(bv, tj, tv, nt, tol, max_iters, lm0, iters, res, conv, gscratch,
+                                                 (int64_t)((smem + 15) / 16 * 2));
+    return cudaGetLastError();
+  }
   static SmemAttrCache attr;
   {
     const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(fk_kernel), smem, attr);
     if (e != cudaSuccess) return e;
   }
-  fk_kernel<<<bv.n_worlds, kFkThreads, smem, s>>>(bv, tj, tv, nt, tol, max_iters, lm0, iters, res, conv);
+  fk_kernel<<<bv.n_worlds, kFkThreads, smem, s>>>(bv, tj, tv, nt, tol, max_iters, lm0, iters, res, conv, nullptr, 0);
   return cudaGetLastError();
 }
 

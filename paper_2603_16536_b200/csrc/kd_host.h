@@ -51,7 +51,8 @@ cudaError_t launch_snfactor(const BatchView& bv, const StepParams& sp, const int
                             cudaStream_t s);
 size_t snfactor_smem_bytes(int nLv, int S);
 cudaError_t launch_fk(const BatchView& bv, const int32_t* tj, const double* tv, int nt, double tol, int max_iters,
-                      double lm0, int32_t* iters, double* res, uint8_t* conv, size_t smem, cudaStream_t s);
+                      double lm0, int32_t* iters, double* res, uint8_t* conv, size_t smem, cudaStream_t s,
+                      double* gscratch = nullptr);
 size_t fk_smem_bytes(int nb, int nr);
 void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s, int w0 = 0, int w1 = -1);
 size_t dense_smem_bytes(int n, int nt, bool global_l);

@@ -143,9 +143,11 @@ def dr_legs(kp=15.0, kd=0.6, pad_mu=0.8, dt=1.0 / 250.0, integrator="moreau", pa
 
 def closed_chain(n_cells=22, link=0.2, mass=0.1) -> SceneDescription:
     """Config 4: a hanging ladder of parallelogram cells (3D revolute joints
-    about y).  Rails are split into one segment per cell; each cell adds one
-    rung -> 2 bodies and 3 joints per cell, one loop per cell.  Rows =
-    5 * joints; n_cells=22 -> 68 joints -> 340 rows (> 300 -> CR path)."""
+    about y).  Rails are split into one segment per cell; each cell adds two
+    rail segments and one rung (3 bodies) and four joints, one loop per cell.
+    Rows = 5 * joints = 20 * n_cells: n_cells=12 -> 240 rows, 14 -> 280
+    (dense HBM-slab kernel under Auto), 22 -> 88 joints -> 440 rows
+    (> 300 -> matrix-free CR path under Auto)."""
     b = _Builder("closed_chain", gravity=(0.0, 0.0, -9.81))
     w = link  # rung width
     prev_l = prev_r = "world"
