@@ -409,7 +409,9 @@ int kd_batch_get_kernels(kd_batch* batch, int32_t* out);
  * 106-187): KD_CR_PATH_NONE (not on the matrix-free backend),
  * KD_CR_PATH_INCIDENCE (incidence-owner lanes keep P J in registers),
  * KD_CR_PATH_ROWS (row owners keep P J in registers), KD_CR_PATH_SHARED
- * (P J staged in shared memory or streamed; worlds above 1024 rows). */
+ * (P J staged in shared memory or streamed; worlds above 1024 rows; worlds
+ * whose vectors exceed one CTA's shared memory keep them in a per-world HBM
+ * slab, so there is no size limit). */
 #define KD_CR_PATH_NONE 0
 #define KD_CR_PATH_INCIDENCE 1
 #define KD_CR_PATH_ROWS 2

@@ -562,8 +562,6 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
   }
   b->global_bin.nt = 256;
   for (Bin* bin : {&b->cr_auto_bin, &b->cr_all_bin}) bin->nt = bin->cap > 256 ? 512 : (bin->cap > 128 ? 256 : 128);
-  if (cr_smem_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) > 232448)
-    return fail(KD_ERR_CAPACITY, "matrix-free path: world too large for one CTA's shared memory");
 
   // device allocations
   BatchView& v = b->view;
@@ -632,6 +630,17 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
   KD_CK(mem.alloc(v.lslab, b->total_lslab));
   KD_CK(mem.alloc(v.sn_lv, b->total_snlv));
   KD_CK(mem.alloc(v.sn_r2p, b->total_snr2p));
+  if (cr_smem_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) > 232448) {
+    // worlds too large for one CTA's shared memory: the shared CR kernel keeps
+    // its vectors (and the staged P J) in a per-world HBM slab instead
+    const int64_t stride = (int64_t)((cr_staged_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) + 15) / 16 * 2);
+    if (mem.alloc(v.cr_scratch, (size_t)stride * std::max(1, n_worlds)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(KD_ERR_CAPACITY, "matrix-free path: the per-world scratch of worlds beyond one CTA's shared memory "
+                                   "does not fit device memory");
+    }
+    v.cr_scratch_stride = stride;
+  }
   KD_CK(mem.alloc(b->d_hist, 1));
   KD_CK(mem.alloc(b->d_err, 4));
   v.hist = b->d_hist;

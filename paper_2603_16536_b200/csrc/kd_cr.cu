@@ -143,8 +143,10 @@ __device__ void apply_op(const CrCtx& c, const double* v, double* out) {
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) cr_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds,
                                                   int smem_doubles, int n_reg) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) double smem_[];
   const int w = bin_worlds[blockIdx.x];
+  // worlds beyond one CTA's shared memory: the same layout in a per-world HBM slab
+  double* smem = bv.cr_scratch ? bv.cr_scratch + (int64_t)w * bv.cr_scratch_stride : smem_;
   WorldStep& ws = bv.wstep[w];
   if (ws.backend != BE_MATRIX_FREE) return;
   const int n = ws.n_rows;
@@ -1130,13 +1132,18 @@ __global__ void __launch_bounds__(NT, MINB) cr_op_kernel(BatchView bv, StepParam
 
 size_t cr_smem_bytes(int n, int nb, int nt) { return 8 * ((size_t)13 * n + 16 * (size_t)nb + 3 * (nt / 32) + 8); }
 // with the optional per-step staging of P J and the index lists
-static size_t cr_staged_bytes(int n, int nb, int nt) {
+size_t cr_staged_bytes(int n, int nb, int nt) {
   return 8 * ((size_t)25 * n + 16 * (size_t)nb + 3 * (nt / 32) + 8 + ((size_t)4 * n + nb + 2) / 2 + 2);
 }
 
 template <int NT, int MINB>
 static cudaError_t launch_cr_t(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap,
                                int nbcap, int n_reg, cudaStream_t s) {
+  if (bv.cr_scratch) {
+    cr_kernel<NT, MINB><<<count, NT, 0, s>>>(bv, sp, worlds, (int)std::min<int64_t>(bv.cr_scratch_stride, 1 << 30),
+                                              n_reg);
+    return cudaGetLastError();
+  }
   const size_t smem = std::max(cr_smem_bytes(ncap, nbcap, NT),
                                std::min<size_t>(232448 / MINB, cr_staged_bytes(ncap, nbcap, NT)));
   static SmemAttrCache attr;

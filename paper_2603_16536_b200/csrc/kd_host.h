@@ -58,6 +58,7 @@ void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s, i
 size_t dense_smem_bytes(int n, int nt, bool global_l);
 size_t dense_factor_doubles(int n);
 size_t cr_smem_bytes(int n, int nb, int nt);
+size_t cr_staged_bytes(int n, int nb, int nt);
 
 }  // namespace kd
 

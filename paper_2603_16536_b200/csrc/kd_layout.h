@@ -248,6 +248,8 @@ struct BatchView {
   const int32_t* sn_prow;  // panel-row positions of every supernode
   const uint32_t* sn_scat; // hand-off scatter lists (Lv index | tile index << 16)
   const uint8_t* sn_kmask;  // per-L-tile 4-column-group nonzero masks (36 per planned model)
+  double* cr_scratch;      // worlds too large for one CTA's shared memory: the shared CR kernel's
+  int64_t cr_scratch_stride;  // per-world HBM slab (doubles per world, indexed by world), else null
   double* sn_lv;           // BE_DENSE_SN hand-off: the factor array per world
   int32_t* sn_r2p;         // BE_DENSE_SN hand-off: compact row -> position per world
 };
