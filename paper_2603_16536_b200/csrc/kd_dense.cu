@@ -405,6 +405,9 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, u
 #ifdef KD_PROF_PADMM
   long long q0 = clock64();
 #endif
+#ifdef KD_PROF_WARP
+  const long long qw0 = clock64();
+#endif
   for (int i = wid; i < T; i += NT / 32) {
     const int ri = tile_rows(i, n), r = lane;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -433,7 +436,14 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, u
       w[32 * i + r] = (a0 + a1) + (a2 + a3);
     }
   }
+#ifdef KD_PROF_WARP
+  __syncwarp();
+  if (KD_PROF_WARP == 1 && prof) prof[4 + wid] += clock64() - qw0;
+#endif
   __syncthreads();
+#ifdef KD_PROF_WARP
+  const long long qw1 = clock64();
+#endif
 #ifdef KD_PROF_PADMM
   long long q1 = clock64();
   prof[0] += q1 - q0;
@@ -478,6 +488,10 @@ __device__ void inv_solve(const double* X, double* b, double* w, int n, int T, u
       b[32 * j + c] = (a0 + a1) + (a2 + a3);
     }
   }
+#ifdef KD_PROF_WARP
+  __syncwarp();
+  if (KD_PROF_WARP == 2 && prof) prof[4 + wid] += clock64() - qw1;
+#endif
   __syncthreads();
 #ifdef KD_PROF_PADMM
   prof[1] += clock64() - q1;
@@ -495,6 +509,159 @@ __device__ __forceinline__ int flag_acquire(const int* f) {
   return v;
 }
 
+// Register-resident tiles of X for the dataflow solve.  During PADMM most of
+// the 255 registers the L^-1 formation needed are free; each warp parks up to
+// KD_DF_REG tiles of X there, in the orientation of the pass that uses them
+// (pass 1: lane = row, pass 2: lane = column, 32 doubles per lane, zeros
+// outside the tile's triangle / rows).  A register tile costs the pass only
+// its 16 broadcast wavefronts instead of 80 (64 for the tile + 16), and the
+// tiles chosen are the ones on the dataflow critical path: the pass-2 tile of
+// the last tile row (published last) and the first tiles of the warp's own
+// tile row.  The dot products run in the same order with the same
+// accumulators as from shared memory (bitwise the same up to the sign of
+// exact zeros).
+#ifndef KD_DF_REG
+#define KD_DF_REG 2
+#endif
+constexpr int DF_NC = KD_DF_REG;
+struct RegTiles {
+  double v[DF_NC > 0 ? DF_NC : 1][32];
+  int id[DF_NC > 0 ? DF_NC : 1];  // pass << 8 | i << 4 | j, or -1
+};
+__device__ __forceinline__ int rt_id(int pass, int i, int j) { return (pass << 8) | (i << 4) | j; }
+
+// slot of tile (pass, i, j) in R, or -1
+__device__ __forceinline__ int rt_slot(const RegTiles& R, int pass, int i, int j) {
+  const int q = rt_id(pass, i, j);
+  int s = -1;
+#pragma unroll
+  for (int k = 0; k < DF_NC; ++k)
+    if (R.id[k] == q) s = k;
+  return s;
+}
+
+// pick and load warp `wid`'s register tiles (after X is final; warp-uniform)
+__device__ void rt_load(RegTiles& R, const double* X, int n, int T, unsigned long long xmask) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // the t-th candidate: 1. the pass-2 tile of the last tile row in this
+  // warp's column, 2. the first tiles of this warp's tile row (pass 1)
+  auto cand = [&](int t) -> int {
+    if (wid >= T) return -1;
+    if (wid < T - 1 && mtile(xmask, T - 1, wid)) {
+      if (t == 0) return rt_id(2, T - 1, wid);
+      --t;
+    }
+    for (int j = 0; j <= wid; ++j)
+      if (mtile(xmask, wid, j)) {
+        if (t == 0) return rt_id(1, wid, j);
+        --t;
+      }
+    return -1;
+  };
+#pragma unroll
+  for (int s = 0; s < DF_NC; ++s) R.id[s] = cand(s);  // static slot index: R stays in registers
+#pragma unroll
+  for (int s = 0; s < DF_NC; ++s) {
+    const int q = R.id[s];
+    if (q < 0) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) R.v[s][e] = 0.0;
+      continue;
+    }
+    const int pass = q >> 8, i = (q >> 4) & 15, j = q & 15;
+    const int ri = tile_rows(i, n);
+    if (i == j) {
+      const double* D = X + diag_tile(i, n);
+      if (pass == 1) {  // lane = row r: X[r][c], c <= r
+#pragma unroll
+        for (int c = 0; c < 32; ++c) R.v[s][c] = (lane < ri && c <= lane) ? D[tri(lane) + c] : 0.0;
+      } else {  // lane = column c: X[r][c], r >= c
+#pragma unroll
+        for (int r = 0; r < 32; ++r) R.v[s][r] = (lane < ri && r >= lane && r < ri) ? D[tri(r) + lane] : 0.0;
+      }
+    } else {
+      const double* A = X + off_tile(i, j, n);
+      if (pass == 1) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) R.v[s][c] = lane < ri ? A[lane * LDT + c] : 0.0;
+      } else {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) R.v[s][r] = r < ri ? A[r * LDT + lane] : 0.0;
+      }
+    }
+  }
+}
+
+// acc += tile . v (4-accumulator off-diagonal order / 2-accumulator diagonal order)
+__device__ __forceinline__ void rt_dot_off(const double* t, const double* v, double& a0, double& a1, double& a2,
+                                           double& a3) {
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll
+  for (int c = 0; c < 32; c += 4) {
+    const double2 p = v2[c / 2], q = v2[c / 2 + 1];
+    a0 += t[c] * p.x;
+    a1 += t[c + 1] * p.y;
+    a2 += t[c + 2] * q.x;
+    a3 += t[c + 3] * q.y;
+  }
+}
+__device__ __forceinline__ void rt_dot_diag(const double* t, const double* v, double& a0, double& a1) {
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    const double2 p = v2[c / 2];
+    a0 += t[c] * p.x;
+    a1 += t[c + 1] * p.y;
+  }
+}
+template <int S>
+struct RtDispatch {  // static register indexing: slot k -> R.v[k]
+  __device__ __forceinline__ static void off(const RegTiles& R, int k, const double* v, double& a0, double& a1,
+                                             double& a2, double& a3) {
+    if (k == S - 1) rt_dot_off(R.v[S - 1], v, a0, a1, a2, a3);
+    else RtDispatch<S - 1>::off(R, k, v, a0, a1, a2, a3);
+  }
+  __device__ __forceinline__ static void diag(const RegTiles& R, int k, const double* v, double& a0, double& a1) {
+    if (k == S - 1) rt_dot_diag(R.v[S - 1], v, a0, a1);
+    else RtDispatch<S - 1>::diag(R, k, v, a0, a1);
+  }
+};
+template <>
+struct RtDispatch<0> {
+  __device__ __forceinline__ static void off(const RegTiles&, int, const double*, double&, double&, double&,
+                                             double&) {}
+  __device__ __forceinline__ static void diag(const RegTiles&, int, const double*, double&, double&) {}
+};
+
+
+// unroll of the shared-memory tile walks in the dataflow solve (columns per
+// step / 4): fewer loads in flight per warp leave registers for register tiles
+#ifndef KD_DF_UNROLL
+#define KD_DF_UNROLL 16
+#endif
+#define KD_PRAGMA_(x) _Pragma(#x)
+#define KD_PRAGMA(x) KD_PRAGMA_(x)
+#define DF_UNROLL KD_PRAGMA(unroll KD_DF_UNROLL)
+
+// Tile-row readiness of the dataflow solve: a release/acquire flag word per
+// tile row, polled by the consumer's lane 0 with a __nanosleep(KD_DF_WAIT)
+// backoff (each poll is a shared-memory load competing with the solve passes
+// for the pipe; 32 ns measured best of 0/32/200 on DR-Legs, +1 %).
+#ifndef KD_DF_WAIT
+#define KD_DF_WAIT 32
+#endif
+__device__ __forceinline__ void df_publish(int* rdy, int i, int epoch) {
+  __threadfence_block();
+  flag_release(rdy + i, epoch);
+}
+__device__ __forceinline__ void df_wait(const int* rdy, int i, int epoch) {
+  while (flag_acquire(rdy + i) != epoch) {
+#if KD_DF_WAIT > 0
+    __nanosleep(KD_DF_WAIT);
+#endif
+  }
+}
+
 // inv_solve for T <= NT/32 tile rows with the barrier between the two passes
 // replaced by per-tile-row dataflow flags.  Warp i computes tile row i of
 // w = X b (pass 1), publishes it (rdy[i] = epoch, release), then runs tile
@@ -503,23 +670,34 @@ __device__ __forceinline__ int flag_acquire(const int* f) {
 // ~(i+1) tile times instead of after the slowest row (T tile times), so the
 // critical path drops from ~2T to ~T+1 tile times.  Every dot product runs in
 // the same order as inv_solve's, so the result is bitwise the same; x goes to
-// xo (pass 1 may still be reading b when early columns finish).
+// xo (pass 1 may still be reading b when early columns finish).  Tiles in R
+// are read from registers.
 template <int NT>
 __device__ void inv_solve_df(const double* X, const double* b, double* w, double* xo, int n, int T,
-                             unsigned long long xmask, int* rdy, int epoch) {
+                             unsigned long long xmask, int* rdy, int epoch, const RegTiles& R,
+                             long long* prof = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();  // b complete
   if (wid >= T) return;  // (the caller's barrier after the solve is outside)
+#ifdef KD_PROF_WARP
+  const long long qd0 = clock64();
+  long long qwait = 0;
+#endif
   {  // pass 1: tile row wid
     const int i = wid;
     const int ri = tile_rows(i, n), r = lane;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    if (r < ri) {
-      for (int j = 0; j < i; ++j) {
-        if (!mtile(xmask, i, j)) continue;
+    for (int j = 0; j < i; ++j) {
+      if (!mtile(xmask, i, j)) continue;
+      const int k = rt_slot(R, 1, i, j);
+      if (k >= 0) {
+        RtDispatch<DF_NC>::off(R, k, b + 32 * j, a0, a1, a2, a3);
+        continue;
+      }
+      if (r < ri) {
         const double* row = X + off_tile(i, j, n) + r * LDT;
         const double2* bj = reinterpret_cast<const double2*>(b + 32 * j);
-#pragma unroll
+DF_UNROLL
         for (int c = 0; c < 32; c += 4) {
           const double2 b01 = bj[c / 2], b23 = bj[c / 2 + 1];
           a0 += row[c] * b01.x;
@@ -528,49 +706,67 @@ __device__ void inv_solve_df(const double* X, const double* b, double* w, double
           a3 += row[c + 3] * b23.y;
         }
       }
-      const double* drow = X + diag_tile(i, n) + tri(r);
-      const double2* bi = reinterpret_cast<const double2*>(b + 32 * i);
-#pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        const double2 bb = bi[c / 2];
-        if (c <= r) a0 += drow[c] * bb.x;
-        if (c + 1 <= r) a1 += drow[c + 1] * bb.y;
+    }
+    {
+      const int k = rt_slot(R, 1, i, i);
+      if (k >= 0) {
+        RtDispatch<DF_NC>::diag(R, k, b + 32 * i, a0, a1);
+      } else if (r < ri) {
+        const double* drow = X + diag_tile(i, n) + tri(r);
+        const double2* bi = reinterpret_cast<const double2*>(b + 32 * i);
+DF_UNROLL
+        for (int c = 0; c < 32; c += 2) {
+          const double2 bb = bi[c / 2];
+          if (c <= r) a0 += drow[c] * bb.x;
+          if (c + 1 <= r) a1 += drow[c + 1] * bb.y;
+        }
       }
-      w[32 * i + r] = (a0 + a1) + (a2 + a3);
     }
+    if (r < ri) w[32 * i + r] = (a0 + a1) + (a2 + a3);
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      flag_release(rdy + i, epoch);
-    }
+    if (lane == 0) df_publish(rdy, i, epoch);
   }
   {  // pass 2: tile column wid, rows consumed as they are published
     const int j = wid;
     const int c = lane, rj = tile_rows(j, n);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     // the diagonal tile needs w_j, which this warp published itself
-    if (c < rj) {
-      const double* D = X + diag_tile(j, n);
-      const double2* wj = reinterpret_cast<const double2*>(w + 32 * j);
-#pragma unroll
-      for (int r = 0; r < 32; r += 2) {
-        const double2 ww = wj[r / 2];
-        if (r >= c && r < rj) a0 += D[tri(r) + c] * ww.x;
-        if (r + 1 >= c && r + 1 < rj) a1 += D[tri(r + 1) + c] * ww.y;
+    {
+      const int k = rt_slot(R, 2, j, j);
+      if (k >= 0) {
+        RtDispatch<DF_NC>::diag(R, k, w + 32 * j, a0, a1);
+      } else if (c < rj) {
+        const double* D = X + diag_tile(j, n);
+        const double2* wj = reinterpret_cast<const double2*>(w + 32 * j);
+DF_UNROLL
+        for (int r = 0; r < 32; r += 2) {
+          const double2 ww = wj[r / 2];
+          if (r >= c && r < rj) a0 += D[tri(r) + c] * ww.x;
+          if (r + 1 >= c && r + 1 < rj) a1 += D[tri(r + 1) + c] * ww.y;
+        }
       }
     }
     for (int i = j + 1; i < T; ++i) {
       if (!mtile(xmask, i, j)) continue;
-      if (lane == 0)
-        while (flag_acquire(rdy + i) != epoch) {
-        }
+#ifdef KD_PROF_WARP
+      const long long qa = clock64();
+#endif
+      if (lane == 0) df_wait(rdy, i, epoch);
       __syncwarp();
+#ifdef KD_PROF_WARP
+      qwait += clock64() - qa;
+#endif
+      const int k = rt_slot(R, 2, i, j);
+      if (k >= 0) {
+        RtDispatch<DF_NC>::off(R, k, w + 32 * i, a0, a1, a2, a3);
+        continue;
+      }
       if (c < rj) {
         const int ri = tile_rows(i, n);
         const double* A = X + off_tile(i, j, n) + c;
         const double2* wi = reinterpret_cast<const double2*>(w + 32 * i);
         if (ri == 32) {
-#pragma unroll
+DF_UNROLL
           for (int r = 0; r < 32; r += 4) {
             const double2 w01 = wi[r / 2], w23 = wi[r / 2 + 1];
             a0 += A[r * LDT] * w01.x;
@@ -579,7 +775,7 @@ __device__ void inv_solve_df(const double* X, const double* b, double* w, double
             a3 += A[(r + 3) * LDT] * w23.y;
           }
         } else {
-#pragma unroll
+DF_UNROLL
           for (int r = 0; r < 32; r += 4) {
             const double2 w01 = wi[r / 2], w23 = wi[r / 2 + 1];
             if (r < ri) a0 += A[r * LDT] * w01.x;
@@ -592,9 +788,11 @@ __device__ void inv_solve_df(const double* X, const double* b, double* w, double
     }
     if (c < rj) xo[32 * j + c] = (a0 + a1) + (a2 + a3);
   }
+#ifdef KD_PROF_WARP
+  if (prof && KD_PROF_WARP == 3) prof[4 + wid] += clock64() - qd0;
+  if (prof && KD_PROF_WARP == 4) prof[4 + wid] += qwait;
+#endif
 }
-
-
 
 // PADMM loop of the dense kernel for GLOBAL_L worlds (any n): the same
 // arithmetic as the register-resident loop of dense_kernel, with every thread
@@ -1028,13 +1226,24 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
       if (d < nr) xv[pos[d]] = -((((v[d] + (d == 0 ? s0 : 0.0)) - eta * x[d]) - rho * yh[d]) - zh[d]);
   };
   write_rhs();
+  RegTiles rtiles;
+  if (df) {
+    rt_load(rtiles, L, n, T, xm);
+    // register tiles multiply whole 32-entry vector segments (zeros in the
+    // tile beyond row/column n): the padding of b and w must hold finite values
+    for (int r = n + tid; r < npad; r += NT) xv[r] = wv_s[r] = 0.0;
+  }
+#ifdef KD_PROF_WARP
+  long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#else
   long long prof[4] = {0, 0, 0, 0};
+#endif
   for (it = 1; it <= sp.max_iters; ++it) {
 #ifdef KD_PROF_PADMM
     const long long p0 = clock64();
 #endif
     if (df) {
-      inv_solve_df<NT>(L, xv, wv_s, xsol, n, T, xm, rdy, it);
+      inv_solve_df<NT>(L, xv, wv_s, xsol, n, T, xm, rdy, it, rtiles, prof);
       __syncthreads();  // x complete
     } else {
       inv_solve<NT>(L, xv, wv_s, n, T, xm, prof);
@@ -1118,6 +1327,9 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   block_max3<NT>(rp, dmax, rc, red);
   const double r_p = rp, r_d = rho * dmax, r_c = rc;
   stamp(4);
+#ifdef KD_PROF_WARP
+  if (lane == 0) ws.phase_cycles[wid] = prof[4 + wid];
+#endif
 #ifdef KD_PROF_PADMM
   if (tid == 0) {
     ws.phase_cycles[5] = prof[0];
