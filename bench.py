@@ -383,8 +383,8 @@ def smem_bytes_per_world(kind, n, iters, applies, plan_slots, solve_terms):
     iteration; the supernodal kernel reads its factor terms (value + vector
     operand) once per iteration; the incidence-owner CR operator moves 4
     doubles per incidence (2 per row) per apply."""
-    if kind in ("dense", "supernodal+dense"):
-        m = plan_slots if kind == "supernodal+dense" else n
+    if kind in ("dense", "supernodal+dense", "supernodal+cluster"):
+        m = plan_slots if kind.startswith("supernodal+") else n
         return 16.0 * iters * m * (m + 1) / 2
     if kind == "supernodal":
         return 16.0 * iters * solve_terms
@@ -536,7 +536,7 @@ def main():
         cri = np.array([d[w].cr_iterations for w in range(Wl)])
         conv_frac.append(float(np.mean([d[w].converged for w in range(Wl)])))
         on_cr = np.array([k == "cr" for k in kinds])
-        on_dense = np.array([k in ("dense", "supernodal", "supernodal+dense") for k in kinds])
+        on_dense = np.array([k in ("dense", "supernodal", "supernodal+dense", "supernodal+cluster") for k in kinds])
         for k in kinds:
             kern_count[k] = kern_count.get(k, 0) + 1
         bytes_dense += float((algorithmic_bytes_k2(n, nb_w, it) * on_dense).sum())

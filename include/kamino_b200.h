@@ -402,6 +402,7 @@ int kd_batch_get_phase_cycles(kd_batch* batch, int64_t* out);
 #define KD_KERNEL_SUPERNODAL 2
 #define KD_KERNEL_CR 3
 #define KD_KERNEL_SUPERNODAL_DENSE 4 /* supernodal factor handed to the dense kernel's L^{-1} + solves */
+#define KD_KERNEL_SUPERNODAL_CLUSTER 5 /* as 4, with the PADMM solves on a CTA pair (K2c, opt-in: KD_CLUSTER=1) */
 int kd_batch_get_kernels(kd_batch* batch, int32_t* out);
 
 /* Per world, which matrix-free kernel solved the last step (diagnostics; the

@@ -36,7 +36,8 @@ KD_BACKEND_DENSE = 0
 KD_BACKEND_MATRIX_FREE = 1
 KD_BACKEND_AUTO = 2
 KD_KERNEL_NONE, KD_KERNEL_DENSE, KD_KERNEL_SUPERNODAL, KD_KERNEL_CR, KD_KERNEL_SUPERNODAL_DENSE = 0, 1, 2, 3, 4
-KERNEL_NAMES = {0: 'none', 1: 'dense', 2: 'supernodal', 3: 'cr', 4: 'supernodal+dense'}
+KD_KERNEL_SUPERNODAL_CLUSTER = 5
+KERNEL_NAMES = {0: 'none', 1: 'dense', 2: 'supernodal', 3: 'cr', 4: 'supernodal+dense', 5: 'supernodal+cluster'}
 CR_PATH_NAMES = {0: 'none', 1: 'incidence', 2: 'rows', 3: 'shared'}
 
 

@@ -98,6 +98,7 @@ constexpr int kSmemMaxRows = 232;
 constexpr int kDenseGlobalMaxRows = KD_DENSE_ROW_CROSSOVER;
 constexpr size_t kSnMaxSmem = 232448;  // per-CTA shared memory opt-in limit (227 KB)
 constexpr int kSnAutoMaxSlots = 32;     // supernodal kernel by default up to one dense tile
+constexpr size_t kClPerCta = 233472 / 2;  // K2c: two CTAs per SM (228 KB of shared memory, 1 KB reserved per CTA)
 
 }  // namespace
 
@@ -149,6 +150,13 @@ struct kd_batch {
   int sparse_mode = 1;
   bool sn_handoff = true;
   int64_t total_snlv = 0, total_snr2p = 0;
+  // K2c (kd_dense_cl.cu, opt-in KD_CLUSTER=1): hand-off models whose X splits
+  // over a CTA pair with two pairs' CTAs per SM (measured slower than K2 on
+  // DR-Legs: DESIGN.md §7)
+  bool cluster = false;
+  std::vector<int> cl_split, cl_xlen;
+  int64_t total_xslab = 0;
+  size_t cl_smem = 0;
   int hist_cap = 0;
   double* d_hist = nullptr;
   double* d_nest = nullptr;  // Nesterov beta table (StepParams::nest_beta)
@@ -412,6 +420,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     b->graphs = !(g && g[0] == '0');
     const char* df = getenv("KD_DENSE_DF");  // KD_DENSE_DF=0: barrier between the dense solve passes
     b->no_df = df && df[0] == '0';
+    const char* cle = getenv("KD_CLUSTER");  // KD_CLUSTER=1: the opt-in K2c path (kd_dense_cl.cu)
+    b->cluster = cle && cle[0] == '1';
   }
   b->n_worlds = n_worlds;
   // model tables
@@ -461,6 +471,44 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       else if (b->sn_handoff && m.sn->S <= kSmemMaxRows && !m.sn->scat.empty()) d.sn = 2;
     }
     for (int k = 0; k < 3; ++k) d.gravity[k] = m.gravity[k];
+    if (i == 0) {
+      b->cl_split.assign(n_models, 0);
+      b->cl_xlen.assign(n_models, 0);
+    }
+    if (d.sn == 2 && b->cluster && m.sn->S <= 256 && m.sn->xmask != ~0ull && row_cap[i] > kClasses[2][0]) {
+      // tile rows [0, k) to CTA 0, [k, T) to CTA 1: the split with the
+      // smaller larger half whose CTAs both fit twice per SM
+      const int T = (m.sn->S + 31) / 32;
+      std::vector<int> rlen(T, 0), ritems(T, 0);
+      for (int ti = 0; ti < T; ++ti)
+        for (int tj = 0; tj <= ti; ++tj)
+          if ((m.sn->xmask >> (ti * (ti + 1) / 2 + tj)) & 1ull) {
+            rlen[ti] += ti == tj ? 528 : 32 * 33;
+            ++ritems[ti];
+          }
+      int items = 0, xlen = 0;
+      for (int ti = 0; ti < T; ++ti) {
+        items += ritems[ti];
+        xlen += rlen[ti];
+      }
+      int best = 0;
+      size_t best_bytes = 0;
+      int l0 = 0;
+      for (int k = 1; k < T; ++k) {
+        l0 += rlen[k - 1];
+        const int own = std::max(l0, xlen - l0);
+        const size_t bytes = dense_cl_smem_bytes(own, items, T);
+        if (bytes + dense_cl_static_bytes() + 1024 <= kClPerCta && (!best || bytes < best_bytes)) {
+          best = k;
+          best_bytes = bytes;
+        }
+      }
+      if (best) {
+        b->cl_split[i] = best;
+        b->cl_xlen[i] = xlen;
+        b->cl_smem = std::max(b->cl_smem, best_bytes);
+      }
+    }
     bodies.insert(bodies.end(), m.bodies.begin(), m.bodies.end());
     joints.insert(joints.end(), m.joints.begin(), m.joints.end());
     geoms.insert(geoms.end(), m.geoms.begin(), m.geoms.end());
@@ -503,6 +551,11 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     W.lslab_off = -1;
     W.snlv_off = -1;
     W.snr2p_off = -1;
+    W.xslab_off = -1;
+    if (b->cl_split[mi]) {
+      W.xslab_off = b->total_xslab;
+      b->total_xslab += b->cl_xlen[mi];
+    }
     if (dm[mi].sn == 2) {
       W.snlv_off = b->total_snlv;
       b->total_snlv += (m.sn->nLv + 1) & ~1;
@@ -629,6 +682,13 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
   KD_CK(mem.alloc(v.ls_valid, b->total_lslots));
   KD_CK(mem.alloc(v.lslab, b->total_lslab));
   KD_CK(mem.alloc(v.sn_lv, b->total_snlv));
+  if (b->total_xslab && mem.alloc(v.xslab, b->total_xslab) != cudaSuccess) {
+    cudaGetLastError();  // no room for the K2c slab: K2 keeps the PADMM of every world
+    b->total_xslab = 0;
+    b->cl_smem = 0;
+    for (DevWorld& W : b->worlds) W.xslab_off = -1;
+    KD_CK(cudaMemcpy(d_worlds, b->worlds.data(), sizeof(DevWorld) * n_worlds, cudaMemcpyHostToDevice));
+  }
   KD_CK(mem.alloc(v.sn_r2p, b->total_snr2p));
   if (cr_smem_bytes(b->cr_all_bin.cap, b->cr_all_bin.nbcap, 512) > 232448) {
     // worlds too large for one CTA's shared memory: the shared CR kernel keeps
@@ -711,6 +771,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
       d.lmask_hi = (int32_t)(uint32_t)(p.lmask >> 32);
       d.xmask_lo = (int32_t)(uint32_t)(p.xmask & 0xffffffffull);
       d.xmask_hi = (int32_t)(uint32_t)(p.xmask >> 32);
+      d.cl_split = b->cl_split[i];
+      d.cl_xlen = b->cl_xlen[i];
       d.kmask_off = (int)kmask.size();
       kmask.insert(kmask.end(), p.kmask.begin(), p.kmask.end());
       d.n_sph = p.n_sph;
@@ -994,6 +1056,10 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
         if (!cnt) continue;
         KD_CK(launch_dense(v, sp, wl, cnt, bin.cap, bin.nt, false, s));
         ++b->launches;
+        if (b->cl_smem && bin.nt == 256) {  // K2c: the PADMM of the bin's K2c worlds
+          KD_CK(launch_dense_cluster(v, sp, wl, cnt, b->cl_smem, s));
+          ++b->launches;
+        }
       }
       {
         const int32_t* wl = part(b->global_bin, cnt);
@@ -1326,7 +1392,7 @@ int kd_batch_get_kernels(kd_batch* b, int32_t* out) {
     const int be = ws[w].backend;
     out[w] = be == BE_SPARSE ? KD_KERNEL_SUPERNODAL
              : (be == BE_DENSE_SMEM || be == BE_DENSE_GLOBAL) ? KD_KERNEL_DENSE
-             : be == BE_DENSE_SN ? KD_KERNEL_SUPERNODAL_DENSE
+             : be == BE_DENSE_SN ? (b->worlds[w].xslab_off >= 0 ? KD_KERNEL_SUPERNODAL_CLUSTER : KD_KERNEL_SUPERNODAL_DENSE)
              : be == BE_MATRIX_FREE ? KD_KERNEL_CR : KD_KERNEL_NONE;
   }
   return KD_OK;

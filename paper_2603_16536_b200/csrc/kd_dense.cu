@@ -1169,6 +1169,27 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   }
   stamp(3);
 
+  if constexpr (!GLOBAL_L) {
+    if (handoff && W.xslab_off >= 0) {
+      // K2c (kd_dense_cl.cu) runs this world's PADMM on a CTA pair: X's
+      // nonzero tiles go to the world's slab in row-major tile order
+      // (off-diagonal tiles 32 x LDT, diagonal tiles packed, 528 doubles each)
+      double* dst = bv.xslab + W.xslab_off;
+      int64_t off = 0;
+      for (int i = 0; i < T; ++i)
+        for (int j = 0; j <= i; ++j) {
+          if (!mtile(xm, i, j)) continue;
+          const int ri = tile_rows(i, n);
+          const double* src = L + (i == j ? diag_tile(i, n) : off_tile(i, j, n));
+          const int len = i == j ? tri(ri) : ri * LDT;
+          for (int e = tid; e < len; e += NT) dst[off + e] = src[e];
+          off += i == j ? 528 : 32 * LDT;
+        }
+      stamp(4);
+      return;
+    }
+  }
+
   if constexpr (GLOBAL_L) {
     // ---- 3'. PADMM (padmm.cpp:87-159) for worlds of any size: thread t owns
     // cone units t, t + NT, ...; y, z, y_hat, z_hat live in the world's HBM

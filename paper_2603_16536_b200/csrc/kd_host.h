@@ -56,6 +56,10 @@ cudaError_t launch_fk(const BatchView& bv, const int32_t* tj, const double* tv, 
 size_t fk_smem_bytes(int nb, int nr);
 void launch_recover(const BatchView& bv, const StepParams& sp, cudaStream_t s, int w0 = 0, int w1 = -1);
 size_t dense_smem_bytes(int n, int nt, bool global_l);
+cudaError_t launch_dense_cluster(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
+                                 size_t smem, cudaStream_t s);
+size_t dense_cl_smem_bytes(int own_len, int n_items, int T);
+size_t dense_cl_static_bytes();
 size_t dense_factor_doubles(int n);
 size_t cr_smem_bytes(int n, int nb, int nt);
 size_t cr_staged_bytes(int n, int nb, int nt);

@@ -124,10 +124,10 @@ struct DevSnPlan {
   int32_t S, nLv, n_jd, lim_base;
   int32_t gram_off, n_gram, pair_off, slotpos_off;
   int32_t sup_off, n_sup, prog_off, prog_words;
-  int32_t n_sph, max_slots, smem_doubles, pad0;  // smem_doubles: per-warp footprint of K2s
+  int32_t n_sph, max_slots, smem_doubles, cl_split;  // smem_doubles: per-warp footprint of K2s; cl_split: first tile row of the cluster PADMM kernel's second CTA (0: the model does not take K2c)
   int32_t gbody_off, n_gbody, kmax, vreg;  // vreg: per-warp vector region (doubles)
   int32_t lmask_lo, lmask_hi, scat_off, n_scat;  // nonzero 32x32 tiles of L in plan order; hand-off scatter list
-  int32_t xmask_lo, xmask_hi, kmask_off, pad2;   // nonzero 32x32 tiles of L^-1; per-L-tile column-group masks
+  int32_t xmask_lo, xmask_hi, kmask_off, cl_xlen;  // nonzero 32x32 tiles of L^-1; per-L-tile column-group masks; K2c slab doubles per world
 };
 
 // Per-world indexing (prefix sums over model capacities).
@@ -145,6 +145,7 @@ struct DevWorld {
   int64_t lslab_off;    // dense-global factor slab (doubles), -1 if none
   int64_t snlv_off;     // supernodal factor hand-off slab (doubles), -1 if none
   int64_t snr2p_off;    // row -> plan position hand-off (int32), -1 if none
+  int64_t xslab_off;    // K2c: the world's X = L^-1 tiles (compact, row-major), -1 if the world does not take K2c
 };
 
 // Per-row Jacobian blocks: J = [block_a | block_b], JM = J M^-1 folded
@@ -250,6 +251,7 @@ struct BatchView {
   const uint8_t* sn_kmask;  // per-L-tile 4-column-group nonzero masks (36 per planned model)
   double* cr_scratch;      // worlds too large for one CTA's shared memory: the shared CR kernel's
   int64_t cr_scratch_stride;  // per-world HBM slab (doubles per world, indexed by world), else null
+  double* xslab;           // K2c hand-off: X = L^-1 per world (nonzero tiles, row-major; off-diagonal 32 x 33, diagonal 528)
   double* sn_lv;           // BE_DENSE_SN hand-off: the factor array per world
   int32_t* sn_r2p;         // BE_DENSE_SN hand-off: compact row -> position per world
 };

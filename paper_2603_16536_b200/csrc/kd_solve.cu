@@ -147,6 +147,7 @@ int build_set(SolveSet& S, const kd_solve_problem* P, int np, const std::vector<
     W.body_off = (int)nbod;
     W.lslab_off = -1;
     W.snlv_off = -1;
+    W.xslab_off = -1;
     W.snr2p_off = -1;
     W.smem_cap = 0;
     for (int c = 0; c < 4; ++c)

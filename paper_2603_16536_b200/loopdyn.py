@@ -459,7 +459,7 @@ class WorldBatch:
 
     def kernels(self):
         """Per world, the device kernel that solved the last step:
-        'none' | 'dense' | 'supernodal' | 'cr'."""
+        'none' | 'dense' | 'supernodal' | 'supernodal+dense' | 'supernodal+cluster' | 'cr'."""
         self._ensure()
         out = np.zeros(max(1, self.n_worlds), np.int32)
         _check(lib().kd_batch_get_kernels(self.handle, _capi.i32ptr(out)))

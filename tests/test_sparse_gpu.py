@@ -122,7 +122,7 @@ def test_handoff_matches_dense_kernel_from_identical_states(monkeypatch):
         de.set_state(p, t, tm)
         ho.step(cfg)
         de.step(cfg)
-        assert ho.kernels() == ["supernodal+dense"] * 16 and de.kernels() == ["dense"] * 16
+        assert set(ho.kernels()) <= {"supernodal+dense", "supernodal+cluster"} and de.kernels() == ["dense"] * 16
         a, d = ho.impulses(), de.impulses()
         worst = max(worst, float(np.abs(a - d).max() / max(1.0, np.abs(d).max())))
         for gh, gd in zip(ho.diagnostics(), de.diagnostics()):
