@@ -14,7 +14,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # full captures at the timed configuration (KD_SPLIT=1 KD_GRAPHS=0: one launch per kernel and step)
 N="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
 export KD_SPLIT=1 KD_GRAPHS=0
-timeout 900 $N -k regex:"dense_kernel<256, 0>" -s 50 -c 1 -o gpurun_out/${TAG}_dense python tools/ncu_bench_target.py dr_legs 4096 50 > gpurun_out/${TAG}_ncu_dense.log 2>&1
+timeout 900 $N -k regex:"dense_kernel<.int.256, .bool.0>" -s 50 -c 1 -o gpurun_out/${TAG}_dense python tools/ncu_bench_target.py dr_legs 4096 50 > gpurun_out/${TAG}_ncu_dense.log 2>&1
 timeout 900 $N -k regex:snfactor_kernel -s 50 -c 1 -o gpurun_out/${TAG}_snfactor python tools/ncu_bench_target.py dr_legs 4096 50 > gpurun_out/${TAG}_ncu_snfactor.log 2>&1
 timeout 900 $N -k regex:assemble_kernel -s 50 -c 1 -o gpurun_out/${TAG}_assemble python tools/ncu_bench_target.py dr_legs 4096 50 > gpurun_out/${TAG}_ncu_assemble.log 2>&1
 timeout 900 $N -k regex:recover_kernel -s 50 -c 1 -o gpurun_out/${TAG}_recover python tools/ncu_bench_target.py dr_legs 4096 50 > gpurun_out/${TAG}_ncu_recover.log 2>&1

@@ -15,10 +15,13 @@ key = f"{kernel}@{workload}"
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                       "dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,"
                       "sm__cycles_active.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,"
-                      "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
+                      "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-hdr, units, vals = rows[0], rows[1], rows[2]
+hdr, units = rows[0], rows[1]
+# the longest captured launch (a bin's first kernel may skip most worlds)
+it = hdr.index("gpu__time_duration.sum")
+vals = max(rows[2:], key=lambda r: float(r[it].replace(",", "")))
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 tot = 0.0
 for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
