@@ -658,7 +658,12 @@ def main():
                        "bodies": [m.n_bodies for m in models], "joints": [m.info.n_joints for m in models],
                        "loops": [m.n_loops for m in models],
                        "rows_mean": rows_mean, "padmm_iterations_mean": iters_mean,
-                       "converged_fraction": float(np.mean(conv_frac)), "dt": cfg.dt,
+                       "converged_fraction": float(np.mean(conv_frac)),
+                       "iteration_regime": ("converging (eps = %g)" % cfg.eps if float(np.mean(conv_frac)) >= 0.5 else
+                                            "fixed %d iterations: %.0f %% of world-steps reach eps = %g within "
+                                            "max_iters, so the rate is a max_iters-iteration figure"
+                                            % (cfg.max_iters, 100.0 * float(np.mean(conv_frac)), cfg.eps)),
+                       "dt": cfg.dt,
                        "integrator": cfg.integrator, "backend": cfg.backend, "settle_steps": args.settle,
                        "kernels": {k: v / rsteps for k, v in kern_count.items()},
                        "jitter": "mt19937_64(seed=1), normal(0,1e-3) (main.cpp:199-211)",
