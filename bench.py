@@ -445,10 +445,21 @@ def main():
         return rc
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the B200 solver has no CPU fallback)")
+    # KD_BENCH_SHARE_GPU=1 (test mode): ranks share the visible GPUs round-robin
+    # and reduce over gloo, so the N-rank path (launcher, deal, reductions)
+    # runs end to end on a box with fewer GPUs than ranks; its `value` is then
+    # not an N-GPU throughput
+    share = os.environ.get("KD_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    red_dev = "cpu" if share else f"cuda:{local}"
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2603_16536_b200 as K
     wl = workloads()[args.workload]
     W = args.worlds_per_gpu or wl[2]
@@ -503,7 +514,7 @@ def main():
         bad = set(clocks.get("reasons") or []) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
         stuck = (clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and not clocks.get("reasons")
                  and clocks["sm_mhz"] < 0.8 * clocks["sm_max_mhz"])
-        redo = torch.tensor([1.0 if (bad or stuck) else 0.0], device=f"cuda:{local}")
+        redo = torch.tensor([1.0 if (bad or stuck) else 0.0], device=red_dev)
         if dist is not None:  # every rank takes the same decision
             dist.all_reduce(redo, op=dist.ReduceOp.MAX)
         if redo.item() == 0.0 or attempt == 1:
@@ -512,8 +523,8 @@ def main():
         for c in chunks:  # keep the e2e chunks on the same trajectory segment
             c[0].step(cfg, args.steps)
     clocks["remeasured"] = remeasured
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-    n_all = torch.tensor([float(Wl)], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    n_all = torch.tensor([float(Wl)], dtype=torch.float64, device=red_dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(n_all, op=dist.ReduceOp.SUM)
@@ -590,7 +601,7 @@ def main():
     d = b.diagnostics()
     rows_mean = float(np.mean([d[w].n_rows for w in range(Wl)]))
     from paper_2603_16536_b200 import sharding
-    run_stats = sharding.reduce_stats(dist, sharding.local_stats(d, Wl), device=f"cuda:{local}")
+    run_stats = sharding.reduce_stats(dist, sharding.local_stats(d, Wl), device=red_dev)
     run_stats["converged_fraction"] = run_stats["converged"] / max(1.0, run_stats["worlds"])
     iters_mean = run_stats["mean_iterations"]
 
@@ -626,8 +637,8 @@ def main():
             hb.sync()
         barrier()
         e2e_ms = f0.elapsed_time(f1)
-        te = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
-        nbytes = torch.tensor([8.0 * (b.pose_len + b.twist_len)], dtype=torch.float64, device=f"cuda:{local}")
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=red_dev)
+        nbytes = torch.tensor([8.0 * (b.pose_len + b.twist_len)], dtype=torch.float64, device=red_dev)
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
             dist.all_reduce(nbytes, op=dist.ReduceOp.SUM)
