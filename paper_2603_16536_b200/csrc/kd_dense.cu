@@ -725,6 +725,9 @@ DF_UNROLL
     if (r < ri) w[32 * i + r] = (a0 + a1) + (a2 + a3);
     __syncwarp();
     if (lane == 0) df_publish(rdy, i, epoch);
+#ifdef KD_PROF_WARP
+    if (prof && KD_PROF_WARP == 5) prof[4 + wid] += clock64() - qd0;
+#endif
   }
   {  // pass 2: tile column wid, rows consumed as they are published
     const int j = wid;

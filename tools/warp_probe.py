@@ -1,7 +1,10 @@
-"""Per-warp cycles of one explicit-inverse solve pass in the dense kernel
-(needs a -DKD_PROF_WARP=1|2 build; run with KD_DENSE_DF=0): mean cycles per
-PADMM iteration each warp spends in its pass-1 tile row (1) or pass-2 tile
-column (2), excluding the barriers.  usage: warp_probe.py LIB [worlds]"""
+"""Per-warp cycles of the explicit-inverse solve in the dense kernel, mean per
+PADMM iteration (needs a -DKD_PROF_WARP=k build):
+  1 / 2  pass-1 tile row / pass-2 tile column, barrier version (KD_DENSE_DF=0);
+  3      dataflow solve: entry barrier -> the warp's column done;
+  4      dataflow solve: time spent waiting for published rows;
+  5      dataflow solve: entry barrier -> the warp's row published.
+usage: warp_probe.py LIB [worlds]"""
 import json
 import os
 import sys
