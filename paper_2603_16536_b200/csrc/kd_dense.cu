@@ -301,6 +301,39 @@ __device__ __forceinline__ void panel_tile(double* L, int i, int k, int n) {
   store_off(A, ri, acc, 1.0, false);
 }
 
+// One 8-row block mb of a tile product: acc[nb][h] += sum_k A(8mb+l/4, k)
+// B(k, 8nb+2(l%4)+h) — the same DMMAs, in the same order, as mma_tile's row
+// block mb, so a tile computed as four row-block jobs is bitwise the same.
+template <class LA, class LB>
+__device__ __forceinline__ void mma_rows(double acc[4][2], int mb, const LA& la, const LB& lb, unsigned kmask = 0xffu) {
+  const int lane = threadIdx.x & 31, qr = lane >> 2, qc = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    if (!((kmask >> ks) & 1u)) continue;
+    const double a = la(8 * mb + qr, 4 * ks + qc);
+    double b[4];
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) b[nb] = lb(4 * ks + qc, 8 * nb + qr);
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) dmma(acc[nb][0], acc[nb][1], a, b[nb]);
+  }
+}
+
+// rows 8mb..8mb+7 of C (off-diagonal, rows) = alpha * acc + beta * C
+__device__ __forceinline__ void store_rows(double* C, int rows, const double acc[4][2], double alpha, bool accumulate,
+                                           int mb) {
+  const int lane = threadIdx.x & 31, qr = lane >> 2, qc = lane & 3;
+  const int r = 8 * mb + qr;
+  if (r >= rows) return;
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int o = r * LDT + 8 * nb + 2 * qc + h;
+      C[o] = accumulate ? C[o] + alpha * acc[nb][h] : alpha * acc[nb][h];
+    }
+}
+
 // ---------------------------------------------------------------- L^{-1}
 // X_kj = Linv_kk * B_kj (in place)
 __device__ __forceinline__ void trmm_left(double* L, int k, int j, int n, int lane) {
@@ -331,6 +364,36 @@ __device__ __forceinline__ void gemm_sub(double* L, int i, int j, int k, int n, 
   mma_tile(acc, OffT{L + off_tile(i, k, n), tile_rows(i, n)}, OffT{L + off_tile(k, j, n), 32}, km);
   store_off(L + off_tile(i, j, n), tile_rows(i, n), acc, -1.0, true);
 }
+
+// Row-block jobs of the two phases whose output rows depend only on the same
+// rows of their left operand (so the four jobs of a tile may run on different
+// warps, in place): a single warp's 32x32 DMMA product is bound by its
+// sub-partition's FP64 tensor rate, so a phase with fewer tiles than warps
+// finishes sooner split into row blocks.
+__device__ __forceinline__ void gemm_sub_rows(double* L, int i, int j, int k, int n, int mb, unsigned km) {
+  const int ri = tile_rows(i, n);
+  if (8 * mb >= ri) return;
+  double acc[4][2];
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+  mma_rows(acc, mb, OffT{L + off_tile(i, k, n), ri}, OffT{L + off_tile(k, j, n), 32}, km);
+  store_rows(L + off_tile(i, j, n), ri, acc, -1.0, true, mb);
+}
+__device__ __forceinline__ void trmm_right_neg_rows(double* L, int i, int k, int n, int mb, unsigned km) {
+  const int ri = tile_rows(i, n);
+  if (8 * mb >= ri) return;
+  double acc[4][2];
+#pragma unroll
+  for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+  double* C = L + off_tile(i, k, n);
+  mma_rows(acc, mb, OffT{C, ri}, DiagL{L + diag_tile(k, n), 32}, km);
+  __syncwarp();
+  store_rows(C, ri, acc, -1.0, false, mb);
+}
+#ifndef KD_INV_SPLIT
+#define KD_INV_SPLIT 1
+#endif
+
 
 // Overwrite the Cholesky factor (diag tiles already inverted) with X = L^{-1}
 // by right-looking block forward substitution on L X = I.
@@ -370,19 +433,47 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, u
     }
     auto row_at = [&](int q) { return full ? kk + 1 + q : nth_bit(rows, q); };
     auto col_at = [&](int q) { return full ? q : nth_bit(cols, q); };
-    // phase 1 (step kk): X_kk,j = Linv_kk B_kk,j for j < kk
-    for (int u = wid; u < nc; u += NW) trmm_left(L, kk, col_at(u), n, lane);
+    // phase 1 (step kk): X_kk,j = Linv_kk B_kk,j for j < kk.  Its output rows
+    // mix every row of B_kk,j, so row-block jobs (one per warp) compute into
+    // registers and store after a barrier.
+    if (KD_INV_SPLIT && nc > 0 && 4 * nc <= NW) {
+      const int t = wid >> 2, mb = wid & 3;
+      const int rk = tile_rows(kk, n);
+      double acc[4][2];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+      double* C = t < nc ? L + off_tile(kk, col_at(t), n) : nullptr;
+      if (C && 8 * mb < rk) mma_rows(acc, mb, DiagL{L + diag_tile(kk, n), rk}, OffT{C, rk});
+      __syncthreads();
+      if (C && 8 * mb < rk) store_rows(C, rk, acc, 1.0, false, mb);
+    } else {
+      for (int u = wid; u < nc; u += NW) trmm_left(L, kk, col_at(u), n, lane);
+    }
     __syncthreads();
     // phase 2 (step kk): B_ij -= L_i,kk X_kk,j for i > kk, j < kk
-    for (int u = wid; u < below * nc; u += NW) {
-      const int i = row_at(u / nc);
-      gemm_sub(L, i, col_at(u % nc), kk, n, lane, km(i, kk));
+    if (KD_INV_SPLIT && below * nc < NW) {  // fewer tiles than warps: row-block jobs
+      for (int u = wid; u < 4 * below * nc; u += NW) {
+        const int t = u >> 2, i = row_at(t / nc);
+        gemm_sub_rows(L, i, col_at(t % nc), kk, n, u & 3, km(i, kk));
+      }
+    } else {
+      for (int u = wid; u < below * nc; u += NW) {
+        const int i = row_at(u / nc);
+        gemm_sub(L, i, col_at(u % nc), kk, n, lane, km(i, kk));
+      }
     }
     __syncthreads();
     // phase 3 (step kk): B_i,kk = -L_i,kk Linv_kk for i > kk
-    for (int u = wid; u < below; u += NW) {
-      const int i = row_at(u);
-      trmm_right_neg(L, i, kk, n, lane, km(i, kk));
+    if (KD_INV_SPLIT && below < NW) {
+      for (int u = wid; u < 4 * below; u += NW) {
+        const int i = row_at(u >> 2);
+        trmm_right_neg_rows(L, i, kk, n, u & 3, km(i, kk));
+      }
+    } else {
+      for (int u = wid; u < below; u += NW) {
+        const int i = row_at(u);
+        trmm_right_neg(L, i, kk, n, lane, km(i, kk));
+      }
     }
     __syncthreads();
   }
