@@ -838,7 +838,9 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     KD_CK(up(v.sn_kmask, kmask));
   }
   for (cudaEvent_t& e : b->ev) KD_CK(cudaEventCreate(&e));
-  KD_CK(cudaDeviceSynchronize());
+  // the uploads above ran on the legacy stream: wait for it alone (a device-wide
+  // synchronize would fail while another host thread captures a step graph)
+  KD_CK(cudaStreamSynchronize(0));
   *out = guard.release();
   return KD_OK;
 }

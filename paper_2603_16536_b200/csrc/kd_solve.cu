@@ -324,7 +324,7 @@ int kd_padmm_solve_batched(int32_t device, const kd_solve_problem* P, int32_t np
     KS_CK(launch_cr(S.v, sp, lists + off, (int)cr.size(), ncap, nbcap,
                     ncap > 256 ? 512 : (ncap > 128 ? 256 : 128), 0));
   }
-  KS_CK(cudaDeviceSynchronize());
+  KS_CK(cudaStreamSynchronize(0));  // the launches above are on the legacy stream
   int32_t err[4];
   KS_CK(cudaMemcpy(err, S.d_err, 16, cudaMemcpyDeviceToHost));
   if (err[0])
@@ -398,7 +398,7 @@ int kd_cr_solve_batched(int32_t device, const kd_solve_problem* P, int32_t np, d
   int32_t* list = nullptr;
   KS_CK(S.dev.up(list, todo));
   KS_CK(launch_cr_shared(S.v, sp, list, (int)todo.size(), ncap, nbcap, 0));
-  KS_CK(cudaDeviceSynchronize());
+  KS_CK(cudaStreamSynchronize(0));  // the launches above are on the legacy stream
   if (S.R) KS_CK(cudaMemcpy(x, S.v.lam, 8 * (size_t)S.R, cudaMemcpyDeviceToHost));
   std::vector<WorldStep> ws(np);
   if (np) KS_CK(cudaMemcpy(ws.data(), S.v.wstep, sizeof(WorldStep) * np, cudaMemcpyDeviceToHost));
