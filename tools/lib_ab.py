@@ -19,7 +19,11 @@ def child(workload, nw, libpath):
     L.LIB_PATH = os.path.abspath(libpath)
     import paper_2603_16536_b200 as K
     from paper_2603_16536_b200 import scenes
-    sc = {"dr_legs": scenes.dr_legs, "stewart_tower": scenes.stewart_tower,
+    def bundled(name):
+        from paper_2603_16536_b200.scene import parse_scene_obj
+        with open(os.path.join(ROOT, "tests", "golden", "scenes_bundle.json")) as f:
+            return parse_scene_obj(json.load(f)[name], name)
+    sc = {"fourbar": lambda: bundled("fourbar"), "dr_legs": scenes.dr_legs, "stewart_tower": scenes.stewart_tower,
           "closed_chain": lambda: scenes.closed_chain(22), "sphere_pile": lambda: scenes.sphere_pile(100),
           "box_pile": lambda: scenes.box_pile(64)}[workload]()
     cfg = K.config_for(sc)
