@@ -63,6 +63,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "world-steps/sec (DR Legs worlds, dense PADMM step)"
+TMEM_B_PER_CLK = 256.0  # tcgen05.ld 32x32b, 8 warps per SM (tools/microbench_tmem.cu on the B200)
 UNIT = "world-steps/s"
 
 
@@ -572,6 +573,7 @@ def main():
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
     sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
     smem_peak = 128.0 * nsm * sm_mhz * 1e6 / 1e9  # GB/s: 128 B/clk/SM shared-memory pipe
+    peak_kind = f"128 B/clk/SM x {nsm} SMs x {sm_mhz:.0f} MHz (sampled SM clock)"
     if cr_ms > dense_ms:
         fam, fam_ms, fam_bytes, fam_smem = "cr", cr_ms, bytes_cr / rsteps, smem_cr / rsteps
         kname = ("cr_op_kernel (K2b: PADMM + warm-started Conjugate Residual over the matrix-free Delassus "
@@ -594,6 +596,20 @@ def main():
                 "memory bytes (X read twice per iteration) / the family event time, against the 128 B/clk/SM "
                 "shared-memory pipe at the sampled SM clock; operand_touch = the SURVEY §8d HBM operand-touch "
                 "model of the reference's dense algorithm (not DRAM traffic: ncu DRAM bytes are in `traffic`)")
+        if kname.startswith("dense_kernel"):
+            # K2 reads X's tiles during PADMM from one register tile per warp,
+            # tensor memory (up to 32 tiles, tcgen05.ld) and shared memory: the
+            # operand roof is both on-chip paths together
+            smem_peak = (128.0 + TMEM_B_PER_CLK) * nsm * sm_mhz * 1e6 / 1e9
+            peak_kind = (f"(128 B/clk shared memory + {TMEM_B_PER_CLK:.0f} B/clk tensor memory, measured by "
+                         f"tools/microbench_tmem.cu) x {nsm} SMs x {sm_mhz:.0f} MHz (sampled SM clock)")
+            note = ("X = L^-1 is formed in shared memory and read during PADMM from one register tile per warp, "
+                    "tensor memory (tcgen05.ld, up to 32 tiles) and shared memory (the rest, and the vector "
+                    "broadcasts): achieved = the solve passes' operand bytes (X read twice per iteration) / the "
+                    "family event time, against both on-chip operand paths at the sampled SM clock; the solve "
+                    "is bound by its per-warp dependency chains (moving most tile reads off shared memory cut "
+                    "the solve by 17 %, DESIGN §9); operand_touch = the SURVEY §8d HBM operand-touch model of "
+                    "the reference's dense algorithm (not DRAM traffic: ncu DRAM bytes are in `traffic`)")
     achieved_smem = fam_smem / (fam_ms / 1e3) / 1e9
     operand_touch = fam_bytes / (fam_ms / 1e3) / 1e9
     worlds_in_launch = sum(v for k, v in kern_count.items() if (k == "cr") == (fam == "cr") and k != "none") / rsteps
@@ -684,7 +700,7 @@ def main():
                                       f"collective"},
             "roofline": {"bound": "smem", "achieved": achieved_smem, "peak": smem_peak, "unit": "GB/s",
                          "frac": achieved_smem / smem_peak,
-                         "peak_kind": f"128 B/clk/SM x {nsm} SMs x {sm_mhz:.0f} MHz (sampled SM clock)",
+                         "peak_kind": peak_kind,
                          "traffic": traffic, "traffic_source": traffic_src, "kernel": kname, "onchip": onchip,
                          "kernel_ms_per_launch": fam_ms, "kernel_share_of_step": fam_ms / step_ms_fam,
                          "algorithmic_smem_bytes_per_launch": fam_smem,

@@ -611,8 +611,11 @@ __device__ __forceinline__ int flag_acquire(const int* f) {
 // tile row.  The dot products run in the same order with the same
 // accumulators as from shared memory (bitwise the same up to the sign of
 // exact zeros).
+#ifndef KD_TMEM
+#define KD_TMEM 1
+#endif
 #ifndef KD_DF_REG
-#define KD_DF_REG 2
+#define KD_DF_REG (KD_TMEM ? 1 : 2)  // with TMEM tiles one register tile per warp measured best
 #endif
 constexpr int DF_NC = KD_DF_REG;
 struct RegTiles {
@@ -631,26 +634,28 @@ __device__ __forceinline__ int rt_slot(const RegTiles& R, int pass, int i, int j
   return s;
 }
 
+// the t-th register-tile candidate of warp wid: 1. the pass-2 tile of the
+// last tile row in this warp's column, 2. the first tiles of this warp's tile
+// row (pass 1)
+__device__ __forceinline__ int rt_cand(int wid, int t, int T, unsigned long long xmask) {
+  if (wid >= T) return -1;
+  if (wid < T - 1 && mtile(xmask, T - 1, wid)) {
+    if (t == 0) return rt_id(2, T - 1, wid);
+    --t;
+  }
+  for (int j = 0; j <= wid; ++j)
+    if (mtile(xmask, wid, j)) {
+      if (t == 0) return rt_id(1, wid, j);
+      --t;
+    }
+  return -1;
+}
+
 // pick and load warp `wid`'s register tiles (after X is final; warp-uniform)
 __device__ void rt_load(RegTiles& R, const double* X, int n, int T, unsigned long long xmask) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // the t-th candidate: 1. the pass-2 tile of the last tile row in this
-  // warp's column, 2. the first tiles of this warp's tile row (pass 1)
-  auto cand = [&](int t) -> int {
-    if (wid >= T) return -1;
-    if (wid < T - 1 && mtile(xmask, T - 1, wid)) {
-      if (t == 0) return rt_id(2, T - 1, wid);
-      --t;
-    }
-    for (int j = 0; j <= wid; ++j)
-      if (mtile(xmask, wid, j)) {
-        if (t == 0) return rt_id(1, wid, j);
-        --t;
-      }
-    return -1;
-  };
 #pragma unroll
-  for (int s = 0; s < DF_NC; ++s) R.id[s] = cand(s);  // static slot index: R stays in registers
+  for (int s = 0; s < DF_NC; ++s) R.id[s] = rt_cand(wid, s, T, xmask);  // static slot index: R stays in registers
 #pragma unroll
   for (int s = 0; s < DF_NC; ++s) {
     const int q = R.id[s];
@@ -724,6 +729,200 @@ struct RtDispatch<0> {
   __device__ __forceinline__ static void diag(const RegTiles&, int, const double*, double&, double&) {}
 };
 
+// Tensor-memory tiles of X for the dataflow solve.  The tile visits of the
+// solve passes that do not fit the register tiles are parked in TMEM (512
+// columns x 128 lanes, allocated per CTA for the PADMM loop; one K2 CTA per
+// SM), in the orientation of the pass that reads them: lane = row (pass 1) or
+// column (pass 2), 32 doubles = 64 columns per tile.  A warp reaches only its
+// lane quarter (warp % 4), which it shares with warp ^ 4: each quarter holds 8
+// tiles, split between its two warps by need.  tcgen05.ld streams a tile row
+// at ~256 B/clk/SM on a path separate from shared memory's 128 B/clk
+// (tools/microbench_tmem.cu), so a TMEM visit costs the shared-memory pipe
+// only its vector broadcast.  Same dot-product order as the register tiles.
+struct TmTiles {
+  unsigned m1, m2;  // bit j: pass-1 tile (wid, j) in TMEM; bit i: pass-2 tile (i, wid)
+  uint32_t c1, c2;  // TMEM address of the first pass-1 / pass-2 tile
+};
+
+// non-register tile visits of warp v, pass-2 tiles first (they sit on the
+// dataflow critical path), then pass 1; at most `budget` of them.  Bit masks
+// over the tile index: row v's tiles (pass 1) and column v's (pass 2); the
+// register tiles (rt_cand's order) are the pass-2 tile (T-1, v) and then the
+// lowest tiles of row v.
+__device__ __forceinline__ unsigned low_bits(unsigned m, int k) {  // the k lowest set bits of m
+  unsigned r = 0u;
+  for (int t = 0; t < k && m; ++t) {
+    const unsigned b = m & (0u - m);
+    r |= b;
+    m ^= b;
+  }
+  return r;
+}
+__device__ __forceinline__ void tm_visits(int v, int T, unsigned long long xmask, int budget, unsigned& m1,
+                                          unsigned& m2, int& need) {
+  m1 = m2 = 0u;
+  need = 0;
+  if (v >= T) return;
+  unsigned row, col = 0u;
+  if (xmask == ~0ull) {
+    row = (2u << v) - 1u;
+    col = ((1u << T) - 1u) & ~((1u << v) - 1u);
+  } else {
+    row = (unsigned)(xmask >> (v * (v + 1) / 2)) & ((2u << v) - 1u);
+    for (int i = v; i < T; ++i) col |= (unsigned)((xmask >> (i * (i + 1) / 2 + v)) & 1ull) << i;
+  }
+  int nreg = DF_NC;
+  if (nreg > 0 && v < T - 1 && ((col >> (T - 1)) & 1u)) {
+    col &= ~(1u << (T - 1));
+    --nreg;
+  }
+  row &= ~low_bits(row, nreg);
+  need = __popc(col) + __popc(row);
+  m2 = low_bits(col, budget);
+  m1 = low_bits(row, budget - __popc(m2));
+}
+
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const double (&d)[8]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    r[2 * k] = (uint32_t)__double2loint(d[k]);
+    r[2 * k + 1] = (uint32_t)__double2hiint(d[k]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+// 8 doubles of this lane's row from TMEM (load and wait in one statement, so
+// no use of the registers can be scheduled before the data arrives)
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, double (&d)[8]) {
+  uint32_t r[16];
+  asm volatile(
+      "{\n tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      " tcgen05.wait::ld.sync.aligned;\n}"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 8; ++k) d[k] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
+}
+
+// 16 doubles of this lane's row (one tcgen05.ld.32x32b.x32, then the wait)
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, double (&d)[16]) {
+  uint32_t r[32];
+  asm volatile(
+      "{\n tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      " tcgen05.wait::ld.sync.aligned;\n}"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 16; ++k) d[k] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
+}
+#ifndef KD_TM_CH
+#define KD_TM_CH 16  // doubles per TMEM load-and-wait (8 or 16)
+#endif
+template <int CH>
+__device__ __forceinline__ void tm_ldc(uint32_t taddr, double (&d)[CH]) {
+  if constexpr (CH == 16) tm_ld16(taddr, d);
+  else tm_ld8(taddr, d);
+}
+
+// the same 4-accumulator (off-diagonal) / 2-accumulator (diagonal) orders as rt_dot_*
+__device__ __forceinline__ void tm_dot_off(uint32_t taddr, const double* v, double& a0, double& a1, double& a2,
+                                           double& a3) {
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll
+  for (int c0 = 0; c0 < 32; c0 += KD_TM_CH) {
+    double t[KD_TM_CH];
+    tm_ldc<KD_TM_CH>(taddr + 2 * c0, t);
+#pragma unroll
+    for (int c = 0; c < KD_TM_CH; c += 4) {
+      const double2 p = v2[(c0 + c) / 2], q = v2[(c0 + c) / 2 + 1];
+      a0 += t[c] * p.x;
+      a1 += t[c + 1] * p.y;
+      a2 += t[c + 2] * q.x;
+      a3 += t[c + 3] * q.y;
+    }
+  }
+}
+__device__ __forceinline__ void tm_dot_diag(uint32_t taddr, const double* v, double& a0, double& a1) {
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll
+  for (int c0 = 0; c0 < 32; c0 += KD_TM_CH) {
+    double t[KD_TM_CH];
+    tm_ldc<KD_TM_CH>(taddr + 2 * c0, t);
+#pragma unroll
+    for (int c = 0; c < KD_TM_CH; c += 2) {
+      const double2 p = v2[(c0 + c) / 2];
+      a0 += t[c] * p.x;
+      a1 += t[c + 1] * p.y;
+    }
+  }
+}
+
+// plan warp wid's TMEM tiles and copy them from X (final, in shared memory)
+// into its lane quarter; tbase = the CTA's allocation (512 columns)
+__device__ void tm_load(TmTiles& M, uint32_t tbase, const double* X, int n, int T, unsigned long long xmask) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lo = wid & 3, hi = lo + 4;
+  unsigned a1, a2, b1, b2;
+  int need_lo, need_hi;
+  tm_visits(lo, T, xmask, 8, a1, a2, need_lo);
+  tm_visits(hi, T, xmask, 8, b1, b2, need_hi);
+  const int bud_lo = min(need_lo, max(4, 8 - need_hi));
+  const int bud_hi = min(need_hi, 8 - bud_lo);
+  int need;
+  tm_visits(wid, T, xmask, wid < 4 ? bud_lo : bud_hi, M.m1, M.m2, need);
+  const uint32_t q = tbase + ((uint32_t)(32 * lo) << 16) + (wid < 4 ? 0u : 64u * bud_lo);
+  M.c1 = q;
+  M.c2 = q + 64u * __popc(M.m1);
+  // lane = row (pass 1) / column (pass 2); zeros outside the tile.  All 32
+  // values are loaded before the four stores (one shared-memory round trip).
+  auto put = [&](uint32_t taddr, int pass, int i, int j) {
+    const int ri = tile_rows(i, n);
+    double d[4][8];
+    if (i == j) {
+      const double* D = X + diag_tile(i, n);
+      if (pass == 1) {
+        const double* row = D + tri(lane);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) d[e >> 3][e & 7] = (lane < ri && e <= lane) ? row[e] : 0.0;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) d[e >> 3][e & 7] = (e >= lane && e < ri) ? D[tri(e) + lane] : 0.0;
+      }
+    } else {
+      const double* A = X + off_tile(i, j, n);
+      if (pass == 1) {
+        const double* row = A + lane * LDT;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) d[e >> 3][e & 7] = lane < ri ? row[e] : 0.0;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) d[e >> 3][e & 7] = e < ri ? A[e * LDT + lane] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tm_st8(taddr + 16 * q, d[q]);
+  };
+  int k = 0;
+  for (int j = 0; j < T; ++j)
+    if ((M.m1 >> j) & 1u) put(M.c1 + 64u * k++, 1, wid, j);
+  k = 0;
+  for (int i = 0; i < T; ++i)
+    if ((M.m2 >> i) & 1u) put(M.c2 + 64u * k++, 2, i, wid);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t tm_addr(uint32_t base, unsigned m, int t) {
+  return base + 64u * __popc(m & ((1u << t) - 1u));
+}
+
 
 // unroll of the shared-memory tile walks in the dataflow solve (columns per
 // step / 4): fewer loads in flight per warp leave registers for register tiles
@@ -766,7 +965,7 @@ __device__ __forceinline__ void df_wait(const int* rdy, int i, int epoch) {
 template <int NT>
 __device__ void inv_solve_df(const double* X, const double* b, double* w, double* xo, int n, int T,
                              unsigned long long xmask, int* rdy, int epoch, const RegTiles& R,
-                             long long* prof = nullptr) {
+                             const TmTiles& M, long long* prof = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();  // b complete
   if (wid >= T) return;  // (the caller's barrier after the solve is outside)
@@ -783,6 +982,10 @@ __device__ void inv_solve_df(const double* X, const double* b, double* w, double
       const int k = rt_slot(R, 1, i, j);
       if (k >= 0) {
         RtDispatch<DF_NC>::off(R, k, b + 32 * j, a0, a1, a2, a3);
+        continue;
+      }
+      if (KD_TMEM && ((M.m1 >> j) & 1u)) {
+        tm_dot_off(tm_addr(M.c1, M.m1, j), b + 32 * j, a0, a1, a2, a3);
         continue;
       }
       if (r < ri) {
@@ -802,6 +1005,8 @@ DF_UNROLL
       const int k = rt_slot(R, 1, i, i);
       if (k >= 0) {
         RtDispatch<DF_NC>::diag(R, k, b + 32 * i, a0, a1);
+      } else if (KD_TMEM && ((M.m1 >> i) & 1u)) {
+        tm_dot_diag(tm_addr(M.c1, M.m1, i), b + 32 * i, a0, a1);
       } else if (r < ri) {
         const double* drow = X + diag_tile(i, n) + tri(r);
         const double2* bi = reinterpret_cast<const double2*>(b + 32 * i);
@@ -829,6 +1034,8 @@ DF_UNROLL
       const int k = rt_slot(R, 2, j, j);
       if (k >= 0) {
         RtDispatch<DF_NC>::diag(R, k, w + 32 * j, a0, a1);
+      } else if (KD_TMEM && ((M.m2 >> j) & 1u)) {
+        tm_dot_diag(tm_addr(M.c2, M.m2, j), w + 32 * j, a0, a1);
       } else if (c < rj) {
         const double* D = X + diag_tile(j, n);
         const double2* wj = reinterpret_cast<const double2*>(w + 32 * j);
@@ -853,6 +1060,10 @@ DF_UNROLL
       const int k = rt_slot(R, 2, i, j);
       if (k >= 0) {
         RtDispatch<DF_NC>::off(R, k, w + 32 * i, a0, a1, a2, a3);
+        continue;
+      }
+      if (KD_TMEM && ((M.m2 >> i) & 1u)) {
+        tm_dot_off(tm_addr(M.c2, M.m2, i), w + 32 * i, a0, a1, a2, a3);
         continue;
       }
       if (c < rj) {
@@ -1072,6 +1283,10 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   const bool df = !GLOBAL_L && T <= NW && !sp.no_df;
   double* xsol = df ? P : xv;
   __shared__ int fail;
+  __shared__ uint32_t tmem_base;  // TMEM allocation of the dataflow solve's tiles
+  // TMEM tiles only where one CTA owns the SM (255 registers x 256 threads):
+  // a second CTA's tcgen05.alloc would wait for the first one's dealloc
+  constexpr bool kTm = KD_TMEM && NT == 256 && !GLOBAL_L;
   const int64_t R0 = W.row_off;
   const RowJ* rj = bv.rowj + R0;
   const int32_t* rb = bv.rbody + 2 * R0;
@@ -1342,8 +1557,33 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   };
   write_rhs();
   RegTiles rtiles;
+  TmTiles mtiles{0u, 0u, 0u, 0u};
+#ifdef KD_PROF_PADMM
+  const long long q_setup = clock64();
+#endif
   if (df) {
     rt_load(rtiles, L, n, T, xm);
+    if (kTm) {
+      if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef KD_PROF_TM
+      const long long q_alloc = clock64();
+#endif
+      tm_load(mtiles, tmem_base, L, n, T, xm);
+#ifdef KD_PROF_TM
+      if (lane == 0) ws.phase_cycles[wid] = clock64() - q_alloc;
+#endif
+    }
+#if defined(KD_PROF_PADMM) && !defined(KD_PROF_TM)
+    __syncthreads();
+    if (tid == 0) ws.phase_cycles[2] = clock64() - q_setup;
+#endif
     // register tiles multiply whole 32-entry vector segments (zeros in the
     // tile beyond row/column n): the padding of b and w must hold finite values
     for (int r = n + tid; r < npad; r += NT) xv[r] = wv_s[r] = 0.0;
@@ -1358,7 +1598,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     const long long p0 = clock64();
 #endif
     if (df) {
-      inv_solve_df<NT>(L, xv, wv_s, xsol, n, T, xm, rdy, it, rtiles, prof);
+      inv_solve_df<NT>(L, xv, wv_s, xsol, n, T, xm, rdy, it, rtiles, mtiles, prof);
       __syncthreads();  // x complete
     } else {
       inv_solve<NT>(L, xv, wv_s, n, T, xm, prof);
@@ -1438,7 +1678,12 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     write_rhs();
   }
   // the last iteration's r_p, r_d, r_c (padmm.cpp:147-157)
-  __syncthreads();  // red is still being read by the last reduction
+  if (kTm && df) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();  // red is still being read by the last reduction (and TMEM reads are done)
+  if (kTm && df && wid == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
   block_max3<NT>(rp, dmax, rc, red);
   const double r_p = rp, r_d = rho * dmax, r_c = rc;
   stamp(4);
