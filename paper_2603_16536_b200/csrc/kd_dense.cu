@@ -824,12 +824,34 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, double (&d)[16]) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) d[k] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
 }
+// a whole 32-double row (one tcgen05.ld.32x32b.x64, then the wait)
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, double (&d)[32]) {
+  uint32_t r[64];
+  asm volatile(
+      "{\n tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+      "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+      " tcgen05.wait::ld.sync.aligned;\n}"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]),
+        "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]),
+        "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+        "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]),
+        "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 32; ++k) d[k] = __hiloint2double((int)r[2 * k + 1], (int)r[2 * k]);
+}
 #ifndef KD_TM_CH
-#define KD_TM_CH 16  // doubles per TMEM load-and-wait (8 or 16)
+#define KD_TM_CH 16  // doubles per TMEM load-and-wait (8, 16 or 32)
 #endif
 template <int CH>
 __device__ __forceinline__ void tm_ldc(uint32_t taddr, double (&d)[CH]) {
-  if constexpr (CH == 16) tm_ld16(taddr, d);
+  if constexpr (CH == 32) tm_ld32(taddr, d);
+  else if constexpr (CH == 16) tm_ld16(taddr, d);
   else tm_ld8(taddr, d);
 }
 
@@ -1315,6 +1337,9 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   }
   for (int e = tid; e < nlen; e += NT) L[e] = 0.0;
   __syncthreads();
+#ifdef KD_PROF_HO
+  const long long h0 = clock64();
+#endif
   if (handoff) {
     // scatter the supernode panels into the tile layout (the plan's flat list
     // of (Lv index, tile index) pairs), then invert the diagonal tiles
@@ -1335,8 +1360,18 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
         if (q[k] != 0xffffffffu) L[q[k] >> 16] = v[k];
     }
     __syncthreads();
+#ifdef KD_PROF_HO
+    const long long h1 = clock64();
+#endif
     for (int k = wid; k < T; k += NW) diag_invert_rinv(L + diag_tile(k, n), tile_rows(k, n), lane);
     __syncthreads();
+#ifdef KD_PROF_HO
+    if (tid == 0) {
+      ws.phase_cycles[5] = h0 - t_prev;  // kernel start -> zero fill done
+      ws.phase_cycles[6] = h1 - h0;      // scatter
+      ws.phase_cycles[7] = clock64() - h1;  // diagonal inverses
+    }
+#endif
     stamp(0);
     stamp(2);
   } else {
