@@ -147,6 +147,7 @@ struct kd_batch {
   std::vector<SnBin> sn_bins;
   bool sparse = true;
   bool no_df = false;
+  bool no_tmem = false;
   int sparse_mode = 1;
   bool sn_handoff = true;
   int64_t total_snlv = 0, total_snr2p = 0;
@@ -420,6 +421,8 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     b->graphs = !(g && g[0] == '0');
     const char* df = getenv("KD_DENSE_DF");  // KD_DENSE_DF=0: barrier between the dense solve passes
     b->no_df = df && df[0] == '0';
+    const char* tme = getenv("KD_TMEM");  // KD_TMEM=0: the dense solve reads X's tiles from shared memory only
+    b->no_tmem = tme && tme[0] == '0';
     const char* cle = getenv("KD_CLUSTER");  // KD_CLUSTER=1: the opt-in K2c path (kd_dense_cl.cu)
     b->cluster = cle && cle[0] == '1';
   }
@@ -1009,6 +1012,7 @@ static StepParams step_params(const kd_batch* b, const kd_step_config* c) {
   sp.sn_handoff = b->sn_handoff ? 1 : 0;
   sp.eta_rho = c->eta + c->rho;
   sp.no_df = b->no_df ? 1 : 0;
+  sp.no_tmem = b->no_tmem ? 1 : 0;
   sp.nest_beta = b->d_nest;
   return sp;
 }

@@ -1309,6 +1309,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   // TMEM tiles only where one CTA owns the SM (255 registers x 256 threads):
   // a second CTA's tcgen05.alloc would wait for the first one's dealloc
   constexpr bool kTm = KD_TMEM && NT == 256 && !GLOBAL_L;
+  const bool tm_on = !sp.no_tmem;  // KD_TMEM=0 at batch creation: tiles from shared memory (same results)
   const int64_t R0 = W.row_off;
   const RowJ* rj = bv.rowj + R0;
   const int32_t* rb = bv.rbody + 2 * R0;
@@ -1598,7 +1599,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
 #endif
   if (df) {
     rt_load(rtiles, L, n, T, xm);
-    if (kTm) {
+    if (kTm && tm_on) {
       if (wid == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                          (unsigned)__cvta_generic_to_shared(&tmem_base)));
@@ -1713,9 +1714,9 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     write_rhs();
   }
   // the last iteration's r_p, r_d, r_c (padmm.cpp:147-157)
-  if (kTm && df) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (kTm && tm_on && df) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();  // red is still being read by the last reduction (and TMEM reads are done)
-  if (kTm && df && wid == 0) {
+  if (kTm && tm_on && df && wid == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }

@@ -262,7 +262,7 @@ struct StepParams {
   int32_t max_iters, acceleration, restart, fixed_mode;
   int32_t cr_iters, warm_start, moreau, backend;  // backend: KD_BACKEND_*
   int32_t sparse, sn_handoff;                      // supernodal path enabled / factor hand-off enabled
-  int32_t cr_only, no_df;  // no_df: KD_DENSE_DF=0 (dense solve passes with a barrier, not dataflow flags); cr_only: one cr_solve(op, rhs = vf, x = x0, cr_iters) per world, no PADMM (kd_cr_solve_batched)
+  int32_t cr_only, no_df, no_tmem;  // no_tmem: KD_TMEM=0 (dense solve tiles from shared memory, not tensor memory); no_df: KD_DENSE_DF=0 (dense solve passes with a barrier, not dataflow flags); cr_only: one cr_solve(op, rhs = vf, x = x0, cr_iters) per world, no PADMM (kd_cr_solve_batched)
   double eta_rho;         // the operator's eta + rho (build_backend's argument; eta + rho in a step)
   const double* nest_beta;  // Nesterov beta_m = (a_m - 1) / a_{m+1}, a_0 = 1, m < max_iters (padmm.cpp:54-71)
 };
