@@ -1633,9 +1633,15 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
 #ifdef KD_PROF_PADMM
     const long long p0 = clock64();
 #endif
+#ifdef KD_PROF_WARP
+    long long qu0 = clock64();
+#endif
     if (df) {
       inv_solve_df<NT>(L, xv, wv_s, xsol, n, T, xm, rdy, it, rtiles, mtiles, prof);
       __syncthreads();  // x complete
+#ifdef KD_PROF_WARP
+      qu0 = clock64();
+#endif
     } else {
       inv_solve<NT>(L, xv, wv_s, n, T, xm, prof);
     }
@@ -1674,7 +1680,14 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     if (kind != ROW_BILATERAL) rc = fmin(ymax, zmax);
     // max(r_p, r_d, r_c) (padmm.cpp:128-131) in one reduction: rho > 0, so
     // max(rho * dmax_i) = rho * max(dmax_i) exactly
+#ifdef KD_PROF_WARP
+    const long long qu1 = clock64();
+    if (KD_PROF_WARP == 6) prof[4 + wid] += qu1 - qu0;
+#endif
     const double combined = block_max_nonneg<NT>(fmax(rp, fmax(rho * dmax, rc)), red);
+#ifdef KD_PROF_WARP
+    if (KD_PROF_WARP == 7) prof[4 + wid] += clock64() - qu1;
+#endif
 #ifdef KD_PROF_PADMM
     const long long p2 = clock64();
     prof[2] += p2 - p1;

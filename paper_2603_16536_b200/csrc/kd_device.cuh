@@ -172,7 +172,7 @@ __device__ __forceinline__ double fast_div(double y, double x) {
   return fma(fma(-x, q, y), r, q);
 }
 __device__ __forceinline__ double fast_sqrt(double x) {
-  if (!(x > 1e-30 && x < 1e30)) return sqrt(x);
+  if (!(x > 1e-30 && x < 1e30)) return x == 0.0 ? x : sqrt(x);  // sqrt(+-0) = +-0 without the slow path
   return x * fast_rsqrt(x);
 }
 

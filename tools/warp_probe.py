@@ -3,7 +3,9 @@ PADMM iteration (needs a -DKD_PROF_WARP=k build):
   1 / 2  pass-1 tile row / pass-2 tile column, barrier version (KD_DENSE_DF=0);
   3      dataflow solve: entry barrier -> the warp's column done;
   4      dataflow solve: time spent waiting for published rows;
-  5      dataflow solve: entry barrier -> the warp's row published.
+  5      dataflow solve: entry barrier -> the warp's row published;
+  6      PADMM units: x-complete barrier -> before the residual reduction;
+  7      the block residual reduction (warp max, barrier, partials).
 usage: warp_probe.py LIB [worlds]"""
 import json
 import os
