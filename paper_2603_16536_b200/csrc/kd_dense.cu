@@ -966,6 +966,9 @@ __device__ __forceinline__ void df_publish(int* rdy, int i, int epoch) {
   __threadfence_block();
   flag_release(rdy + i, epoch);
 }
+#ifndef KD_DF_BATCH
+#define KD_DF_BATCH 1
+#endif
 __device__ __forceinline__ void df_wait(const int* rdy, int i, int epoch) {
   while (flag_acquire(rdy + i) != epoch) {
 #if KD_DF_WAIT > 0
@@ -1069,12 +1072,27 @@ DF_UNROLL
         }
       }
     }
+    unsigned ready = 0u;  // KD_DF_BATCH: bit i = row i seen published (this epoch)
     for (int i = j + 1; i < T; ++i) {
       if (!mtile(xmask, i, j)) continue;
 #ifdef KD_PROF_WARP
       const long long qa = clock64();
 #endif
-      if (lane == 0) df_wait(rdy, i, epoch);
+      if (KD_DF_BATCH) {
+        // one acquire per lane (lane k polls row k): every row published by
+        // now is seen at once, so later rows of the column need no poll
+        while (!((ready >> i) & 1u)) {
+          const int f = lane < T ? flag_acquire(rdy + lane) : epoch;
+          ready = __ballot_sync(0xffffffffu, f == epoch);
+          if (!((ready >> i) & 1u)) {
+#if KD_DF_WAIT > 0
+            __nanosleep(KD_DF_WAIT);
+#endif
+          }
+        }
+      } else if (lane == 0) {
+        df_wait(rdy, i, epoch);
+      }
       __syncwarp();
 #ifdef KD_PROF_WARP
       qwait += clock64() - qa;
