@@ -742,7 +742,25 @@ struct RtDispatch<0> {
 struct TmTiles {
   unsigned m1, m2;  // bit j: pass-1 tile (wid, j) in TMEM; bit i: pass-2 tile (i, wid)
   uint32_t c1, c2;  // TMEM address of the first pass-1 / pass-2 tile
+  unsigned r1, r2;  // bit j: tile (wid, j), j < wid, of X nonzero; bit i: tile (i, wid), i > wid, nonzero
 };
+// the warp's nonzero off-diagonal tiles of its tile row / tile column (the
+// solve passes walk these bits instead of testing the mask per tile)
+__device__ __forceinline__ void df_masks(TmTiles& M, int T, unsigned long long xmask) {
+  const int v = threadIdx.x >> 5;
+  unsigned row = 0u, col = 0u;
+  if (v < T) {
+    if (xmask == ~0ull) {
+      row = (1u << v) - 1u;
+      col = ((1u << T) - 1u) & ~((2u << v) - 1u);
+    } else {
+      row = (unsigned)(xmask >> (v * (v + 1) / 2)) & ((1u << v) - 1u);
+      for (int i = v + 1; i < T; ++i) col |= (unsigned)((xmask >> (i * (i + 1) / 2 + v)) & 1ull) << i;
+    }
+  }
+  M.r1 = row;
+  M.r2 = col;
+}
 
 // non-register tile visits of warp v, pass-2 tiles first (they sit on the
 // dataflow critical path), then pass 1; at most `budget` of them.  Bit masks
@@ -1002,8 +1020,8 @@ __device__ void inv_solve_df(const double* X, const double* b, double* w, double
     const int i = wid;
     const int ri = tile_rows(i, n), r = lane;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int j = 0; j < i; ++j) {
-      if (!mtile(xmask, i, j)) continue;
+    for (unsigned mj = M.r1; mj; mj &= mj - 1u) {
+      const int j = __ffs(mj) - 1;
       const int k = rt_slot(R, 1, i, j);
       if (k >= 0) {
         RtDispatch<DF_NC>::off(R, k, b + 32 * j, a0, a1, a2, a3);
@@ -1073,8 +1091,8 @@ DF_UNROLL
       }
     }
     unsigned ready = 0u;  // KD_DF_BATCH: bit i = row i seen published (this epoch)
-    for (int i = j + 1; i < T; ++i) {
-      if (!mtile(xmask, i, j)) continue;
+    for (unsigned mi = M.r2; mi; mi &= mi - 1u) {
+      const int i = __ffs(mi) - 1;
 #ifdef KD_PROF_WARP
       const long long qa = clock64();
 #endif
@@ -1611,12 +1629,13 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   };
   write_rhs();
   RegTiles rtiles;
-  TmTiles mtiles{0u, 0u, 0u, 0u};
+  TmTiles mtiles{0u, 0u, 0u, 0u, 0u, 0u};
 #ifdef KD_PROF_PADMM
   const long long q_setup = clock64();
 #endif
   if (df) {
     rt_load(rtiles, L, n, T, xm);
+    df_masks(mtiles, T, xm);
     if (kTm && tm_on) {
       if (wid == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
