@@ -987,6 +987,13 @@ __device__ __forceinline__ void df_publish(int* rdy, int i, int epoch) {
 #ifndef KD_DF_BATCH
 #define KD_DF_BATCH 1
 #endif
+// KD_DF_UNITS: each thread takes the cone unit whose first row sits at its own
+// solve position, so a warp's units read the x segment its own pass-2 column
+// produced (contacts spanning segments wait on the other columns' flags) and
+// the barrier between the solve and the units goes away
+#ifndef KD_DF_UNITS
+#define KD_DF_UNITS 1
+#endif
 __device__ __forceinline__ void df_wait(const int* rdy, int i, int epoch) {
   while (flag_acquire(rdy + i) != epoch) {
 #if KD_DF_WAIT > 0
@@ -1009,6 +1016,7 @@ template <int NT>
 __device__ void inv_solve_df(const double* X, const double* b, double* w, double* xo, int n, int T,
                              unsigned long long xmask, int* rdy, int epoch, const RegTiles& R,
                              const TmTiles& M, long long* prof = nullptr) {
+  int* crdy = rdy + 8;  // tile-column flags: x segment j final (KD_DF_UNITS)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();  // b complete
   if (wid >= T) return;  // (the caller's barrier after the solve is outside)
@@ -1150,6 +1158,10 @@ DF_UNROLL
       }
     }
     if (c < rj) xo[32 * j + c] = (a0 + a1) + (a2 + a3);
+    if (KD_DF_UNITS) {
+      __syncwarp();
+      if (lane == 0) df_publish(crdy, j, epoch);
+    }
   }
 #ifdef KD_PROF_WARP
   if (prof && KD_PROF_WARP == 3) prof[4 + wid] += clock64() - qd0;
@@ -1361,7 +1373,7 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
     }
   };
   if (tid == 0) fail = 0;
-  if (tid < 8) rdy[tid] = 0;
+  if (tid < 16) rdy[tid] = 0;  // 8 tile-row + 8 tile-column flags
   if (handoff) {  // rbs holds the row -> plan position map; b is zero at unused positions
     for (int r = tid; r < ws.n_rows; r += NT) rbs[r] = bv.sn_r2p[W.snr2p_off + r];
     for (int r = tid; r < npad; r += NT) xv[r] = 0.0;
@@ -1583,9 +1595,25 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   const int n_jd = ws.n_rows - ws.n_limits - 3 * ws.n_contacts;
   const int first_contact = n_jd + ws.n_limits;
   const int n_units = first_contact + ws.n_contacts;
-  const bool has_unit = tid < n_units;
-  const int row0 = tid < first_contact ? tid : first_contact + 3 * (tid - first_contact);
-  const int kind = !has_unit ? ROW_BILATERAL : (tid < n_jd ? ROW_BILATERAL : (tid < first_contact ? ROW_LIMIT : ROW_CONTACT));
+  // this thread's cone unit: unit tid, or (KD_DF_UNITS, dataflow solve) the
+  // unit whose first row sits at solve position tid (npad <= NT); the units'
+  // arithmetic does not depend on the assignment
+  int uix = tid;
+  if (KD_DF_UNITS && df) {
+    int* uat = reinterpret_cast<int*>(wv_s);  // npad ints; wv_s is free before the first solve
+    for (int p = tid; p < npad; p += NT) uat[p] = -1;
+    __syncthreads();
+    for (int u = tid; u < n_units; u += NT) {
+      const int r0 = u < first_contact ? u : first_contact + 3 * (u - first_contact);
+      uat[handoff ? rbs[r0] : r0] = u;
+    }
+    __syncthreads();
+    uix = tid < npad ? uat[tid] : -1;
+    __syncthreads();
+  }
+  const bool has_unit = uix >= 0 && uix < n_units;
+  const int row0 = !has_unit ? 0 : (uix < first_contact ? uix : first_contact + 3 * (uix - first_contact));
+  const int kind = !has_unit ? ROW_BILATERAL : (uix < n_jd ? ROW_BILATERAL : (uix < first_contact ? ROW_LIMIT : ROW_CONTACT));
   const int nr = !has_unit ? 0 : (kind == ROW_CONTACT ? 3 : 1);
   const double mu = has_unit ? bv.rmu[R0 + row0] : 0.0;
   int pos[3] = {row0, row0 + 1, row0 + 2};  // the unit's rows in the solve's order
@@ -1675,7 +1703,26 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
 #endif
     if (df) {
       inv_solve_df<NT>(L, xv, wv_s, xsol, n, T, xm, rdy, it, rtiles, mtiles, prof);
-      __syncthreads();  // x complete
+      if (KD_DF_UNITS) {
+        // the x segments this warp's units read: its own column (published by
+        // this warp) and, for contacts spanning segments, other columns
+        unsigned need = 0u;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          if (d < nr) need |= 1u << (pos[d] >> 5);
+        need = __reduce_or_sync(0xffffffffu, need) & ~(1u << wid);
+        unsigned ready = 0u;
+        while ((ready & need) != need) {
+          const int f = lane < T ? flag_acquire(rdy + 8 + lane) : it;
+          ready = __ballot_sync(0xffffffffu, f == it);
+#if KD_DF_WAIT > 0
+          if ((ready & need) != need) __nanosleep(KD_DF_WAIT);
+#endif
+        }
+        __syncwarp();
+      } else {
+        __syncthreads();  // x complete
+      }
 #ifdef KD_PROF_WARP
       qu0 = clock64();
 #endif
@@ -1820,7 +1867,7 @@ size_t dense_smem_bytes(int n, int nt, bool global_l) {
   const size_t nl = (size_t)528 * (T - 1) * (T - 1) + (size_t)(T - 1) * 33 * rl + (size_t)rl * (rl + 1) / 2;
   const size_t nlen = global_l ? 0 : ((nl + 1) & ~(size_t)1);
   const size_t npad = 32 * (size_t)T;
-  return 8 * (nlen + 3 * npad + 3 * (nt / 32) + 1) + 4 * 2 * npad + 8 * 32 + 32 + 64;
+  return 8 * (nlen + 3 * npad + 3 * (nt / 32) + 1) + 4 * 2 * npad + 8 * 32 + 64 + 64;  // + 16 flag words
 }
 
 template <int NT, bool G>
