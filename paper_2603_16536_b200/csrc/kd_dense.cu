@@ -408,7 +408,7 @@ __device__ __forceinline__ bool mtile(unsigned long long mask, int ti, int tj) {
 }
 template <int NT>
 __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, unsigned long long xmask,
-                            const uint8_t* kmask = nullptr) {
+                            const uint8_t* kmask = nullptr, long long* prof = nullptr) {
   auto km = [&](int i, int k) -> unsigned { return kmask ? kmask[i * (i + 1) / 2 + k] : 0xffu; };
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -417,6 +417,9 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, u
     return __ffs(m) - 1;
   };
   const bool full = lmask == ~0ull && xmask == ~0ull;  // dense factor: every tile, any T
+#ifdef KD_PROF_INV
+  long long c1 = 0, c2 = 0, c3 = 0, cq = clock64();
+#endif
   for (int k = 1; k < T; ++k) {
     // the column-(k-1) contributions B_i,k-1 = -L_i,k-1 Linv_k-1 (phase 3 of step k-1)
     // and B_ij -= L_i,k-1 X_k-1,j (phase 2) are applied below, in order.
@@ -450,6 +453,9 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, u
       for (int u = wid; u < nc; u += NW) trmm_left(L, kk, col_at(u), n, lane);
     }
     __syncthreads();
+#ifdef KD_PROF_INV
+    { const long long t = clock64(); c1 += t - cq; cq = t; }
+#endif
     // phase 2 (step kk): B_ij -= L_i,kk X_kk,j for i > kk, j < kk
     if (KD_INV_SPLIT && below * nc < NW) {  // fewer tiles than warps: row-block jobs
       for (int u = wid; u < 4 * below * nc; u += NW) {
@@ -463,6 +469,9 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, u
       }
     }
     __syncthreads();
+#ifdef KD_PROF_INV
+    { const long long t = clock64(); c2 += t - cq; cq = t; }
+#endif
     // phase 3 (step kk): B_i,kk = -L_i,kk Linv_kk for i > kk
     if (KD_INV_SPLIT && below < NW) {
       for (int u = wid; u < 4 * below; u += NW) {
@@ -476,11 +485,22 @@ __device__ void tri_inverse(double* L, int n, int T, unsigned long long lmask, u
       }
     }
     __syncthreads();
+#ifdef KD_PROF_INV
+    { const long long t = clock64(); c3 += t - cq; cq = t; }
+#endif
   }
   // final step T-1: X_T-1,j = Linv B for j < T-1
   for (int u = wid; u < T - 1; u += NW)
     if (mtile(xmask, T - 1, u)) trmm_left(L, T - 1, u, n, lane);
   __syncthreads();
+#ifdef KD_PROF_INV
+  if (prof && threadIdx.x == 0) {
+    prof[5] = c1;  // phase 1 (incl. its barriers)
+    prof[6] = c2;  // phase 2
+    prof[7] = c3;  // phase 3
+    prof[1] = clock64() - cq;  // final step
+  }
+#endif
 }
 
 // x = X^T X b with X = L^{-1} (so x = D^{-1} b).  Warp i owns tile row i for
@@ -1558,7 +1578,12 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
       lm = ((unsigned long long)(uint32_t)SP.lmask_hi << 32) | (uint32_t)SP.lmask_lo;
       xm = ((unsigned long long)(uint32_t)SP.xmask_hi << 32) | (uint32_t)SP.xmask_lo;
     }
+#ifdef KD_PROF_INV
+    tri_inverse<NT>(L, n, T, lm, xm, handoff ? bv.sn_kmask + bv.snplan[W.model].kmask_off : nullptr,
+                    reinterpret_cast<long long*>(ws.phase_cycles));
+#else
     tri_inverse<NT>(L, n, T, lm, xm, handoff ? bv.sn_kmask + bv.snplan[W.model].kmask_off : nullptr);
+#endif
   }
   stamp(3);
 
