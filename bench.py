@@ -532,6 +532,9 @@ def main():
     ms_max = float(t.item())
     total_worlds = int(n_all.item())
     value = total_worlds * args.steps / (ms_max / 1e3)
+    # the last timed step's per-world diagnostics: the same trajectory point
+    # (settle + warm-up + steps) as the CPU baseline's
+    d_timed = b.diagnostics()
 
     # ---- roofline pass: per-world n, iterations and kernel of a few more
     # (statistically identical) steps for the algorithmic models
@@ -614,7 +617,7 @@ def main():
     operand_touch = fam_bytes / (fam_ms / 1e3) / 1e9
     worlds_in_launch = sum(v for k, v in kern_count.items() if (k == "cr") == (fam == "cr") and k != "none") / rsteps
     traffic, traffic_src, onchip = ncu_traffic(kname.split(" ")[0], args.workload, worlds_in_launch)
-    d = b.diagnostics()
+    d = d_timed
     rows_mean = float(np.mean([d[w].n_rows for w in range(Wl)]))
     from paper_2603_16536_b200 import sharding
     run_stats = sharding.reduce_stats(dist, sharding.local_stats(d, Wl), device=red_dev)
