@@ -80,6 +80,10 @@ struct Bin {
   int count = 0;
   int32_t* d_worlds = nullptr;
   std::vector<int32_t> worlds;
+  // every world's model is planned with all collision pairs in planned slots,
+  // so K1 never sends one of them here (kd_assemble.cu backend choice): the
+  // launch is skipped (an empty 1-CTA-per-world launch still costs ~10 us)
+  bool never = false;
   // the batch's parts (world ranges [cut[p], cut[p+1])): this bin's worlds in each
   int hoff[4] = {0, 0, 0, 0}, hcount[4] = {0, 0, 0, 0};
   void set_parts(const int* cut, int np) {
@@ -594,14 +598,29 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     h_pose.insert(h_pose.end(), m.init_pose.begin(), m.init_pose.end());
     h_twist.insert(h_twist.end(), m.init_twist.begin(), m.init_twist.end());
   }
+  // models whose worlds always take their plan's kernel under a dense choice:
+  // K2s end to end (sn == 1) never reaches the dense bins, the hand-off
+  // (sn == 2) runs in them but never in the HBM-slab bin
+  std::vector<int> always_planned(n_models, 0);
+  for (int i = 0; i < n_models; ++i) {
+    const auto* pl = b->models[i].sn.get();
+    bool all = dm[i].sn != 0 && pl;
+    if (all)
+      for (int32_t ps : pl->pair_slot) all = all && ps >= 0;
+    always_planned[i] = all ? dm[i].sn : 0;
+  }
   for (int c = 0; c < 4; ++c) {
     if (class_worlds[c].empty()) continue;
     Bin bin;
     bin.cap = kClasses[c][0];
     bin.nt = kClasses[c][1];
     bin.worlds = class_worlds[c];
+    bin.never = true;
+    for (int32_t w : bin.worlds) bin.never = bin.never && always_planned[world_model[w]] == 1;
     b->dense_bins.push_back(bin);
   }
+  b->global_bin.never = true;
+  for (int32_t w : b->global_bin.worlds) b->global_bin.never = b->global_bin.never && always_planned[world_model[w]] != 0;
   for (int i = 0; i < n_models; ++i) {
     if (!dm[i].sn) continue;
     kd_batch::SnBin sbn;
@@ -1059,7 +1078,7 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
       }
       for (const Bin& bin : b->dense_bins) {
         const int32_t* wl = part(bin, cnt);
-        if (!cnt) continue;
+        if (!cnt || bin.never) continue;
         KD_CK(launch_dense(v, sp, wl, cnt, bin.cap, bin.nt, false, s));
         ++b->launches;
         if (b->cl_smem && bin.nt == 256) {  // K2c: the PADMM of the bin's K2c worlds
@@ -1069,7 +1088,7 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
       }
       {
         const int32_t* wl = part(b->global_bin, cnt);
-        if (cnt) {
+        if (cnt && !b->global_bin.never) {
           KD_CK(launch_dense(v, sp, wl, cnt, b->global_bin.cap, 256, true, s));
           ++b->launches;
         }
