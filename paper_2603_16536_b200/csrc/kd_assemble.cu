@@ -590,31 +590,48 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
   // ---- 6. rows: JM, preconditioner, v_f, remaining warm start (delassus.cpp:12-57; stepper.cpp:19-46, 175-176)
   const bool jvalid = sp.warm_start && ws.jcache_valid;
   for (int r = lane; r < n; r += 32) {
-    RowJ& R = rj[r];
+    // J in registers (16-byte loads), JM formed there and written with
+    // 16-byte stores: the scalar read-modify-write of the row filled the
+    // load/store queue (ncu: lg_throttle 25 % of K1's stalls); same
+    // arithmetic in the same order
+    double2* R2 = reinterpret_cast<double2*>(&rj[r]);
+    double J[12], JMr[12];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double2 v = R2[k];
+      J[2 * k] = v.x;
+      J[2 * k + 1] = v.y;
+    }
     const int ba = rb[2 * r], bb = rb[2 * r + 1];
     double d = reg[r];
     if (ba >= 0) {
       const BodyS& B = bs[ba];
-      const V3 t = vmat(V3{R.J[3], R.J[4], R.J[5]}, ldm(B.Iwinv));
-      R.JM[0] = R.J[0] * B.inv_mass; R.JM[1] = R.J[1] * B.inv_mass; R.JM[2] = R.J[2] * B.inv_mass;
-      R.JM[3] = t.x; R.JM[4] = t.y; R.JM[5] = t.z;
+      const V3 t = vmat(V3{J[3], J[4], J[5]}, ldm(B.Iwinv));
+      JMr[0] = J[0] * B.inv_mass; JMr[1] = J[1] * B.inv_mass; JMr[2] = J[2] * B.inv_mass;
+      JMr[3] = t.x; JMr[4] = t.y; JMr[5] = t.z;
       double s = 0;
-      for (int k = 0; k < 6; ++k) s += R.JM[k] * R.J[k];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s += JMr[k] * J[k];
       d += s;
     } else {
-      for (int k = 0; k < 6; ++k) R.JM[k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) JMr[k] = 0.0;
     }
     if (bb >= 0) {
       const BodyS& B = bs[bb];
-      const V3 t = vmat(V3{R.J[9], R.J[10], R.J[11]}, ldm(B.Iwinv));
-      R.JM[6] = R.J[6] * B.inv_mass; R.JM[7] = R.J[7] * B.inv_mass; R.JM[8] = R.J[8] * B.inv_mass;
-      R.JM[9] = t.x; R.JM[10] = t.y; R.JM[11] = t.z;
+      const V3 t = vmat(V3{J[9], J[10], J[11]}, ldm(B.Iwinv));
+      JMr[6] = J[6] * B.inv_mass; JMr[7] = J[7] * B.inv_mass; JMr[8] = J[8] * B.inv_mass;
+      JMr[9] = t.x; JMr[10] = t.y; JMr[11] = t.z;
       double s = 0;
-      for (int k = 0; k < 6; ++k) s += R.JM[6 + k] * R.J[6 + k];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s += JMr[6 + k] * J[6 + k];
       d += s;
     } else {
-      for (int k = 0; k < 6; ++k) R.JM[6 + k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) JMr[6 + k] = 0.0;
     }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) R2[6 + k] = make_double2(JMr[2 * k], JMr[2 * k + 1]);
     scale[r] = 1.0 / sqrt(fmax(d, 1e-12));
   }
   __syncwarp();
