@@ -641,19 +641,30 @@ __global__ void __launch_bounds__(256) assemble_kernel(BatchView bv, StepParams 
       p = scale[first_contact + 3 * ((r - first_contact) / 3)];
     }
     // v_f = J u_free - v*; scaled by P
-    double u6a[6], u6b[6];
+    // (16-byte loads: BodyS::uf and the RowJ halves are 16-byte aligned)
     const int ba = rb[2 * r], bb = rb[2 * r + 1];
+    const double2* J2 = reinterpret_cast<const double2*>(rj[r].J);
     double s = 0.0;
     if (ba >= 0) {
-      for (int k = 0; k < 6; ++k) u6a[k] = bs[ba].uf[k];
+      const double2* u2 = reinterpret_cast<const double2*>(bs[ba].uf);
       double t = 0;
-      for (int k = 0; k < 6; ++k) t += rj[r].J[k] * u6a[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double2 j = J2[k], u = u2[k];
+        t += j.x * u.x;
+        t += j.y * u.y;
+      }
       s += t;
     }
     if (bb >= 0) {
-      for (int k = 0; k < 6; ++k) u6b[k] = bs[bb].uf[k];
+      const double2* u2 = reinterpret_cast<const double2*>(bs[bb].uf);
       double t = 0;
-      for (int k = 0; k < 6; ++k) t += rj[r].J[6 + k] * u6b[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double2 j = J2[3 + k], u = u2[k];
+        t += j.x * u.x;
+        t += j.y * u.y;
+      }
       s += t;
     }
     vf[r] = p * (s - bias[r]);

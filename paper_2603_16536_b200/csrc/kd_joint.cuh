@@ -41,9 +41,14 @@ __device__ __forceinline__ double joint_coord(const DevJoint& j, const Frames& f
 }
 
 __device__ __forceinline__ void put_row(RowJ* rj, int32_t* rb, int r, int ba, int bb, V3 al, V3 aa, V3 bl, V3 ba3) {
-  double* J = rj[r].J;
-  J[0] = al.x; J[1] = al.y; J[2] = al.z; J[3] = aa.x; J[4] = aa.y; J[5] = aa.z;
-  J[6] = bl.x; J[7] = bl.y; J[8] = bl.z; J[9] = ba3.x; J[10] = ba3.y; J[11] = ba3.z;
+  // six 16-byte stores (RowJ rows are 16-byte aligned: 192-byte rows in a cudaMalloc'd array)
+  double2* J = reinterpret_cast<double2*>(rj[r].J);
+  J[0] = make_double2(al.x, al.y);
+  J[1] = make_double2(al.z, aa.x);
+  J[2] = make_double2(aa.y, aa.z);
+  J[3] = make_double2(bl.x, bl.y);
+  J[4] = make_double2(bl.z, ba3.x);
+  J[5] = make_double2(ba3.y, ba3.z);
   rb[2 * r] = ba;
   rb[2 * r + 1] = bb;
 }

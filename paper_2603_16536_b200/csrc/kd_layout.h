@@ -15,6 +15,7 @@
 //   row_off[w] + r with r in the reference row order
 //   [bilateral | dynamics | limits | contacts] (constraints.hpp:33-38).
 #pragma once
+#include <cstddef>
 
 #include <stdint.h>
 
@@ -167,6 +168,10 @@ struct BodyS {
   double mass, inv_mass;
   double up[6];      // u+
 };
+
+// K1 moves RowJ halves and BodyS::uf with 16-byte accesses (arrays are cudaMalloc'd)
+static_assert(sizeof(RowJ) % 16 == 0, "RowJ rows must keep 16-byte alignment");
+static_assert(sizeof(BodyS) % 16 == 0 && offsetof(BodyS, uf) % 16 == 0, "BodyS::uf must be 16-byte aligned");
 
 struct Contact {
   int32_t ga, gb, pair, pad;
