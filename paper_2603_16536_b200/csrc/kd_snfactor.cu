@@ -133,19 +133,22 @@ __global__ void __launch_bounds__(kFactorThreads, kFactorMinBlocks)
         if (diag) Lv[g.dst] = 1.0;
         return;
       }
-      const double* a = rj[rs].JM + ((g.flags & SG_S1) ? 6 : 0);
-      const double* c = rj[rt].J + ((g.flags & SG_T1) ? 6 : 0);
-      double s = 0.0;
+      // 16-byte loads of the row halves (RowJ rows are 16-byte aligned)
+      auto half_dot = [](const double* a, const double* c) {
+        const double2* a2 = reinterpret_cast<const double2*>(a);
+        const double2* c2 = reinterpret_cast<const double2*>(c);
+        double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) s += a[k] * c[k];
-      if (g.flags & SG_TWO) {
-        const double* a2 = rj[rs].JM + ((g.flags & SG_S2) ? 6 : 0);
-        const double* c2 = rj[rt].J + ((g.flags & SG_T2) ? 6 : 0);
-        double s2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) s2 += a2[k] * c2[k];
-        s += s2;
-      }
+        for (int k = 0; k < 3; ++k) {
+          const double2 x = a2[k], y = c2[k];
+          s += x.x * y.x;
+          s += x.y * y.y;
+        }
+        return s;
+      };
+      double s = half_dot(rj[rs].JM + ((g.flags & SG_S1) ? 6 : 0), rj[rt].J + ((g.flags & SG_T1) ? 6 : 0));
+      if (g.flags & SG_TWO)
+        s += half_dot(rj[rs].JM + ((g.flags & SG_S2) ? 6 : 0), rj[rt].J + ((g.flags & SG_T2) ? 6 : 0));
       if (diag) s += reg[rs];
       double d = (Ps[rs] * s) * Ps[rt];
       if (diag) d += eta_rho;
