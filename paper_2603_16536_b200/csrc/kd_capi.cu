@@ -84,6 +84,7 @@ struct Bin {
   // so K1 never sends one of them here (kd_assemble.cu backend choice): the
   // launch is skipped (an empty 1-CTA-per-world launch still costs ~10 us)
   bool never = false;
+  bool rare = false;  // every world's model is planned: a world lands here only as a fallback
   // the batch's parts (world ranges [cut[p], cut[p+1])): this bin's worlds in each
   int hoff[4] = {0, 0, 0, 0}, hcount[4] = {0, 0, 0, 0};
   void set_parts(const int* cut, int np) {
@@ -152,6 +153,7 @@ struct kd_batch {
   bool sparse = true;
   bool no_df = false;
   bool no_tmem = false;
+  bool slab_sweep_forced = false;
   int sparse_mode = 1;
   bool sn_handoff = true;
   int64_t total_snlv = 0, total_snr2p = 0;
@@ -620,7 +622,15 @@ int kd_batch_create(int32_t device, const kd_model* const* models, int32_t n_mod
     b->dense_bins.push_back(bin);
   }
   b->global_bin.never = true;
-  for (int32_t w : b->global_bin.worlds) b->global_bin.never = b->global_bin.never && always_planned[world_model[w]] != 0;
+  {
+    const char* sw = getenv("KD_SLAB_SWEEP");  // KD_SLAB_SWEEP=1: every slab bin through the sweep kernel (tests)
+    b->global_bin.rare = true;
+    b->slab_sweep_forced = sw && sw[0] == '1';
+  }
+  for (int32_t w : b->global_bin.worlds) {
+    b->global_bin.never = b->global_bin.never && always_planned[world_model[w]] != 0;
+    b->global_bin.rare = b->global_bin.rare && dm[world_model[w]].sn != 0;
+  }
   for (int i = 0; i < n_models; ++i) {
     if (!dm[i].sn) continue;
     kd_batch::SnBin sbn;
@@ -1089,7 +1099,9 @@ static int enqueue_one(kd_batch* b, const kd_step_config* c, const StepParams& s
       {
         const int32_t* wl = part(b->global_bin, cnt);
         if (cnt && !b->global_bin.never) {
-          KD_CK(launch_dense(v, sp, wl, cnt, b->global_bin.cap, 256, true, s));
+          if (b->global_bin.rare || b->slab_sweep_forced)
+            KD_CK(launch_dense_global_sweep(v, sp, wl, cnt, b->global_bin.cap, s));
+          else KD_CK(launch_dense(v, sp, wl, cnt, b->global_bin.cap, 256, true, s));
           ++b->launches;
         }
       }

@@ -1344,10 +1344,10 @@ __device__ void padmm_units_global(const BatchView& bv, const StepParams& sp, in
 template <int NT>
 constexpr int dense_min_blocks() { return NT <= 64 ? KD_DENSE_MINB64 : (NT <= 128 ? KD_DENSE_MINB128 : 1); }
 
+// One world on one CTA (the body of the dense kernels below).
 template <int NT, bool GLOBAL_L>
-__global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
+__device__ __forceinline__ void dense_world(const BatchView& bv, const StepParams& sp, const int w) {
   extern __shared__ __align__(16) double smem[];
-  const int w = bin_worlds[blockIdx.x];
   WorldStep& ws = bv.wstep[w];
   // BE_DENSE_SN: the supernodal kernel already factored D in its plan's order
   // (kd_sparse.cu); this CTA forms L^-1 in that order and runs the solves
@@ -1879,6 +1879,35 @@ __global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(Batch
   }  // !GLOBAL_L
 }
 
+template <int NT, bool GLOBAL_L>
+__global__ void __launch_bounds__(NT, dense_min_blocks<NT>()) dense_kernel(BatchView bv, StepParams sp, const int32_t* bin_worlds) {
+  dense_world<NT, GLOBAL_L>(bv, sp, bin_worlds[blockIdx.x]);
+}
+
+// The HBM-slab bin of planned models is a rare fallback (K1 sends a world
+// there only when an active contact has no planned slot): instead of one
+// mostly empty CTA per world (one CTA per SM at 255 registers, ~15 us per
+// part and step), each CTA tests 256 worlds' backends at once and runs the
+// few that chose the slab one after another.
+__global__ void __launch_bounds__(256, 1) dense_global_sweep(BatchView bv, StepParams sp, const int32_t* bin_worlds,
+                                                             int count) {
+  __shared__ int hits[256];
+  __shared__ int nhit;
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (threadIdx.x == 0) nhit = 0;
+  __syncthreads();
+  if (i < count) {
+    const int w = bin_worlds[i];
+    if (bv.wstep[w].backend == BE_DENSE_GLOBAL) hits[atomicAdd(&nhit, 1)] = w;
+  }
+  __syncthreads();
+  const int m = nhit;
+  for (int k = 0; k < m; ++k) {
+    dense_world<256, true>(bv, sp, hits[k]);
+    __syncthreads();  // the world's shared memory is reused by the next one
+  }
+}
+
 // Shared-memory bytes the dense kernel needs for n rows with NT threads.
 size_t dense_factor_doubles(int n) {
   const int T = (n + 31) / 32;
@@ -1905,6 +1934,19 @@ static cudaError_t launch_t(const BatchView& bv, const StepParams& sp, const int
     if (e != cudaSuccess) return e;
   }
   dense_kernel<NT, G><<<count, NT, smem, s>>>(bv, sp, worlds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_global_sweep(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
+                                     int cap, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const size_t smem = dense_smem_bytes(cap, 256, true);
+  static SmemAttrCache attr;
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(dense_global_sweep), smem, attr);
+    if (e != cudaSuccess) return e;
+  }
+  dense_global_sweep<<<(count + 255) / 256, 256, smem, s>>>(bv, sp, worlds, count);
   return cudaGetLastError();
 }
 

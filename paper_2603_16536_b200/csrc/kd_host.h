@@ -41,6 +41,8 @@ double host_joint_coordinate(const HostModel& m, int joint, const double* poses7
 void launch_assemble(const BatchView& bv, const StepParams& sp, cudaStream_t s, int w0 = 0, int w1 = -1);
 cudaError_t launch_dense(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int cap, int nt,
                   bool global_l, cudaStream_t s);
+cudaError_t launch_dense_global_sweep(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count,
+                                      int cap, cudaStream_t s);
 cudaError_t launch_cr(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap, int nbcap,
                int nt, cudaStream_t s);
 cudaError_t launch_cr_shared(const BatchView& bv, const StepParams& sp, const int32_t* worlds, int count, int ncap,

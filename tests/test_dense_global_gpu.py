@@ -116,3 +116,32 @@ def test_dense_and_matrix_free_agree_above_crossover():
         worst = max(worst, float(np.abs(pd - ps).max()))
     assert gd.kernels() == ["dense"] and gs.kernels() == ["cr"]
     assert worst < 1e-6
+
+
+def test_slab_sweep_kernel_bitwise(monkeypatch):
+    """The sweep kernel (one CTA tests 256 worlds' backends and runs the slab
+    worlds among them in turn; the default for slab bins of planned models,
+    whose worlds land there only as a fallback) gives the per-world slab
+    kernel's results bit for bit (KD_SLAB_SWEEP=1 forces it)."""
+    import numpy as np
+    import paper_2603_16536_b200 as K
+    from paper_2603_16536_b200.scenes import closed_chain
+    sc = closed_chain(12)
+    cfg = K.config_for(sc)
+    res = []
+    for force in ("0", "1"):
+        monkeypatch.setenv("KD_SLAB_SWEEP", force)
+        m = K.build_model(sc)
+        b = K.WorldBatch()
+        for _ in range(300):
+            b.add_world(m)
+        p, t, tm = b.get_state()
+        t = K.bench_jitter(t, [m.n_bodies] * 300, seed=2)
+        b.set_state(p, t, tm)
+        b.step(cfg, 6)
+        p, t, _ = b.get_state()
+        res.append((p, t, [d.iterations for d in b.diagnostics()], b.kernels()))
+    monkeypatch.delenv("KD_SLAB_SWEEP")
+    assert res[0][3] == res[1][3] and "dense" in res[0][3][0]
+    assert res[0][2] == res[1][2]
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
